@@ -1,0 +1,750 @@
+// kvr_oracle.cpp — plain CPU oracle (TEST INFRASTRUCTURE; see kvr_oracle.h).
+//
+// Written from PAPER.md (arxiv 2601.18999) and the readings recorded in
+// DESIGN.md §3 ("Readings of the paper", ids A1..A27 follow SURVEY §8(c)).
+// Deliberately plain: std::unordered_map keyed by the chained block identity,
+// one node per cached block, a linear scan over every cached node for each
+// victim choice, std::deque FIFOs, fp64 arithmetic in the literal operation
+// order (built with -ffp-contract=off -fno-fast-math).  Nothing here is
+// shared with the CUDA path.
+#include "kvr_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <unordered_map>
+#include <unordered_set>
+#include <utility>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Block identity (A1, A26; SURVEY §8(c) "Definitions").  The paper keys its
+// radix tree by token position along the path; a block's
+// identity must therefore encode its whole prefix.  S_d = sum_{e<=d}
+// fmix64(c_e ^ (e+1)*K ^ salt) mod 2^64, H_d = fmix64(S_d).
+// ---------------------------------------------------------------------------
+const uint64_t K_POS = 0x9E3779B97F4A7C15ULL;
+
+uint64_t fmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+// Philox4x32-10 (Salmon et al. 2011, Random123; constants as in curand's
+// curand_philox4x32_x.h).  Counter-based: the RLT draw of worker i uses
+// counter (e_i, i, tag 1), the RANDOM router counter (j, 0xFFFFFFFF, tag 2).
+void philox(const uint32_t cin[4], const uint32_t kin[2], uint32_t out[4]) {
+  uint32_t c0 = cin[0], c1 = cin[1], c2 = cin[2], c3 = cin[3];
+  uint32_t k0 = kin[0], k1 = kin[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+uint64_t philox_r64(uint64_t key, uint64_t n, uint32_t stream, uint32_t tag) {
+  uint32_t c[4] = {(uint32_t)n, (uint32_t)(n >> 32), stream, tag};
+  uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  uint32_t o[4];
+  philox(c, k, o);
+  return (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+}
+
+// uniform index in [0, m): floor(r * m / 2^64)  (A6)
+uint64_t pick(uint64_t r, uint64_t m) {
+  return (uint64_t)(((unsigned __int128)r * (unsigned __int128)m) >> 64);
+}
+
+int validate_trace(const kvro_trace* tr) {
+  if (!tr || tr->block_tokens == 0) return 1;
+  if (tr->n_queries && (!tr->arrival_ms || !tr->n_in_blocks || !tr->n_out_blocks ||
+                        !tr->out_tokens || !tr->block_offsets || !tr->block_keys))
+    return 1;
+  if (tr->n_queries && !tr->block_offsets) return 1;
+  if (tr->block_offsets && tr->block_offsets[0] != 0) return 1;
+  double prev = 0.0;
+  for (uint32_t j = 0; j < tr->n_queries; ++j) {
+    if (tr->n_in_blocks[j] < 1) return 1;
+    uint64_t n = (uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j];
+    if (tr->block_offsets[j + 1] - tr->block_offsets[j] != n) return 1;
+    double a = tr->arrival_ms[j];
+    if (!std::isfinite(a) || a < 0.0 || a < prev) return 1;
+    prev = a;
+  }
+  return 0;
+}
+
+std::vector<uint64_t> chain_all(const kvro_trace* tr) {
+  uint64_t total = tr->n_queries ? tr->block_offsets[tr->n_queries] : 0;
+  std::vector<uint64_t> H(total);
+  for (uint32_t j = 0; j < tr->n_queries; ++j) {
+    uint64_t S = 0;
+    uint64_t o = tr->block_offsets[j];
+    uint64_t n = tr->block_offsets[j + 1] - o;
+    for (uint64_t d = 0; d < n; ++d) {
+      S += fmix64(tr->block_keys[o + d] ^ ((d + 1) * K_POS) ^ tr->hash_salt);
+      H[o + d] = fmix64(S);
+    }
+  }
+  return H;
+}
+
+// ---------------------------------------------------------------------------
+// One worker's cache S_i (Eq. 3): a prefix tree of blocks.
+// ---------------------------------------------------------------------------
+struct Node {
+  uint64_t parent;     // identity of the parent block (valid iff has_parent)
+  bool has_parent;     // false: child of the root
+  uint32_t nchild;     // number of cached children
+  uint32_t slot;       // physical slot (A6 slot rule)
+  uint64_t stamp;      // index j of the last query that touched it (A7)
+  uint32_t depth;      // position along the path, 1-based
+};
+
+struct Cache {
+  uint32_t B = 0;
+  std::unordered_map<uint64_t, Node> S;   // cache state S_i
+  std::unordered_set<uint64_t> T;         // RLT marking set (Alg. 1 l.1)
+};
+
+struct UpdateCtx {
+  uint32_t eviction = KVRO_EVICT_LRU;
+  uint32_t fallback = KVRO_RLT_EARLY_RESET;
+  uint64_t j = 0;                                      // stamp of this query
+  std::function<uint64_t(uint64_t)> choose;            // uniform index in [0, n)
+  std::function<std::pair<uint64_t, uint32_t>(uint64_t)> next_use;  // OPT only
+  uint64_t hits = 0, inserted = 0, evictions = 0, draws = 0, resets = 0, fallbacks = 0;
+  std::vector<uint64_t> victims;
+  std::vector<uint8_t>* miss_flags = nullptr;
+  bool invariant_violation = false;
+};
+
+// (stamp, -depth) order of Leaf-LRU (A7): true if a is less recently used.
+bool lru_less(const Node& a, const Node& b) {
+  if (a.stamp != b.stamp) return a.stamp < b.stamp;
+  return a.depth > b.depth;
+}
+
+// UpdateCache(S_i, Gamma_j, B_i) — Eq. 3 with Alg. 1 (RLT) or
+// Leaf-LRU, block by block in path order.
+void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
+  for (uint32_t d = 0; d < n; ++d) {
+    const uint64_t t = H[d];
+    const bool has_p = d > 0;
+    const uint64_t p = has_p ? H[d - 1] : 0;
+    // Alg. 1 l.6-9: mark t; the (B+1)-th distinct marked token resets T to {t}.
+    if (x.eviction == KVRO_EVICT_RLT) {
+      if (!C.T.count(t)) {
+        if (C.T.size() + 1 == (size_t)C.B + 1) {
+          C.T.clear();
+          C.T.insert(t);
+          x.resets++;
+        } else {
+          C.T.insert(t);
+        }
+      }
+    }
+    // Alg. 1 l.10-11: hit
+    auto it = C.S.find(t);
+    if (it != C.S.end()) {
+      it->second.stamp = x.j;
+      x.hits++;
+      if (x.miss_flags) x.miss_flags->push_back(0);
+      continue;
+    }
+    if (x.miss_flags) x.miss_flags->push_back(1);
+    uint32_t slot;
+    if (C.S.size() == C.B) {
+      // Alg. 1 l.13-16 / Leaf-LRU: choose the victim v
+      uint64_t v = 0;
+      bool found = false;
+      if (x.eviction == KVRO_EVICT_LRU) {
+        // least recently used node among those not touched by this query;
+        // always a leaf and never on Gamma_j (A7).
+        const Node* best = nullptr;
+        for (auto& kv : C.S) {
+          if (kv.second.stamp >= x.j) continue;
+          if (!best || lru_less(kv.second, *best)) { best = &kv.second; v = kv.first; found = true; }
+        }
+        if (found && C.S[v].nchild != 0) x.invariant_violation = true;
+      } else if (x.eviction == KVRO_EVICT_RLT) {
+        // U = leaf tokens \ T, excluding parent(t) (A4)
+        std::vector<std::pair<uint32_t, uint64_t>> U;  // (slot, id)
+        for (auto& kv : C.S) {
+          if (kv.second.nchild != 0) continue;
+          if (has_p && kv.first == p) continue;
+          if (C.T.count(kv.first)) continue;
+          U.push_back({kv.second.slot, kv.first});
+        }
+        bool no_draw = false;
+        if (U.empty()) {
+          // A5: Alg. 1 leaves U = {} undefined
+          x.fallbacks++;
+          if (x.fallback == KVRO_RLT_EARLY_RESET) {
+            C.T.clear();
+            C.T.insert(t);
+            x.resets++;
+          }
+          if (x.fallback == KVRO_RLT_LRU_MARKED) {
+            const Node* best = nullptr;
+            for (auto& kv : C.S) {
+              if (kv.second.nchild != 0) continue;
+              if (has_p && kv.first == p) continue;
+              if (!best || lru_less(kv.second, *best)) { best = &kv.second; v = kv.first; found = true; }
+            }
+            no_draw = true;
+          } else {
+            for (auto& kv : C.S) {
+              if (kv.second.nchild != 0) continue;
+              if (has_p && kv.first == p) continue;
+              U.push_back({kv.second.slot, kv.first});
+            }
+          }
+        }
+        if (!no_draw) {
+          // Alg. 1 l.15: uniform over U, U ordered by physical slot (A6)
+          std::sort(U.begin(), U.end());
+          if (!U.empty()) {
+            uint64_t idx = x.choose(U.size());
+            if (idx >= U.size()) idx = U.size() - 1;
+            v = U[idx].second;
+            found = true;
+            x.draws++;
+          }
+        }
+      } else {  // OPT (Belady on leaves): furthest next use; ties -> lowest slot
+        const Node* best = nullptr;
+        std::pair<uint64_t, uint32_t> bnu{0, 0};
+        for (auto& kv : C.S) {
+          if (kv.second.nchild != 0) continue;
+          if (has_p && kv.first == p) continue;
+          auto nu = x.next_use(kv.first);
+          bool better;
+          if (!best) better = true;
+          else if (nu.first != bnu.first) better = nu.first > bnu.first;
+          else if (nu.first == UINT64_MAX) better = kv.second.slot < best->slot;
+          else better = nu.second > bnu.second;
+          if (better) { best = &kv.second; bnu = nu; v = kv.first; found = true; }
+        }
+      }
+      if (!found) { x.invariant_violation = true; return; }
+      // Evict(S, v)
+      Node nv = C.S[v];
+      if (nv.nchild != 0) x.invariant_violation = true;
+      slot = nv.slot;
+      if (nv.has_parent) C.S[nv.parent].nchild--;
+      C.T.erase(v);
+      C.S.erase(v);
+      x.victims.push_back(v);
+      x.evictions++;
+    } else {
+      slot = (uint32_t)C.S.size();
+    }
+    // Load(S, t)
+    Node nn;
+    nn.parent = p; nn.has_parent = has_p; nn.nchild = 0; nn.slot = slot;
+    nn.stamp = x.j; nn.depth = d + 1;
+    C.S[t] = nn;
+    if (has_p) C.S[p].nchild++;
+    x.inserted++;
+  }
+}
+
+// longest m <= n_in with H[0..m-1] all in S
+uint32_t match_prefix(const Cache& C, const uint64_t* H, uint32_t n_in) {
+  uint32_t m = 0;
+  while (m < n_in && C.S.count(H[m])) ++m;
+  return m;
+}
+
+bool check_cache(const Cache& C) {
+  if (C.S.size() > C.B) return false;
+  if (C.T.size() > C.B) return false;
+  std::unordered_map<uint64_t, uint32_t> kids;
+  std::vector<int> slot_used(C.B, 0);
+  for (auto& kv : C.S) {
+    if (kv.second.slot >= C.B) return false;
+    if (slot_used[kv.second.slot]++) return false;
+    if (kv.second.has_parent) {
+      auto it = C.S.find(kv.second.parent);
+      if (it == C.S.end()) return false;                       // prefix closure
+      if (it->second.depth + 1 != kv.second.depth) return false;
+      kids[kv.second.parent]++;
+    } else if (kv.second.depth != 1) {
+      return false;
+    }
+  }
+  for (auto& kv : C.S)
+    if (kv.second.nchild != kids[kv.first]) return false;
+  for (uint64_t t : C.T)
+    if (!C.S.count(t)) return false;                           // T subset of S
+  return true;
+}
+
+uint64_t cache_fingerprint(const Cache& C) {
+  uint64_t f = C.S.size() * 0x100000001B3ULL;
+  for (auto& kv : C.S) f += fmix64(kv.first ^ ((uint64_t)kv.second.slot << 1) ^ (kv.second.stamp * 31));
+  for (uint64_t t : C.T) f += fmix64(t + 7);
+  return f;
+}
+
+// log-bucket histogram bin (exact bit rule, 4 bins per octave): 0 for lat < 1 ms
+uint32_t hist_bin(double lat, uint32_t bins) {
+  if (!(lat >= 1.0)) return 0;
+  int e;
+  double f = std::frexp(lat, &e);   // lat = f * 2^e, f in [0.5, 1)
+  uint32_t q = (uint32_t)((f * 2.0 - 1.0) * 4.0);
+  uint64_t b = 1 + 4 * (uint64_t)(e - 1) + q;
+  return b >= bins ? bins - 1 : (uint32_t)b;
+}
+
+struct Rec {  // one pending completion (A12)
+  double c, a, Ehat, phi0, phi1, phi2, Chat;
+  uint64_t ka;
+};
+
+struct Worker {
+  Cache cache;
+  double P = 0.0, F = 0.0, Pt = 0.0;
+  double th[4] = {0, 0, 0, 0};
+  std::deque<Rec> fifo;
+  uint64_t k = 0, e = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+uint32_t kvro_version(void) { return 1; }
+uint64_t kvro_fmix64(uint64_t x) { return fmix64(x); }
+void kvro_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) { philox(ctr, key, out); }
+
+int kvro_chain(const kvro_trace* tr, uint64_t* out) {
+  if (validate_trace(tr) || !out) return 1;
+  std::vector<uint64_t> H = chain_all(tr);
+  if (!H.empty()) std::memcpy(out, H.data(), H.size() * sizeof(uint64_t));
+  return 0;
+}
+
+int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* pol,
+             uint64_t K, kvro_result* out, kvro_query_record* records,
+             uint64_t* victims, uint64_t victims_cap, uint32_t* hist, int check_invariants) {
+  if (!cfg || !pol || !out) return 1;
+  if (validate_trace(tr)) return 1;
+  const uint32_t W = cfg->W, B = cfg->capacity_blocks;
+  if (W < 1 || W > 32 || B < 1 || B > 65536) return 1;
+  if (pol->eviction > KVRO_EVICT_RLT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
+      pol->router > KVRO_ROUTE_RANDOM)
+    return 1;
+  if (!(pol->rho > 0.0 && pol->rho <= 1.0) || !(pol->delta_t_ms > 0.0)) return 1;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)       // P:197 with beta = 1
+    if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
+
+  std::memset(out, 0, sizeof(*out));
+  if (hist) std::memset(hist, 0, sizeof(uint32_t) * cfg->latency_hist_bins);
+  const std::vector<uint64_t> H = chain_all(tr);
+  std::vector<Worker> w(W);
+  for (auto& x : w) {
+    x.cache.B = B;
+    for (int k = 0; k < 4; ++k) x.th[k] = pol->theta0[k];
+  }
+  const bool lbgr = pol->router == KVRO_ROUTE_LBGR;
+  const double rho = pol->rho, dt = pol->delta_t_ms, mu = pol->mu;
+  uint64_t D = K;
+  uint64_t vcursor = 0;
+  bool vlog_full = false;
+  std::vector<uint32_t> m(W);
+  std::vector<double> Ehat(W), Chat(W), phi0(W), phi1(W), phi2(W);
+
+  for (uint32_t j = 0; j < tr->n_queries; ++j) {
+    const double t = tr->arrival_ms[j];
+    const uint32_t n_in = tr->n_in_blocks[j], n_out = tr->n_out_blocks[j];
+    const uint32_t q = tr->block_tokens * n_in;                   // |q_j| (A1)
+    const uint64_t* Hj = H.data() + tr->block_offsets[j];
+
+    // 1. catch-up: decay ticks (Alg. 2 l.17) merged with completions
+    //    (Alg. 2 l.11-14); tick before completion before routing (A11)
+    for (uint32_t i = 0; i < W; ++i) {
+      Worker& x = w[i];
+      for (;;) {
+        if (lbgr) {
+          double tau = (double)(x.k + 1) * dt;
+          bool has = !x.fifo.empty();
+          if (tau <= t && (!has || tau <= x.fifo.front().c)) {
+            x.Pt = rho * x.Pt;
+            x.k++;
+            continue;
+          }
+        }
+        if (!x.fifo.empty() && x.fifo.front().c <= t) {
+          Rec r = x.fifo.front();
+          x.fifo.pop_front();
+          if (lbgr) {
+            // OnlineUpdate: NLMS step on the squared residual (A8)
+            double E = r.c - r.a;
+            double res = E - r.Ehat;
+            double phi3 = 1.0;
+            double s = r.phi0 * r.phi0;
+            s = s + r.phi1 * r.phi1;
+            s = s + r.phi2 * r.phi2;
+            s = s + phi3 * phi3;
+            double g = (mu * res) / (1.0 + s);
+            x.th[0] = x.th[0] + g * r.phi0;
+            x.th[1] = x.th[1] + g * r.phi1;
+            x.th[2] = x.th[2] + g * r.phi2;
+            x.th[3] = x.th[3] + g * phi3;
+            // ReleaseLoad: remove the decayed remainder rho^kappa * Chat (A10)
+            uint64_t kap = x.k - r.ka;
+            double pw = 1.0, b = rho;
+            while (kap) {
+              if (kap & 1) pw = pw * b;
+              b = b * b;
+              kap >>= 1;
+            }
+            x.Pt = x.Pt - r.Chat * pw;
+            if (x.Pt < 0.0) x.Pt = 0.0;
+          }
+          continue;
+        }
+        break;
+      }
+    }
+
+    // 2. longest cached prefix on every worker (h_ij)
+    for (uint32_t i = 0; i < W; ++i) {
+      m[i] = match_prefix(w[i].cache, Hj, n_in);
+      out->probes += std::min<uint64_t>(m[i] + 1, n_in);
+    }
+
+    // 3. score + argmin (lowest index on ties, A15)
+    uint32_t best = 0;
+    double score_best = 0.0;
+    if (pol->router == KVRO_ROUTE_LBGR) {
+      for (uint32_t i = 0; i < W; ++i) {
+        double x = (double)(tr->block_tokens * m[i]);
+        double y = (double)(q - tr->block_tokens * m[i]);
+        double C = (pol->est_alpha_cached_ms * x) + (pol->est_alpha_miss_ms * y);   // Eq. 5
+        double f0 = x / 1000.0, f1 = y / 1000.0, f2 = w[i].Pt / 1000.0, f3 = 1.0;  // A9
+        double d = w[i].th[0] * f0;
+        d = d + w[i].th[1] * f1;
+        d = d + w[i].th[2] * f2;
+        d = d + w[i].th[3] * f3;
+        Ehat[i] = (C + w[i].Pt) + d;                                               // Eq. 4
+        Chat[i] = C; phi0[i] = f0; phi1[i] = f1; phi2[i] = f2;
+      }
+      for (uint32_t i = 1; i < W; ++i)
+        if (Ehat[i] < Ehat[best]) best = i;
+      score_best = Ehat[best];
+    } else if (pol->router == KVRO_ROUTE_STATIC_LINEAR) {   // A17
+      double bs = 0.0;
+      for (uint32_t i = 0; i < W; ++i) {
+        double x = (double)(tr->block_tokens * m[i]);
+        double s = (pol->w_load * (double)w[i].fifo.size()) - (pol->w_hit * (x / (double)q));
+        if (i == 0 || s < bs) { bs = s; best = i; }
+      }
+      score_best = bs;
+    } else if (pol->router == KVRO_ROUTE_THRESHOLD) {       // A16
+      size_t mx = w[0].fifo.size(), mn = w[0].fifo.size();
+      for (uint32_t i = 1; i < W; ++i) {
+        mx = std::max(mx, w[i].fifo.size());
+        mn = std::min(mn, w[i].fifo.size());
+      }
+      if ((double)mx > pol->tau * (double)std::max<size_t>(1, mn)) {
+        for (uint32_t i = 1; i < W; ++i)
+          if (w[i].fifo.size() < w[best].fifo.size()) best = i;
+      } else {
+        for (uint32_t i = 1; i < W; ++i)
+          if (m[i] > m[best]) best = i;
+      }
+    } else if (pol->router == KVRO_ROUTE_ROUND_ROBIN) {
+      best = j % W;
+    } else {  // RANDOM
+      best = (uint32_t)pick(philox_r64(K, j, 0xFFFFFFFFu, 2), W);
+    }
+    Worker& xs = w[best];
+
+    if (cfg->pending_ring && xs.fifo.size() >= cfg->pending_ring) {
+      out->status = KVRO_TRIAL_RING_OVERFLOW;
+      break;
+    }
+    uint64_t fp_before = 0;
+    if (check_invariants)
+      for (uint32_t i = 0; i < W; ++i)
+        if (i != best) fp_before += cache_fingerprint(w[i].cache) * (i + 1);
+
+    // 4. UpdateCache on i* only (Eq. 3)
+    UpdateCtx ux;
+    ux.eviction = pol->eviction;
+    ux.fallback = pol->rlt_fallback;
+    ux.j = j;
+    ux.choose = [&](uint64_t nU) -> uint64_t {
+      uint64_t r = philox_r64(K, xs.e, best, 1);
+      xs.e++;
+      return pick(r, nU);
+    };
+    update_cache(xs.cache, Hj, n_in + n_out, ux);
+    if (ux.invariant_violation) return 9;
+    out->inserted_blocks += ux.inserted;
+    out->evictions += ux.evictions;
+    out->rlt_draws += ux.draws;
+    out->rlt_resets += ux.resets;
+    out->rlt_fallbacks += ux.fallbacks;
+
+    // 5. accounting: Eq. 1-2 truth, FIFO single server (A12-A14, A20)
+    const uint32_t h = tr->block_tokens * m[best];
+    const double x = (double)h, y = (double)(q - h);
+    const double pre = (cfg->alpha_cached_ms * x) + (cfg->alpha_miss_ms * y);
+    const double O = cfg->out_ms_per_token * (double)tr->out_tokens[j];
+    const double cost = pre + O;
+    const double start = (t >= xs.F) ? t : xs.F;
+    const double ttft = (start + pre) - t;
+    const double comp = start + cost;
+    const double lat = comp - t;
+    xs.F = comp;
+    xs.P = xs.P + cost;
+    Rec r;
+    r.c = comp; r.a = t;
+    r.Ehat = lbgr ? Ehat[best] : 0.0;
+    r.phi0 = lbgr ? phi0[best] : 0.0;
+    r.phi1 = lbgr ? phi1[best] : 0.0;
+    r.phi2 = lbgr ? phi2[best] : 0.0;
+    r.Chat = lbgr ? Chat[best] : 0.0;
+    r.ka = xs.k;
+    xs.fifo.push_back(r);
+    if (xs.fifo.size() > out->max_pending) out->max_pending = xs.fifo.size();
+    if (lbgr) xs.Pt = xs.Pt + Chat[best];                                     // Eq. 6
+    out->hit_tokens += h;
+    out->input_tokens += q;
+    out->sum_latency_ms = out->sum_latency_ms + lat;
+    out->sum_ttft_ms = out->sum_ttft_ms + ttft;
+    if (lat > out->max_latency_ms) out->max_latency_ms = lat;
+    out->queries++;
+
+    // 6. decision digest
+    D = fmix64(D ^ (uint64_t)j);
+    D = fmix64(D ^ (uint64_t)best);
+    D = fmix64(D ^ (uint64_t)m[best]);
+    for (uint64_t v : ux.victims) D = fmix64(D ^ v);
+    D = fmix64(D ^ (uint64_t)ux.victims.size());
+
+    if (records) {
+      kvro_query_record& R = records[j];
+      R.worker = best; R.hit_tokens = h; R.n_victims = (uint32_t)ux.victims.size(); R._pad = 0;
+      R.ttft_ms = ttft; R.latency_ms = lat; R.score = score_best; R.victim_offset = vcursor;
+      for (uint64_t v : ux.victims) {
+        if (victims && vcursor < victims_cap) victims[vcursor] = v;
+        else if (victims) vlog_full = true;
+        vcursor++;
+      }
+    }
+    if (hist && cfg->latency_hist_bins) hist[hist_bin(lat, cfg->latency_hist_bins)]++;
+
+    if (check_invariants) {
+      for (uint32_t i = 0; i < W; ++i)
+        if (!check_cache(w[i].cache)) return 9;
+      uint64_t fp_after = 0;
+      for (uint32_t i = 0; i < W; ++i)
+        if (i != best) fp_after += cache_fingerprint(w[i].cache) * (i + 1);
+      if (fp_after != fp_before) return 9;                // Eq. 3: others unchanged
+      if (m[best] > n_in || ux.hits + ux.inserted != (uint64_t)n_in + n_out) return 9;
+      for (uint32_t i = 0; i < W; ++i)
+        if (w[i].Pt < 0.0) return 9;
+      if (ttft > lat && cfg->out_ms_per_token >= 0.0) return 9;
+    }
+  }
+
+  // end of trial: makespan max_i P_i (A21), last completion, sum of loads
+  for (uint32_t i = 0; i < W; ++i) {
+    if (w[i].P > out->makespan_ms) out->makespan_ms = w[i].P;
+    if (w[i].F > out->last_completion_ms) out->last_completion_ms = w[i].F;
+    out->sum_load_ms = out->sum_load_ms + w[i].P;
+  }
+  out->decision_digest = D;
+  if (out->status == 0 && vlog_full) out->status = KVRO_TRIAL_VICTIM_LOG_FULL;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Single-cache analysis tools (W = 1; §3.2, App. C).  Arrivals and costs are
+// ignored: only the eviction process over the flattened block sequence.
+// ---------------------------------------------------------------------------
+int kvro_single_replay(const kvro_trace* tr, uint32_t B, uint32_t eviction, uint32_t fallback,
+                       uint64_t K, uint8_t* miss_flags, uint64_t* total_misses,
+                       const uint32_t* choices, uint32_t* arity, uint32_t max_draws,
+                       uint32_t* n_draws) {
+  if (validate_trace(tr) || B < 1 || eviction > KVRO_EVICT_OPT || fallback > KVRO_RLT_LRU_MARKED)
+    return 1;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
+  const std::vector<uint64_t> H = chain_all(tr);
+  // next-use index for OPT: identity -> ascending list of query indices
+  std::unordered_map<uint64_t, std::vector<uint64_t>> occ;
+  std::unordered_map<uint64_t, uint32_t> depth_of;
+  if (eviction == KVRO_EVICT_OPT) {
+    for (uint32_t j = 0; j < tr->n_queries; ++j)
+      for (uint64_t o = tr->block_offsets[j]; o < tr->block_offsets[j + 1]; ++o) {
+        occ[H[o]].push_back(j);
+        depth_of[H[o]] = (uint32_t)(o - tr->block_offsets[j]) + 1;
+      }
+  }
+  Cache C;
+  C.B = B;
+  std::vector<uint8_t> flags;
+  uint64_t e = 0, misses = 0;
+  uint32_t draw_idx = 0;
+  bool overflow = false;
+  for (uint32_t j = 0; j < tr->n_queries; ++j) {
+    UpdateCtx ux;
+    ux.eviction = eviction;
+    ux.fallback = fallback;
+    ux.j = j;
+    ux.miss_flags = &flags;
+    ux.choose = [&](uint64_t nU) -> uint64_t {
+      uint64_t idx;
+      if (choices) {
+        idx = draw_idx < max_draws ? choices[draw_idx] : 0;
+        if (idx >= nU) idx = nU - 1;
+      } else {
+        idx = pick(philox_r64(K, e, 0, 1), nU);
+      }
+      if (arity) {
+        if (draw_idx < max_draws) arity[draw_idx] = (uint32_t)nU;
+        else overflow = true;
+      }
+      draw_idx++;
+      e++;
+      return idx;
+    };
+    const uint64_t jj = j;
+    ux.next_use = [&](uint64_t id) -> std::pair<uint64_t, uint32_t> {
+      const std::vector<uint64_t>& v = occ[id];
+      auto it = std::upper_bound(v.begin(), v.end(), jj);
+      if (it == v.end()) return {UINT64_MAX, 0};
+      return {*it, depth_of[id]};
+    };
+    uint64_t n = tr->block_offsets[j + 1] - tr->block_offsets[j];
+    update_cache(C, H.data() + tr->block_offsets[j], (uint32_t)n, ux);
+    if (ux.invariant_violation) return 9;
+    misses += ux.inserted;
+  }
+  if (miss_flags && !flags.empty()) std::memcpy(miss_flags, flags.data(), flags.size());
+  if (total_misses) *total_misses = misses;
+  if (n_draws) *n_draws = draw_idx;
+  return overflow ? 4 : 0;
+}
+
+namespace {
+struct BF {
+  uint32_t B;
+  std::vector<uint64_t> acc;      // flattened accesses
+  std::vector<uint64_t> par;      // parent identity of each access (0 + flag)
+  std::vector<uint8_t> has_par;
+  std::unordered_map<uint64_t, uint64_t> parent_of;
+  std::map<std::pair<size_t, std::vector<uint64_t>>, uint64_t> memo;
+
+  uint64_t solve(size_t pos, std::vector<uint64_t>& cached) {   // cached kept sorted
+    if (pos == acc.size()) return 0;
+    auto key = std::make_pair(pos, cached);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    const uint64_t t = acc[pos];
+    uint64_t res;
+    if (std::binary_search(cached.begin(), cached.end(), t)) {
+      res = solve(pos + 1, cached);
+    } else if (cached.size() < B) {
+      std::vector<uint64_t> nx = cached;
+      nx.insert(std::upper_bound(nx.begin(), nx.end(), t), t);
+      res = 1 + solve(pos + 1, nx);
+    } else {
+      res = UINT64_MAX;
+      for (uint64_t u : cached) {
+        if (has_par[pos] && u == par[pos]) continue;
+        bool leaf = true;   // no cached child
+        for (uint64_t c : cached) {
+          auto pi = parent_of.find(c);
+          if (pi != parent_of.end() && pi->second == u) { leaf = false; break; }
+        }
+        if (!leaf) continue;
+        std::vector<uint64_t> nx;
+        for (uint64_t c : cached) if (c != u) nx.push_back(c);
+        nx.insert(std::upper_bound(nx.begin(), nx.end(), t), t);
+        uint64_t r = solve(pos + 1, nx);
+        if (r != UINT64_MAX && 1 + r < res) res = 1 + r;
+      }
+    }
+    memo[key] = res;
+    return res;
+  }
+};
+}  // namespace
+
+int kvro_bruteforce_min_misses(const kvro_trace* tr, uint32_t B, uint64_t* min_misses) {
+  if (validate_trace(tr) || B < 1 || !min_misses) return 1;
+  uint64_t total = tr->n_queries ? tr->block_offsets[tr->n_queries] : 0;
+  if (B > 6 || total > 48) return 3;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
+  const std::vector<uint64_t> H = chain_all(tr);
+  BF bf;
+  bf.B = B;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    for (uint64_t o = tr->block_offsets[j]; o < tr->block_offsets[j + 1]; ++o) {
+      bool hp = o > tr->block_offsets[j];
+      bf.acc.push_back(H[o]);
+      bf.has_par.push_back(hp);
+      bf.par.push_back(hp ? H[o - 1] : 0);
+      if (hp) bf.parent_of[H[o]] = H[o - 1];
+    }
+  std::vector<uint64_t> empty;
+  *min_misses = bf.solve(0, empty);
+  return 0;
+}
+
+int kvro_rlt_exact_expectation(const kvro_trace* tr, uint32_t B, uint32_t fallback,
+                               double* mean, double* second_moment, uint64_t* leaves) {
+  if (!mean || !second_moment) return 1;
+  const uint32_t MAXD = 4096;
+  std::vector<uint32_t> choice(MAXD, 0), arity(MAXD, 0);
+  double m1 = 0.0, m2 = 0.0;
+  uint64_t nleaves = 0;
+  for (;;) {
+    uint64_t misses = 0;
+    uint32_t nd = 0;
+    int rc = kvro_single_replay(tr, B, KVRO_EVICT_RLT, fallback, 0, nullptr, &misses,
+                                choice.data(), arity.data(), MAXD, &nd);
+    if (rc) return rc;
+    double p = 1.0;
+    for (uint32_t k = 0; k < nd; ++k) p = p / (double)arity[k];
+    m1 += p * (double)misses;
+    m2 += p * (double)misses * (double)misses;
+    if (++nleaves > 20000000ULL) return 3;
+    // odometer over the decision tree (later arities depend on earlier choices)
+    int k = (int)nd - 1;
+    while (k >= 0 && choice[k] + 1 >= arity[k]) --k;
+    if (k < 0) break;
+    choice[k]++;
+    for (uint32_t r = k + 1; r < MAXD; ++r) choice[r] = 0;
+  }
+  *mean = m1;
+  *second_moment = m2;
+  if (leaves) *leaves = nleaves;
+  return 0;
+}
+
+}  // extern "C"
