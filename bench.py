@@ -1,0 +1,354 @@
+#!/usr/bin/env python3
+"""Benchmark: simulated queries/sec of the replay engine (BASELINE.json metric).
+
+One step = one kvr_sim_run_multi launch over the whole workload of this rank:
+config 2 of BASELINE.json (W=8 workers, B=512 blocks, three 100k-query GSP traces
+with low / medium / high shared-prefix ratio 0.3/0.5/0.9, LBGR routing, RLT vs
+Leaf-LRU eviction) with 1,024 replays per GPU (weak scaling: every rank runs its
+own 1,024 trials; trial keys differ per rank).  Unit of work: one query in one
+replay ("query-replay").
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl kvr|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle (the
+tier's reference arm) on host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2601_18999_b200 import workloads as wl  # noqa: E402
+
+W_WORKERS, B_BLOCKS = 8, 512
+RATIOS = (0.3, 0.5, 0.9)
+N_QUERIES = 100_000
+TRIALS_PER_GPU = 1024
+GSP_GROUPS, GSP_PER_GROUP = 125, 800           # 125 x 800 = 100k queries per trace
+GSP_LENGTHS = (128, 256, 512, 1024, 2048)      # paper's {512..8192} tokens / 4
+UTIL = 0.5                                     # all-miss utilisation of the Poisson arrivals
+RING = 4096                                    # pending-completion FIFO per worker
+TRACE_SEEDS = (0xC2, 0xC3, 0xC4)
+METRIC = "simulated queries/sec (all replays)"
+UNIT = "query-replays/s"
+
+
+def build_traces(n_queries=N_QUERIES):
+    trs = []
+    for r, s in zip(RATIOS, TRACE_SEEDS):
+        per = max(1, n_queries // GSP_GROUPS)
+        trs.append(wl.gsp(GSP_GROUPS, per, r, seed=s, W=W_WORKERS, util=UTIL, lengths=GSP_LENGTHS))
+    return trs
+
+
+def trial_plan(rank, n_trials=TRIALS_PER_GPU):
+    """trial t -> trace t mod 3, eviction RLT for even (t div 3), LRU for odd; keys unique per rank."""
+    t = np.arange(n_trials)
+    trace_of = (t % len(RATIOS)).astype(np.uint32)
+    evict = ((t // len(RATIOS)) % 2 == 0).astype(np.uint32)     # 1 = RLT, 0 = LRU
+    keys = (np.uint64(rank) * np.uint64(1 << 32) + t.astype(np.uint64) + np.uint64(1))
+    return trace_of, evict, keys
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace('.', '', 1).isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace('.', '', 1).isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def algorithmic_bytes(res):
+    """SURVEY §8(d) / DESIGN.md §6: algorithmic shared-memory bytes (probe 10 B, insert 22 B,
+    evict 14 B) and trace bytes (8 B per block + 24 B per query) of a set of trial results."""
+    probes = float(res["probes"].sum())
+    ins = float(res["inserted_blocks"].sum())
+    ev = float(res["evictions"].sum())
+    smem = 10.0 * probes + 22.0 * ins + 14.0 * ev
+    return smem
+
+
+def trace_bytes(traces, trace_of):
+    per = np.array([8.0 * t.total_blocks + 24.0 * t.n_queries for t in traces])
+    return float(per[trace_of].sum())
+
+
+def peaks():
+    p = {"hbm_gbs": 6452.8, "sm_max_mhz": 1965.0, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({"hbm_gbs": float(m["hbm_gbs"]), "sm_max_mhz": float(m["sm_max_mhz"]),
+                  "src": "measured"})
+    except Exception:
+        pass
+    return p
+
+
+def run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads):
+    """CPU oracle (as it stands) on host cores: `threads` trials, each on the first
+    n_prefix queries of its trace.  Returns (query-replays, seconds, threads)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    cfg = oracle.OracleConfig(W=W_WORKERS, capacity_blocks=B_BLOCKS, pending_ring=RING)
+    prefixes = [t.prefix(n_prefix) for t in traces]
+
+    def one(i):
+        pol = oracle.OraclePolicy(eviction=int(evict[i]))
+        r = oracle.run(cfg, prefixes[int(trace_of[i])], pol, int(keys[i]))
+        return r.result["queries"]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:   # ctypes releases the GIL
+        q = sum(ex.map(one, range(threads)))
+    return q, time.perf_counter() - t0
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build_oracle()
+    traces = build_traces()
+    trace_of, evict, keys = trial_plan(0)
+    threads = max(1, min(os.cpu_count() or 1, 16))
+    n_prefix = args.ref_queries
+    for _ in range(args.warmup):
+        run_oracle_sample(traces, trace_of, evict, keys, max(50, n_prefix // 10), threads)
+    tot_q, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        q, s = run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads)
+        tot_q += q
+        tot_s += s
+    v = tot_q / tot_s
+    sample = (f"{threads} oracle trials x first {n_prefix} queries of the config-2 traces "
+              f"per step (W=8, B=512, LBGR, RLT/LRU)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_json(args),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(args):
+    return {"workload": "config2: W=8, B=512 blocks, 3 GSP traces (125 groups x 800 queries, "
+                        "128-2048 tokens, prefix ratio 0.3/0.5/0.9), LBGR x {RLT, L-LRU}",
+            "replays_per_gpu": TRIALS_PER_GPU, "queries_per_trace": N_QUERIES,
+            "block_tokens": 16, "parallelism": f"replica-sharded x{args.gpus}",
+            "l2": "inputs larger than L2 (3 packed traces ~250 MB) + 256 MB L2 flush between steps"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kvr", choices=["kvr", "reference"])
+    ap.add_argument("--ref-queries", type=int, default=1500)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--queries", type=int, default=N_QUERIES, help=argparse.SUPPRESS)
+    ap.add_argument("--trials", type=int, default=TRIALS_PER_GPU, help=argparse.SUPPRESS)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2601_18999_b200.kvr import DeviceTrace, Policy, Simulator, policies_array
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    traces = build_traces(args.queries)
+    trace_of, evict, keys = trial_plan(rank, args.trials)
+    n_trials = len(keys)
+    pols = policies_array([Policy(eviction=int(e)) for e in evict])
+    stream = torch.cuda.current_stream()
+    dts = [DeviceTrace(t, device=dev) for t in traces]
+    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING)
+    buf = sim.alloc(dts, n_trials, 0, dev)
+    buf["keys"].copy_(torch.from_numpy(keys.view(np.int64)))
+    buf["policies"].copy_(torch.from_numpy(pols.view(np.uint8)))
+    buf["trial_trace"].copy_(torch.from_numpy(trace_of.view(np.int32)))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    counters = torch.zeros(13, dtype=torch.int64, device=dev)
+
+    def step(timed_ms):
+        flush.fill_(1)                                     # L2 flush, outside the timed region
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.launch(dts, n_trials, buf, with_policies=True, stream=stream)
+        if world > 1:   # the single NCCL reduce of summary counters
+            dist.reduce(counters, dst=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        timed_ms.append(e0.elapsed_time(e1))
+
+    warm = []
+    for _ in range(args.warmup):
+        step(warm)
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            step(times)
+    res = sim.collect(buf, n_trials).results
+    bad = int((res["status"] != 0).sum())
+    t_local = float(np.sum(times))
+    tmax = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    t_max = float(tmax.item())
+    q_per_step = float(res["queries"].sum())
+    total_q = q_per_step * args.steps * world
+    value = total_q / (t_max / 1000.0)
+
+    # roofline of the dominant kernel (the replay kernel is the whole step)
+    pk = peaks()
+    clk_s = clk.summary()
+    f_mhz = clk_s["sm_mhz"] or pk["sm_max_mhz"]
+    smem_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e9        # GB/s at max clock
+    smem_bytes = algorithmic_bytes(res)
+    per_launch_s = (t_local / args.steps) / 1000.0
+    achieved_smem = smem_bytes / per_launch_s / 1e9
+    tb = trace_bytes(traces, trace_of)
+    achieved_hbm = tb / per_launch_s / 1e9
+    probes = float(res["probes"].sum())
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
+            "config": config_json(args),
+            "roofline": {"bound": "smem", "achieved": achieved_smem, "peak": smem_peak,
+                         "unit": "GB/s", "frac": achieved_smem / smem_peak, "traffic": None,
+                         "peak_src": "148 SM x 128 B/clk x sm_max_mhz (DESIGN.md §6)",
+                         "hbm_trace": {"achieved": achieved_hbm, "peak": pk["hbm_gbs"],
+                                       "frac": achieved_hbm / pk["hbm_gbs"],
+                                       "peak_src": pk["src"]}},
+            "prefix_probes_per_s": probes * world / per_launch_s,
+            "hit_rate": float(res["hit_tokens"].sum() / max(1, res["input_tokens"].sum())),
+            "trial_status_nonzero": bad,
+            "gpu_launches": args.steps * 1,
+            "clocks": clk_s}
+
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args)
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = max(1, min(os.cpu_count() or 1, 16))
+        nq = 1500
+        q, s = run_oracle_sample(traces, trace_of, evict, keys, nq, threads)
+        line["cpu_baseline"] = {"value": q / s, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": f"{threads} trials x first {nq} queries of the "
+                                          f"config-2 traces (W=8, B=512)"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):
+    """Same metric through the public API with HOST buffers: per step the pinned raw
+    traces, keys and policies go host->device, kvr_trace_load packs them, kvr_sim_run_multi
+    replays, and the per-trial results come back device->host, all inside the timed region."""
+    import torch
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator
+
+    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING)
+    n = len(keys)
+    pinned = {}
+    h2d = 0
+    for i, t in enumerate(traces):
+        for name in ("arrival_ms", "n_in_blocks", "n_out_blocks", "out_tokens", "block_offsets",
+                     "block_keys"):
+            h2d += getattr(t, name).nbytes
+    h2d += keys.nbytes + pols.nbytes + trace_of.nbytes
+    d2h = n * 144
+    times = []
+    for it in range(2 + max(1, args.steps // 2)):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dts = [DeviceTrace(t, device=dev, pinned=False) for t in traces]
+        out = sim.run(dts, keys, pols, trial_trace=trace_of, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+        q = float(out.results["queries"].sum())
+        for d in dts:
+            d.close()
+    ms = float(np.mean(times))
+    return {"value": q / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,326 @@
+// kvr_api.cu — host side of the C ABI declared in include/kvr.h: argument
+// validation, handles, state-tier selection, workspace sizing and launches.
+// No device memory is allocated here; every buffer belongs to the caller.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kvr_internal.h"
+
+struct kvr_trace {
+  uint32_t N, block_tokens, max_n;
+  uint64_t total, salt;
+  kvr::QueryHdr* hdr;
+  uint64_t* hash;
+};
+
+struct kvr_sim {
+  kvr_sim_config cfg;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+kvr_status fail(kvr_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+kvr_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(KVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool policy_ok(const kvr_policy& p, std::string* why) {
+  char b[256];
+  auto bad = [&](const char* s) { snprintf(b, sizeof b, "policy: %s", s); *why = b; return false; };
+  if (p.eviction > KVR_EVICT_RLT) return bad("eviction must be LRU(0) or RLT(1)");
+  if (p.rlt_fallback > KVR_RLT_LRU_MARKED) return bad("rlt_fallback must be 0..2");
+  if (p.router > KVR_ROUTE_RANDOM) return bad("router must be 0..4");
+  if (!(p.rho > 0.0 && p.rho <= 1.0)) return bad("rho must be in (0, 1]");
+  if (!(p.delta_t_ms > 0.0)) return bad("delta_t_ms must be > 0 (inf allowed)");
+  const double fin[] = {p.est_alpha_cached_ms, p.est_alpha_miss_ms, p.mu, p.theta0[0], p.theta0[1],
+                        p.theta0[2], p.theta0[3], p.tau, p.w_hit, p.w_load};
+  for (double v : fin)
+    if (!std::isfinite(v)) return bad("parameters must be finite");
+  return true;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+int smem_optin() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+struct Plan {
+  uint32_t tier;
+  size_t smem;
+  int ctas_per_sm;
+  uint32_t grid;
+  kvr::WorkerLayout lay;
+  size_t ws_fifo, ws_state, ws_total;
+};
+
+kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan* pl) {
+  const kvr_sim_config& c = sim->cfg;
+  const int optin = smem_optin();
+  if (optin <= 0) return fail(KVR_ERR_CUDA, "no CUDA device available");
+  const size_t base = kvr::ctrl_bytes() + kvr::kNumStages * kvr::stage_bytes(max_n);
+  const kvr::WorkerLayout l16 = kvr::make_layout(c.capacity_blocks, 2);
+  const kvr::WorkerLayout l32 = kvr::make_layout(c.capacity_blocks, 4);
+  const size_t smem1 = base + (size_t)c.W * l16.bytes;
+  const bool fit1 = c.capacity_blocks <= 65535 && smem1 <= (size_t)optin;
+  uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
+  if (tier == 1 && !fit1)
+    return fail(KVR_ERR_UNSUPPORTED, "shared-memory tier needs %zu B > %d B (W=%u, B=%u)", smem1,
+                optin, c.W, c.capacity_blocks);
+  if (tier == 2 && base > (size_t)optin)
+    return fail(KVR_ERR_UNSUPPORTED, "query staging needs %zu B of shared memory", base);
+  pl->tier = tier;
+  pl->lay = tier == 1 ? l16 : l32;
+  pl->smem = tier == 1 ? smem1 : base;
+  cudaError_t e = kvr::replay_attrs(tier, pl->smem, &pl->ctas_per_sm, c.W);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+  if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
+  const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
+  pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
+  pl->ws_fifo = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * kvr::kFifoRecBytes);
+  pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->lay.bytes : 0;
+  pl->ws_total = 256 + pl->ws_fifo + pl->ws_state;
+  return KVR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kvr_last_error(void) { return g_err.c_str(); }
+uint32_t kvr_abi_version(void) { return KVR_ABI_VERSION; }
+
+kvr_status kvr_trace_packed_bytes(const kvr_trace_desc* d, size_t* packed, size_t* scratch) {
+  if (!d || !packed || !scratch) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *packed = kvr::packed_bytes(d->n_queries, d->n_blocks_total);
+  *scratch = 256;
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_load(const kvr_trace_desc* d, void* d_packed, size_t packed_bytes,
+                          void* d_scratch, size_t scratch_bytes, void* stream, kvr_trace** out) {
+  if (!d || !out) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (d->block_tokens == 0) return fail(KVR_ERR_INVALID_ARG, "block_tokens must be >= 1");
+  if (!d_packed || !d_scratch) return fail(KVR_ERR_INVALID_ARG, "null packed/scratch buffer");
+  if (((uintptr_t)d_packed & 15) != 0) return fail(KVR_ERR_INVALID_ARG, "d_packed must be 16-B aligned");
+  if (packed_bytes < kvr::packed_bytes(d->n_queries, d->n_blocks_total))
+    return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "packed buffer too small");
+  if (scratch_bytes < 16) return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "scratch too small");
+  if (d->n_queries && (!d->arrival_ms || !d->n_in_blocks || !d->n_out_blocks || !d->out_tokens ||
+                       !d->block_offsets || (d->n_blocks_total && !d->block_keys)))
+    return fail(KVR_ERR_INVALID_ARG, "null trace array");
+  cudaStream_t s = (cudaStream_t)stream;
+  kvr::QueryHdr* hdr = (kvr::QueryHdr*)d_packed;
+  uint64_t* hash = (uint64_t*)((uint8_t*)d_packed + kvr::packed_hash_offset(d->n_queries));
+  cudaError_t e = kvr::launch_pack(*d, hdr, hash, (uint32_t*)d_scratch, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pack kernel");
+  uint32_t h_scr[4] = {0, 0, 0, 0};
+  e = cudaMemcpyAsync(h_scr, d_scratch, 16, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "trace validation readback");
+  if (h_scr[0]) {
+    return fail(KVR_ERR_INVALID_ARG, "malformed trace (flags 0x%x:%s%s%s)", h_scr[0],
+                (h_scr[0] & 1) ? " n_in<1 or offsets/length mismatch" : "",
+                (h_scr[0] & 2) ? " arrivals not finite/nonnegative/nondecreasing" : "",
+                (h_scr[0] & 4) ? " block_offsets[0]!=0 or [N]!=n_blocks_total" : "");
+  }
+  kvr_trace* t = new kvr_trace;
+  t->N = d->n_queries;
+  t->block_tokens = d->block_tokens;
+  t->max_n = h_scr[1];
+  t->total = d->n_blocks_total;
+  t->salt = d->hash_salt;
+  t->hdr = hdr;
+  t->hash = hash;
+  *out = t;
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_info(const kvr_trace* tr, uint32_t* n_queries, uint32_t* max_path_blocks,
+                          uint64_t* n_blocks_total) {
+  if (!tr) return fail(KVR_ERR_INVALID_ARG, "null trace");
+  if (n_queries) *n_queries = tr->N;
+  if (max_path_blocks) *max_path_blocks = tr->max_n;
+  if (n_blocks_total) *n_blocks_total = tr->total;
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_chained_hashes(const kvr_trace* tr, const uint64_t** d_hashes) {
+  if (!tr || !d_hashes) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *d_hashes = tr->hash;
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_destroy(kvr_trace* tr) {
+  delete tr;
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
+  if (!cfg || !out) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (cfg->W < 1 || cfg->W > kvr::kMaxW) return fail(KVR_ERR_UNSUPPORTED, "W must be in 1..32");
+  if (cfg->capacity_blocks < 1 || cfg->capacity_blocks > 65536)
+    return fail(KVR_ERR_UNSUPPORTED, "capacity_blocks must be in 1..65536");
+  if (cfg->pending_ring < 1) return fail(KVR_ERR_INVALID_ARG, "pending_ring must be >= 1");
+  if (cfg->latency_hist_bins > kvr::kMaxHistBins)
+    return fail(KVR_ERR_INVALID_ARG, "latency_hist_bins must be <= 256");
+  if (cfg->force_tier > 2) return fail(KVR_ERR_INVALID_ARG, "force_tier must be 0, 1 or 2");
+  const kvr_service_model& t = cfg->truth;
+  if (!std::isfinite(t.alpha_cached_ms) || !std::isfinite(t.alpha_miss_ms) ||
+      !std::isfinite(t.out_ms_per_token))
+    return fail(KVR_ERR_INVALID_ARG, "service model must be finite");
+  std::string why;
+  if (!policy_ok(cfg->default_policy, &why)) return fail(KVR_ERR_INVALID_ARG, "%s", why.c_str());
+  kvr_sim* s = new kvr_sim;
+  s->cfg = *cfg;
+  *out = s;
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_destroy(kvr_sim* sim) {
+  delete sim;
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_plan(const kvr_sim* sim, uint32_t max_path_blocks, uint32_t* tier,
+                        size_t* smem_bytes, uint32_t* ctas_per_sm) {
+  if (!sim) return fail(KVR_ERR_INVALID_ARG, "null sim");
+  Plan pl;
+  kvr_status st = make_plan(sim, max_path_blocks, 1u << 30, &pl);
+  if (st) return st;
+  if (tier) *tier = pl.tier;
+  if (smem_bytes) *smem_bytes = pl.smem;
+  if (ctas_per_sm) *ctas_per_sm = (uint32_t)pl.ctas_per_sm;
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_workspace_bytes_multi(const kvr_sim* sim, uint32_t n_traces,
+                                         const kvr_trace* const* traces, uint32_t n_trials,
+                                         size_t* bytes) {
+  if (!sim || !traces || !bytes || n_traces == 0) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  uint32_t max_n = 1;
+  for (uint32_t i = 0; i < n_traces; ++i) {
+    if (!traces[i]) return fail(KVR_ERR_INVALID_ARG, "null trace %u", i);
+    max_n = std::max(max_n, traces[i]->max_n);
+  }
+  Plan pl;
+  kvr_status st = make_plan(sim, max_n, n_trials, &pl);
+  if (st) return st;
+  *bytes = pl.ws_total;
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_workspace_bytes(const kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
+                                   size_t* bytes) {
+  return kvr_sim_workspace_bytes_multi(sim, 1, &trace, n_trials, bytes);
+}
+
+kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* traces,
+                             const uint32_t* d_trial_trace, uint32_t n_trials,
+                             const uint64_t* d_keys, const kvr_policy* d_policies,
+                             kvr_trial_result* d_results, uint32_t* d_hist,
+                             kvr_query_record* d_records, uint64_t* d_victims, uint64_t victims_cap,
+                             void* d_ws, size_t ws_bytes, void* stream) {
+  if (!sim || !traces) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  if (n_traces == 0 || n_traces > kvr::kMaxTraces)
+    return fail(KVR_ERR_UNSUPPORTED, "n_traces must be in 1..%u", kvr::kMaxTraces);
+  if (n_traces > 1 && !d_trial_trace) return fail(KVR_ERR_INVALID_ARG, "d_trial_trace required");
+  if (n_trials == 0) return KVR_OK;
+  if (!d_keys || !d_results || !d_ws) return fail(KVR_ERR_INVALID_ARG, "null keys/results/workspace");
+  const kvr_sim_config& c = sim->cfg;
+  uint32_t max_n = 1, max_N = 0;
+  for (uint32_t i = 0; i < n_traces; ++i) {
+    const kvr_trace* t = traces[i];
+    if (!t) return fail(KVR_ERR_INVALID_ARG, "null trace %u", i);
+    if (t->max_n > c.capacity_blocks)
+      return fail(KVR_ERR_CAPACITY,
+                  "trace %u has a complete path of %u blocks > capacity B=%u (premise beta*L_max<=B)",
+                  i, t->max_n, c.capacity_blocks);
+    max_n = std::max(max_n, t->max_n);
+    max_N = std::max(max_N, t->N);
+  }
+  const uint32_t R = std::min(c.record_trials, n_trials);
+  if (R && !d_records) return fail(KVR_ERR_INVALID_ARG, "record_trials > 0 needs d_records");
+  Plan pl;
+  kvr_status st = make_plan(sim, max_n, n_trials, &pl);
+  if (st) return st;
+  if (ws_bytes < pl.ws_total)
+    return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, pl.ws_total);
+
+  kvr::ReplayParams p;
+  std::memset(&p, 0, sizeof(p));
+  for (uint32_t i = 0; i < n_traces; ++i) {
+    p.traces[i].hdr = traces[i]->hdr;
+    p.traces[i].hash = traces[i]->hash;
+    p.traces[i].N = traces[i]->N;
+    p.traces[i].max_n = traces[i]->max_n;
+    p.traces[i].block_tokens = traces[i]->block_tokens;
+  }
+  p.trial_trace = n_traces > 1 ? d_trial_trace : nullptr;
+  p.n_traces = n_traces;
+  p.n_trials = n_trials;
+  p.W = c.W;
+  p.B = c.capacity_blocks;
+  p.ring = c.pending_ring;
+  p.record_trials = R;
+  p.rec_stride = max_N;
+  p.bins = d_hist ? c.latency_hist_bins : 0;
+  p.stage_bytes = (uint32_t)kvr::stage_bytes(max_n);
+  p.lay = pl.lay;
+  p.truth = c.truth;
+  p.defpol = c.default_policy;
+  p.policies = d_policies;
+  p.keys = d_keys;
+  p.results = d_results;
+  p.hist = p.bins ? d_hist : nullptr;
+  p.records = R ? d_records : nullptr;
+  p.victims = (R && d_victims && victims_cap) ? d_victims : nullptr;
+  p.victims_per_trial = p.victims ? victims_cap / R : 0;
+  uint8_t* ws = (uint8_t*)d_ws;
+  p.work_counter = (unsigned int*)ws;
+  p.fifo = ws + 256;
+  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_fifo : nullptr;
+
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);
+  if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
+  e = kvr::launch_replay(pl.tier, p, pl.grid, pl.smem, s);
+  if (e != cudaSuccess) return cuda_fail(e, "replay launch");
+  return KVR_OK;
+}
+
+kvr_status kvr_sim_run(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
+                       const uint64_t* d_keys, const kvr_policy* d_policies,
+                       kvr_trial_result* d_results, uint32_t* d_hist, kvr_query_record* d_records,
+                       uint64_t* d_victims, uint64_t victims_cap, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  return kvr_sim_run_multi(sim, 1, &trace, nullptr, n_trials, d_keys, d_policies, d_results, d_hist,
+                           d_records, d_victims, victims_cap, d_ws, ws_bytes, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// kvr_internal.h — layouts shared by the host API (kvr_api.cu) and the kernels
+// (kvr_pack.cu, kvr_replay.cu).  Not part of the public ABI (include/kvr.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "kvr.h"
+
+namespace kvr {
+
+constexpr uint32_t kNumStages = 3;      // query staging ring depth (bulk-async copies)
+constexpr uint32_t kMaxTraces = 64;     // traces per multi-trace launch
+constexpr uint32_t kFifoRecBytes = 64;  // one pending completion {c,a,E^,phi0..2,C^,k_a}
+constexpr uint32_t kMaxHistBins = 256;
+constexpr uint32_t kMaxW = 32;
+
+// Packed trace, per query: a 32-byte header, bulk-copied with the query's hashes.
+struct __align__(16) QueryHdr {
+  double arrival_ms;
+  uint64_t block_off;   // offset of the query's first identity in the hash array
+  uint32_t n_in, n_out, out_tokens, _pad;
+};
+static_assert(sizeof(QueryHdr) == 32, "header is 32 B");
+
+struct TraceDev {
+  const QueryHdr* hdr;  // [N]
+  const uint64_t* hash; // [total] chained identities, CSR order
+  uint32_t N, max_n, block_tokens, _pad;
+};
+
+// packed buffer = [QueryHdr x N][pad to 16][u64 hash x total]
+inline size_t packed_hash_offset(uint32_t N) { return ((size_t)N * sizeof(QueryHdr) + 15) & ~(size_t)15; }
+inline size_t packed_bytes(uint32_t N, uint64_t total) { return packed_hash_offset(N) + total * 8 + 16; }
+
+// Per-worker cache state (one worker = one warp).  Slot arrays of the prefix
+// tree (identity, parent slot, child count, LRU list links), an open-addressed
+// linear-probing table identity -> slot, and the LEAF / MARK bitmaps (RLT's
+// marking set T is exactly the MARK bits because T is a subset of S).
+struct WorkerLayout {
+  uint32_t B, T, nwords, idx_bytes;
+  size_t off_key, off_parent, off_nchild, off_prev, off_next, off_table, off_leaf, off_mark, bytes;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
+  WorkerLayout L{};
+  L.B = B;
+  uint32_t T = 1;
+  while (T < 2 * B) T <<= 1;     // load factor <= 1/2
+  L.T = T;
+  L.nwords = (B + 31) / 32;
+  L.idx_bytes = idx_bytes;
+  size_t o = 0;
+  L.off_key = o;    o = align16(o + (size_t)B * 8);
+  L.off_parent = o; o = align16(o + (size_t)B * idx_bytes);
+  L.off_nchild = o; o = align16(o + (size_t)B * idx_bytes);
+  L.off_prev = o;   o = align16(o + (size_t)B * idx_bytes);
+  L.off_next = o;   o = align16(o + (size_t)B * idx_bytes);
+  L.off_table = o;  o = align16(o + (size_t)T * idx_bytes);
+  L.off_leaf = o;   o = align16(o + (size_t)L.nwords * 4);
+  L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);
+  L.bytes = o;
+  return L;
+}
+
+// Control block at the start of dynamic shared memory.
+struct __align__(16) Ctrl {
+  unsigned long long mbar[kNumStages];
+  double score[2][kMaxW];
+  uint32_t mhit[2][kMaxW];
+  uint32_t npend[2][kMaxW];
+  double P[kMaxW], F[kMaxW];
+  double sum_lat, sum_ttft, max_lat;
+  unsigned long long digest, vcursor;
+  unsigned long long cnt[10];   // probes, inserted, evictions, draws, resets, fallbacks, hit, in, queries, maxpend
+  kvr_policy pol;                      // this trial's policy
+  uint32_t trial, status, abortf[2];   // abort flag double-buffered by query parity
+  uint32_t hist[kMaxHistBins];
+};
+
+inline size_t ctrl_bytes() { return align16(sizeof(Ctrl)); }
+inline size_t stage_bytes(uint32_t max_n) { return align16(sizeof(QueryHdr) + 8 * ((size_t)max_n + 2)); }
+
+struct ReplayParams {
+  TraceDev traces[kMaxTraces];
+  const uint32_t* trial_trace;   // [n_trials] or null
+  uint32_t n_traces, n_trials, W, B;
+  uint32_t ring, record_trials, rec_stride, bins;
+  uint32_t stage_bytes;
+  uint32_t _pad0;
+  WorkerLayout lay;
+  kvr_service_model truth;
+  kvr_policy defpol;
+  const kvr_policy* policies;
+  const uint64_t* keys;
+  kvr_trial_result* results;
+  uint32_t* hist;
+  kvr_query_record* records;
+  uint64_t* victims;
+  uint64_t victims_per_trial;
+  uint8_t* fifo;                 // [grid][W][ring][64 B]
+  uint8_t* gstate;               // [grid][W][lay.bytes] (global tier) or null
+  unsigned int* work_counter;
+};
+
+// launchers (kvr_pack.cu / kvr_replay.cu)
+cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, uint32_t* scratch,
+                        cudaStream_t s);
+// tier 1 = tables in shared memory (u16 slot ids), 2 = tables in global memory (u32 slot ids)
+cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W);
+cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
+                          cudaStream_t s);
+
+}  // namespace kvr

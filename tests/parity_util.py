@@ -1,0 +1,95 @@
+"""Shared helpers for the GPU-vs-oracle parity tests (tests only)."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+INT_FIELDS = ("queries", "hit_tokens", "input_tokens", "probes", "inserted_blocks", "evictions",
+              "rlt_draws", "rlt_resets", "rlt_fallbacks", "max_pending", "decision_digest", "status")
+FP_FIELDS = ("sum_latency_ms", "sum_ttft_ms", "max_latency_ms", "makespan_ms",
+             "last_completion_ms", "sum_load_ms")
+# north_star: decisions and counts bit-exact; latency/TTFT/makespan aggregates within 1e-12 rel.
+# Both sides evaluate the same fp64 expressions in the same order without contraction, so the
+# test demands bit equality and reports the relative error if that ever fails.
+FP_RTOL = 1e-12
+
+
+def to_oracle_policy(oracle, pol):
+    d = dataclasses.asdict(pol)
+    return oracle.OraclePolicy(**d)
+
+
+def run_oracle(oracle, tr, W, B, pols, keys, truth, ring, record, victims_cap, bins=0):
+    cfg = oracle.OracleConfig(W=W, capacity_blocks=B, alpha_cached_ms=truth[0],
+                              alpha_miss_ms=truth[1], out_ms_per_token=truth[2],
+                              pending_ring=ring, latency_hist_bins=bins)
+    outs = []
+    for k, pol in zip(keys, pols):
+        r = oracle.run(cfg, tr, to_oracle_policy(oracle, pol), int(k), record=record,
+                       victims_cap=victims_cap)
+        assert r.rc == 0, r.rc
+        outs.append(r)
+    return outs
+
+
+def run_gpu(kvr, traces, W, B, pols, keys, truth, ring, record, victims_cap, force_tier=0,
+            trial_trace=None, bins=0):
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
+    dts = [DeviceTrace(t) for t in traces]
+    sim = Simulator(W, B, alpha_cached_ms=truth[0], alpha_miss_ms=truth[1],
+                    out_ms_per_token=truth[2], pending_ring=ring,
+                    record_trials=len(keys) if record else 0, force_tier=force_tier,
+                    latency_hist_bins=bins)
+    out = sim.run(dts, np.asarray(keys, np.uint64), policies_array(pols),
+                  trial_trace=trial_trace, victims_cap=victims_cap * len(keys) if record else 0)
+    return out, dts, sim
+
+
+def assert_result_equal(g, o, ctx=""):
+    for f in INT_FIELDS:
+        assert int(g[f]) == int(o[f]), f"{ctx} field {f}: gpu {int(g[f])} oracle {int(o[f])}"
+    for f in FP_FIELDS:
+        gv, ov = float(g[f]), float(o[f])
+        rel = abs(gv - ov) / max(abs(ov), 1e-300)
+        assert gv == ov, f"{ctx} field {f}: gpu {gv!r} oracle {ov!r} rel {rel:.3e}"
+
+
+def assert_records_equal(grec, orec, n, ctx=""):
+    for fld in ("worker", "hit_tokens", "n_victims", "victim_offset"):
+        a, b = grec[fld][:n], orec[fld][:n]
+        if not np.array_equal(a, b):
+            j = int(np.nonzero(a != b)[0][0])
+            raise AssertionError(f"{ctx} record {fld} differs first at query {j}: "
+                                 f"gpu {a[j]} oracle {b[j]}")
+    for fld in ("ttft_ms", "latency_ms", "score"):
+        a, b = grec[fld][:n], orec[fld][:n]
+        if not np.array_equal(a, b):
+            j = int(np.nonzero(a != b)[0][0])
+            raise AssertionError(f"{ctx} record {fld} differs first at query {j}: "
+                                 f"gpu {a[j]!r} oracle {b[j]!r}")
+
+
+def compare(oracle, kvr, tr, W, B, pols, keys, truth=(0.0, 1.0, 20.0), ring=256, record=True,
+            victims_cap=None, force_tier=0, bins=0):
+    n = tr.n_queries
+    if victims_cap is None:
+        victims_cap = max(1, tr.total_blocks)
+    out, _, _ = run_gpu(kvr, [tr], W, B, pols, keys, truth, ring, record, victims_cap,
+                        force_tier=force_tier, bins=bins)
+    orc = run_oracle(oracle, tr, W, B, pols, keys, truth, ring, record, victims_cap, bins=bins)
+    for t, o in enumerate(orc):
+        ctx = f"trial {t} key {keys[t]} pol {pols[t]}"
+        g = out.results[t]
+        if o.result["status"] == 1 or int(g["status"]) == 1:   # ring overflow: stop point only
+            assert int(g["status"]) == o.result["status"] and int(g["queries"]) == o.result["queries"], ctx
+            continue
+        assert_result_equal(g, o.result, ctx)
+        if record:
+            assert_records_equal(out.records[t], o.records, n, ctx)
+            nv = int(o.result["evictions"])
+            gv = out.victims[t * victims_cap: t * victims_cap + min(nv, victims_cap)]
+            assert np.array_equal(gv, o.victims[: min(nv, victims_cap)]), ctx + " victims"
+        if bins:
+            assert np.array_equal(out.hist[t], o.hist), ctx + " hist"
+    return out, orc
