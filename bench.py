@@ -38,8 +38,8 @@ N_QUERIES = 100_000
 TRIALS_PER_GPU = 1024
 GSP_GROUPS, GSP_PER_GROUP = 125, 800           # 125 x 800 = 100k queries per trace
 GSP_LENGTHS = (128, 256, 512, 1024, 2048)      # paper's {512..8192} tokens / 4
-UTIL = 0.5                                     # all-miss utilisation of the Poisson arrivals
-RING = 4096                                    # pending-completion FIFO per worker
+UTIL = 0.4                                     # all-miss utilisation of the Poisson arrivals
+RING = 16384                                   # pending-completion FIFO per worker
 TRACE_SEEDS = (0xC2, 0xC3, 0xC4)
 METRIC = "simulated queries/sec (all replays)"
 UNIT = "query-replays/s"
@@ -206,8 +206,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--queries", type=int, default=N_QUERIES, help=argparse.SUPPRESS)
     ap.add_argument("--trials", type=int, default=TRIALS_PER_GPU, help=argparse.SUPPRESS)
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling run: one launch, no warm-up / e2e / cpu baseline")
     args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
+    if args.ncu:
+        args.warmup, args.steps, args.no_e2e, args.no_cpu_baseline = 0, 1, True, True
+    else:
+        args.warmup = max(3, args.warmup)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -536,12 +536,17 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     if (lat > out->max_latency_ms) out->max_latency_ms = lat;
     out->queries++;
 
-    // 6. decision digest
+    // 6. decision digest (DESIGN.md §3 "decision digest"): per query the index,
+    //    the chosen worker, its hit blocks, the victim count and an order-sensitive
+    //    combination of the victims, V = XOR_k fmix64(H_{v_k} ^ (k+1)*K).
+    uint64_t V = 0;
+    for (size_t k = 0; k < ux.victims.size(); ++k)
+      V ^= fmix64(ux.victims[k] ^ ((uint64_t)(k + 1) * K_POS));
     D = fmix64(D ^ (uint64_t)j);
     D = fmix64(D ^ (uint64_t)best);
     D = fmix64(D ^ (uint64_t)m[best]);
-    for (uint64_t v : ux.victims) D = fmix64(D ^ v);
     D = fmix64(D ^ (uint64_t)ux.victims.size());
+    D = fmix64(D ^ V);
 
     if (records) {
       kvro_query_record& R = records[j];

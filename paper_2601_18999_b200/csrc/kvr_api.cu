@@ -74,18 +74,19 @@ struct Plan {
   int ctas_per_sm;
   uint32_t grid;
   kvr::WorkerLayout lay;
-  size_t ws_fifo, ws_state, ws_total;
+  kvr::AuxLayout aux;
+  size_t ws_aux, ws_state, ws_total;
 };
 
 kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan* pl) {
   const kvr_sim_config& c = sim->cfg;
   const int optin = smem_optin();
   if (optin <= 0) return fail(KVR_ERR_CUDA, "no CUDA device available");
-  const size_t base = kvr::ctrl_bytes() + kvr::kNumStages * kvr::stage_bytes(max_n);
+  const size_t base = kvr::smem_base_bytes(c.W, max_n);
   const kvr::WorkerLayout l16 = kvr::make_layout(c.capacity_blocks, 2);
   const kvr::WorkerLayout l32 = kvr::make_layout(c.capacity_blocks, 4);
   const size_t smem1 = base + (size_t)c.W * l16.bytes;
-  const bool fit1 = c.capacity_blocks <= 65535 && smem1 <= (size_t)optin;
+  const bool fit1 = c.capacity_blocks <= 65533 && smem1 <= (size_t)optin;   // 0xFFFE/F = tomb/empty
   uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
   if (tier == 1 && !fit1)
     return fail(KVR_ERR_UNSUPPORTED, "shared-memory tier needs %zu B > %d B (W=%u, B=%u)", smem1,
@@ -100,9 +101,10 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
-  pl->ws_fifo = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * kvr::kFifoRecBytes);
+  pl->aux = kvr::make_aux(c.capacity_blocks, c.pending_ring, max_n);
+  pl->ws_aux = (size_t)pl->grid * c.W * pl->aux.bytes;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->lay.bytes : 0;
-  pl->ws_total = 256 + pl->ws_fifo + pl->ws_state;
+  pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
   return KVR_OK;
 }
 
@@ -291,6 +293,8 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   p.rec_stride = max_N;
   p.bins = d_hist ? c.latency_hist_bins : 0;
   p.stage_bytes = (uint32_t)kvr::stage_bytes(max_n);
+  p.scratch_bytes = (uint32_t)kvr::scratch_bytes(max_n);
+  p.aux = pl.aux;
   p.lay = pl.lay;
   p.truth = c.truth;
   p.defpol = c.default_policy;
@@ -303,8 +307,8 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   p.victims_per_trial = p.victims ? victims_cap / R : 0;
   uint8_t* ws = (uint8_t*)d_ws;
   p.work_counter = (unsigned int*)ws;
-  p.fifo = ws + 256;
-  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_fifo : nullptr;
+  p.aux_base = ws + 256;
+  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux : nullptr;
 
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);

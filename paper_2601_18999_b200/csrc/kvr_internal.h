@@ -33,22 +33,23 @@ struct TraceDev {
 inline size_t packed_hash_offset(uint32_t N) { return ((size_t)N * sizeof(QueryHdr) + 15) & ~(size_t)15; }
 inline size_t packed_bytes(uint32_t N, uint64_t total) { return packed_hash_offset(N) + total * 8 + 16; }
 
-// Per-worker cache state (one worker = one warp).  Slot arrays of the prefix
-// tree (identity, parent slot, child count, LRU list links), an open-addressed
-// linear-probing table identity -> slot, and the LEAF / MARK bitmaps (RLT's
-// marking set T is exactly the MARK bits because T is a subset of S).
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Per-worker cache state (one worker = one warp), latency-critical part, held in
+// shared memory (tier 1, u16 slot ids) or global memory (tier 2, u32 slot ids):
+// slot arrays of the prefix tree (identity, parent slot, child count), an
+// open-addressed linear-probing table identity -> slot with tombstones, and the
+// LEAF / MARK bitmaps (RLT's marking set T is exactly the MARK bits, T in S).
 struct WorkerLayout {
   uint32_t B, T, nwords, idx_bytes;
-  size_t off_key, off_parent, off_nchild, off_prev, off_next, off_table, off_leaf, off_mark, bytes;
+  size_t off_key, off_parent, off_nchild, off_table, off_leaf, off_mark, bytes;
 };
-
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   WorkerLayout L{};
   L.B = B;
-  uint32_t T = 1;
-  while (T < 2 * B) T <<= 1;     // load factor <= 1/2
+  uint32_t T = 2;
+  while (T < 2 * B) T <<= 1;     // load factor <= 1/2 (tombstones rebuilt at 3/4)
   L.T = T;
   L.nwords = (B + 31) / 32;
   L.idx_bytes = idx_bytes;
@@ -56,13 +57,33 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   L.off_key = o;    o = align16(o + (size_t)B * 8);
   L.off_parent = o; o = align16(o + (size_t)B * idx_bytes);
   L.off_nchild = o; o = align16(o + (size_t)B * idx_bytes);
-  L.off_prev = o;   o = align16(o + (size_t)B * idx_bytes);
-  L.off_next = o;   o = align16(o + (size_t)B * idx_bytes);
   L.off_table = o;  o = align16(o + (size_t)T * idx_bytes);
   L.off_leaf = o;   o = align16(o + (size_t)L.nwords * 4);
   L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);
   L.bytes = o;
   return L;
+}
+
+// Per-worker auxiliary state in global memory (L2-resident): the pending
+// completion FIFO, the Leaf-LRU recency log (append-only ring of (stamp, slot),
+// compacted when full) and the per-slot stamps that validate log entries.
+struct AuxLayout {
+  uint32_t ring, log_cap;
+  size_t off_fifo, off_stamp, off_log, bytes;
+};
+
+inline AuxLayout make_aux(uint32_t B, uint32_t ring, uint32_t max_n) {
+  AuxLayout A{};
+  A.ring = ring;
+  uint32_t C = 64;
+  while (C < 2 * (B + max_n + 32)) C <<= 1;
+  A.log_cap = C;
+  size_t o = 0;
+  A.off_fifo = o;  o = align16(o + (size_t)ring * kFifoRecBytes);
+  A.off_stamp = o; o = align16(o + (size_t)B * 4);
+  A.off_log = o;   o = align16(o + (size_t)C * 8);
+  A.bytes = (o + 127) & ~(size_t)127;
+  return A;
 }
 
 // Control block at the start of dynamic shared memory.
@@ -82,15 +103,17 @@ struct __align__(16) Ctrl {
 
 inline size_t ctrl_bytes() { return align16(sizeof(Ctrl)); }
 inline size_t stage_bytes(uint32_t max_n) { return align16(sizeof(QueryHdr) + 8 * ((size_t)max_n + 2)); }
+// per-warp scratch (u32 entries): LRU victims of one query
+inline size_t scratch_bytes(uint32_t max_n) { return align16(4 * ((size_t)max_n + 32)); }
 
 struct ReplayParams {
   TraceDev traces[kMaxTraces];
   const uint32_t* trial_trace;   // [n_trials] or null
   uint32_t n_traces, n_trials, W, B;
   uint32_t ring, record_trials, rec_stride, bins;
-  uint32_t stage_bytes;
-  uint32_t _pad0;
+  uint32_t stage_bytes, scratch_bytes;
   WorkerLayout lay;
+  AuxLayout aux;
   kvr_service_model truth;
   kvr_policy defpol;
   const kvr_policy* policies;
@@ -100,10 +123,14 @@ struct ReplayParams {
   kvr_query_record* records;
   uint64_t* victims;
   uint64_t victims_per_trial;
-  uint8_t* fifo;                 // [grid][W][ring][64 B]
+  uint8_t* aux_base;             // [grid][W][aux.bytes]
   uint8_t* gstate;               // [grid][W][lay.bytes] (global tier) or null
   unsigned int* work_counter;
 };
+
+inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
+  return ctrl_bytes() + kNumStages * stage_bytes(max_n) + (size_t)W * scratch_bytes(max_n);
+}
 
 // launchers (kvr_pack.cu / kvr_replay.cu)
 cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, uint32_t* scratch,

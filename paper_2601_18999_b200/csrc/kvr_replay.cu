@@ -3,25 +3,29 @@
 //   1. catch-up   (each warp, its worker): decay ticks merged with FIFO
 //                 completions -> NLMS OnlineUpdate + ReleaseLoad
 //                 (Alg. 2 l.11-17; readings A8, A10, A11)
-//   2. match      (each warp, 32 lanes probe 32 blocks, ballot -> first miss):
+//   2. match      (each warp: 32 lanes probe 32 blocks, ballot -> first miss):
 //                 longest cached prefix m_ij of the query
 //   3. score      LBGR Eq. 4-5 / STATIC / THRESHOLD / RR / RANDOM
 //   -- one __syncthreads per query --
 //   4. argmin     (every warp, shuffle reduction; lowest index on ties, A15)
-//   5. update     (warp i* only): UpdateCache (Eq. 3) with RLT
-//                 (Alg. 1; marking = MARK bitmap, uniform unmarked
-//                 leaf by a warp popcount scan + Philox draw) or Leaf-LRU
-//                 (O(1) intrusive list in (stamp,-depth) order)
+//   5. update     (warp i* only): UpdateCache (Eq. 3)
+//        hits     lane-parallel: slot lookups, RLT marks with the |T|=B+1 reset
+//                 located by a ballot prefix count (Alg. 1 l.6-9), recency stamps
+//        misses   RLT (Alg. 1 l.12-17): the only serial chain — per eviction a
+//                 warp popcount scan over register-resident LEAF & ~MARK words
+//                 and one precomputed Philox draw (32 draws per lane batch);
+//                 Leaf-LRU: the e victims are the first e valid
+//                 entries of the recency log (batch select == sequential L-LRU)
+//        apply    lane-parallel: table deletes (tombstones), slot arrays,
+//                 table inserts (CAS), victim digest, log append
 //   6. accounting (warp i*): Eq. 1-2 truth, Eq. 6, FIFO latency / TTFT (A12-A14, A20)
 // while the other warps already run steps 1-3 of query j+1.  Query headers and
 // identities are staged in shared memory by 1-D bulk-async copies (TMA engine,
 // cp.async.bulk + mbarrier) kNumStages-1 queries ahead.
 //
-// Scalar per-worker state (loads, theta, counters, list head) is warp-uniform:
-// every lane holds the same value and performs the same fp64 operation, so
-// no broadcast is needed; stores of shared scalars are made by all lanes
-// with identical values.  fp64 follows the oracle's written operation order;
-// the library is compiled with -fmad=false (no contraction) and IEEE division.
+// Scalar per-worker state (loads, theta, counters) is warp-uniform: every lane
+// holds the same value and executes the same fp64 operation; fp64 follows the
+// oracle's written operation order with -fmad=false and IEEE division.
 #include <math.h>
 
 #include "kvr_device.cuh"
@@ -30,12 +34,16 @@
 namespace kvr {
 
 template <typename Idx>
+struct Nil {
+  static constexpr Idx empty = (Idx)~(Idx)0;
+  static constexpr Idx tomb = (Idx)(~(Idx)0 - 1);
+};
+
+template <typename Idx>
 struct WorkerView {
   uint64_t* key;
   Idx* parent;
   Idx* nchild;
-  Idx* prev;
-  Idx* next;
   Idx* table;
   uint32_t* leaf;
   uint32_t* mark;
@@ -47,128 +55,83 @@ __device__ __forceinline__ WorkerView<Idx> make_view(uint8_t* base, const Worker
   v.key = reinterpret_cast<uint64_t*>(base + L.off_key);
   v.parent = reinterpret_cast<Idx*>(base + L.off_parent);
   v.nchild = reinterpret_cast<Idx*>(base + L.off_nchild);
-  v.prev = reinterpret_cast<Idx*>(base + L.off_prev);
-  v.next = reinterpret_cast<Idx*>(base + L.off_next);
   v.table = reinterpret_cast<Idx*>(base + L.off_table);
   v.leaf = reinterpret_cast<uint32_t*>(base + L.off_leaf);
   v.mark = reinterpret_cast<uint32_t*>(base + L.off_mark);
   return v;
 }
 
+// ---------------------------------------------------------------- hash table
 template <typename Idx>
-__device__ __forceinline__ Idx table_lookup(const WorkerView<Idx>& S, uint32_t mask, uint64_t h) {
-  const Idx NIL = (Idx)~(Idx)0;
+__device__ __forceinline__ Idx tbl_find(const WorkerView<Idx>& S, uint32_t mask, uint64_t h) {
   uint32_t pos = (uint32_t)h & mask;
+#pragma unroll 1
   for (;;) {
     const Idx e = S.table[pos];
-    if (e == NIL) return NIL;
-    if (S.key[e] == h) return e;
+    if (e == Nil<Idx>::empty) return Nil<Idx>::empty;
+    if (e != Nil<Idx>::tomb && S.key[e] == h) return e;
     pos = (pos + 1) & mask;
   }
 }
 
-// linear probing insert: first empty position from home (table never full, T >= 2B)
+// tombstone the entry of `slot` (identity h); lanes may run this concurrently
 template <typename Idx>
-__device__ __forceinline__ void table_insert(const WorkerView<Idx>& S, uint32_t mask, uint64_t h,
-                                             Idx slot, uint32_t lane) {
-  const Idx NIL = (Idx)~(Idx)0;
+__device__ __forceinline__ void tbl_erase(const WorkerView<Idx>& S, uint32_t mask, uint64_t h, Idx slot) {
   uint32_t pos = (uint32_t)h & mask;
-  while (S.table[pos] != NIL) pos = (pos + 1) & mask;
-  __syncwarp();
-  if (lane == 0) S.table[pos] = slot;
-  __syncwarp();
+#pragma unroll 1
+  while (S.table[pos] != slot) pos = (pos + 1) & mask;
+  S.table[pos] = Nil<Idx>::tomb;
 }
 
-// backward-shift deletion of `slot` (identity h) keeps probe sequences intact
-template <typename Idx>
-__device__ __forceinline__ void table_delete(const WorkerView<Idx>& S, uint32_t mask, uint64_t h,
-                                             Idx slot, uint32_t lane) {
-  const Idx NIL = (Idx)~(Idx)0;
-  uint32_t i = (uint32_t)h & mask;
-  while (S.table[i] != slot) i = (i + 1) & mask;
-  uint32_t j = (i + 1) & mask;
+// claim position pos if it is EMPTY or TOMB (CAS); returns 1 if it was EMPTY
+__device__ __forceinline__ uint32_t tbl_claim_at(uint16_t* table, uint32_t pos, uint16_t slot,
+                                                 bool* ok) {
+  uint32_t* w32 = reinterpret_cast<uint32_t*>(table) + (pos >> 1);
+  const uint32_t sh = (pos & 1u) * 16u;
+  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(w32);
+#pragma unroll 1
   for (;;) {
-    const Idx e = S.table[j];
-    if (e == NIL) break;
-    const uint32_t home = (uint32_t)S.key[e] & mask;
-    if (((j - home) & mask) >= ((j - i) & mask)) {
-      __syncwarp();
-      if (lane == 0) S.table[i] = e;
-      __syncwarp();
-      i = j;
-    }
-    j = (j + 1) & mask;
+    const uint32_t e = (cur >> sh) & 0xffffu;
+    if (e != 0xffffu && e != 0xfffeu) { *ok = false; return 0; }
+    const uint32_t nw = (cur & ~(0xffffu << sh)) | ((uint32_t)slot << sh);
+    const uint32_t old = atomicCAS(w32, cur, nw);
+    if (old == cur) { *ok = true; return e == 0xffffu ? 1u : 0u; }
+    cur = old;
   }
-  __syncwarp();
-  if (lane == 0) S.table[i] = NIL;
-  __syncwarp();
+}
+__device__ __forceinline__ uint32_t tbl_claim_at(uint32_t* table, uint32_t pos, uint32_t slot,
+                                                 bool* ok) {
+  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(table + pos);
+#pragma unroll 1
+  for (;;) {
+    if (cur != 0xffffffffu && cur != 0xfffffffeu) { *ok = false; return 0; }
+    const uint32_t old = atomicCAS(table + pos, cur, slot);
+    if (old == cur) { *ok = true; return cur == 0xffffffffu ? 1u : 0u; }
+    cur = old;
+  }
+}
+template <typename Idx>
+__device__ __forceinline__ uint32_t tbl_insert(const WorkerView<Idx>& S, uint32_t mask, uint64_t h,
+                                               Idx slot) {
+  uint32_t pos = (uint32_t)h & mask;
+#pragma unroll 1
+  for (;;) {
+    bool ok;
+    const uint32_t was_empty = tbl_claim_at(S.table, pos, slot, &ok);
+    if (ok) return was_empty;
+    pos = (pos + 1) & mask;
+  }
 }
 
-__device__ __forceinline__ void bit_set(uint32_t* w, uint32_t s, uint32_t lane) {
-  const uint32_t v = w[s >> 5] | (1u << (s & 31));
+// rebuild without tombstones (warp): clear, then re-insert every live slot
+template <typename Idx>
+__device__ __noinline__ void tbl_rebuild(const WorkerView<Idx>& S, uint32_t T, uint32_t size,
+                                         uint32_t lane) {
   __syncwarp();
-  if (lane == 0) w[s >> 5] = v;
+  for (uint32_t i = lane; i < T; i += 32) S.table[i] = Nil<Idx>::empty;
   __syncwarp();
-}
-__device__ __forceinline__ void bit_clear(uint32_t* w, uint32_t s, uint32_t lane) {
-  const uint32_t v = w[s >> 5] & ~(1u << (s & 31));
+  for (uint32_t s = lane; s < size; s += 32) tbl_insert<Idx>(S, T - 1, S.key[s], (Idx)s);
   __syncwarp();
-  if (lane == 0) w[s >> 5] = v;
-  __syncwarp();
-}
-__device__ __forceinline__ bool bit_test(const uint32_t* w, uint32_t s) {
-  return (w[s >> 5] >> (s & 31)) & 1u;
-}
-
-// Uniform choice over U = LEAF (& ~MARK if use_mark) minus parent slot p, in
-// physical-slot order (reading A6).  Returns |U| through *total; if idx_src is
-// given it is the 64-bit random draw and the selected slot is returned.
-__device__ __forceinline__ uint32_t rlt_count(const uint32_t* leaf, const uint32_t* mark,
-                                              uint32_t nwords, uint32_t p, bool use_mark,
-                                              uint32_t lane, uint32_t& lane_cnt,
-                                              uint32_t& incl) {
-  const uint32_t wpl = (nwords + 31) >> 5;
-  const uint32_t w0 = lane * wpl, w1 = min(nwords, w0 + wpl);
-  uint32_t c = 0;
-  for (uint32_t wi = w0; wi < w1; ++wi) {
-    uint32_t u = leaf[wi];
-    if (use_mark) u &= ~mark[wi];
-    if (wi == (p >> 5)) u &= ~(1u << (p & 31));
-    c += __popc(u);
-  }
-  uint32_t v = c;
-#pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, v, s);
-    if (lane >= (uint32_t)s) v += y;
-  }
-  lane_cnt = c;
-  incl = v;
-  return __shfl_sync(kFull, v, 31);
-}
-
-__device__ __forceinline__ uint32_t rlt_select(const uint32_t* leaf, const uint32_t* mark,
-                                               uint32_t nwords, uint32_t p, bool use_mark,
-                                               uint32_t lane, uint32_t lane_cnt, uint32_t incl,
-                                               uint32_t idx) {
-  const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
-  uint32_t slot = 0;
-  if (lane == owner) {
-    const uint32_t wpl = (nwords + 31) >> 5;
-    uint32_t rem = idx - (incl - lane_cnt);
-    for (uint32_t wi = lane * wpl;; ++wi) {
-      uint32_t u = leaf[wi];
-      if (use_mark) u &= ~mark[wi];
-      if (wi == (p >> 5)) u &= ~(1u << (p & 31));
-      const uint32_t pc = __popc(u);
-      if (rem < pc) {
-        slot = wi * 32 + select_bit(u, rem);
-        break;
-      }
-      rem -= pc;
-    }
-  }
-  return __shfl_sync(kFull, slot, owner);
 }
 
 __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
@@ -180,57 +143,305 @@ __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
   return b >= bins ? bins - 1 : (uint32_t)b;
 }
 
-template <typename Idx>
-__device__ __forceinline__ void list_unlink(const WorkerView<Idx>& S, Idx s, Idx& head, Idx& tail,
-                                            uint32_t lane) {
-  const Idx NIL = (Idx)~(Idx)0;
-  const Idx pr = S.prev[s], nx = S.next[s];
-  __syncwarp();
-  if (lane == 0) {
-    if (pr != NIL) S.next[pr] = nx;
-    if (nx != NIL) S.prev[nx] = pr;
+__device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
+
+// ------------------------------------------------------- Leaf-LRU recency log
+// entry = stamp << 32 | slot; valid iff stamp[slot] == entry stamp.  The first
+// e valid entries from the head are the e least-recently-used nodes in
+// (stamp, -depth) order because each query appends its path deepest first.
+struct RecencyLog {
+  uint64_t* log;
+  uint32_t* stamp;
+  uint32_t cap_mask;
+};
+
+// take the first `need` valid entries in [head, tail) as victims -> out[0..need);
+// returns the new head (just past the last victim)
+__device__ __noinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
+                                          uint32_t need, uint32_t* out, uint32_t lane) {
+  uint32_t k = 0, pos = head;
+#pragma unroll 1
+  while (k < need && pos < tail) {
+    const uint32_t idx = pos + lane;
+    const bool act = idx < tail;
+    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
+    const uint32_t slot = (uint32_t)ent;
+    const bool valid = act && R.stamp[slot] == (uint32_t)(ent >> 32);
+    const uint32_t bal = __ballot_sync(kFull, valid);
+    const uint32_t nv = __popc(bal);
+    const uint32_t take = min(nv, need - k);
+    const uint32_t rank = __popc(bal & lanemask_lt(lane));
+    if (valid && rank < take) out[k + rank] = slot;
+    k += take;
+    if (take > 0 && k == need) pos += select_bit(bal, take - 1) + 1u;   // through the last victim
+    else pos += 32u;
   }
   __syncwarp();
-  if (pr == NIL) head = nx;
-  if (nx == NIL) tail = pr;
+  return pos;
 }
 
-// insert s at the start of the current query's segment (the segment holds the
-// nodes touched by this query, deepest first, at the tail of the list)
-template <typename Idx>
-__device__ __forceinline__ void list_insert_seg(const WorkerView<Idx>& S, Idx s, Idx& head,
-                                                Idx& tail, Idx& seg, uint32_t lane) {
-  const Idx NIL = (Idx)~(Idx)0;
-  if (seg == NIL) {
-    const Idx t = tail;
-    __syncwarp();
-    if (lane == 0) {
-      S.prev[s] = t;
-      S.next[s] = NIL;
-      if (t != NIL) S.next[t] = s;
-    }
-    __syncwarp();
-    if (t == NIL) head = s;
-    tail = s;
-  } else {
-    const Idx pr = S.prev[seg];
-    __syncwarp();
-    if (lane == 0) {
-      S.prev[s] = pr;
-      S.next[s] = seg;
-      S.prev[seg] = s;
-      if (pr != NIL) S.next[pr] = s;
-    }
-    __syncwarp();
-    if (pr == NIL) head = s;
+// first valid entry from head (LRU over leaves != parent(t), fallback A5)
+__device__ __noinline__ uint32_t log_first_valid(const RecencyLog& R, uint32_t head, uint32_t tail,
+                                                 uint32_t lane) {
+#pragma unroll 1
+  for (;; head += 32) {
+    const uint32_t idx = head + lane;
+    const bool act = idx < tail;
+    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
+    const bool valid = act && R.stamp[(uint32_t)ent] == (uint32_t)(ent >> 32);
+    const uint32_t bal = __ballot_sync(kFull, valid);
+    if (bal) return (uint32_t)__shfl_sync(kFull, (uint32_t)ent, __ffs(bal) - 1);
   }
-  seg = s;
 }
+
+// in-place order-preserving compaction of [head, tail): returns the new tail
+__device__ __noinline__ uint32_t log_compact(const RecencyLog& R, uint32_t head, uint32_t tail,
+                                             uint32_t lane) {
+  uint32_t w = head;
+#pragma unroll 1
+  for (uint32_t r = head; r < tail; r += 32) {
+    const uint32_t idx = r + lane;
+    const bool act = idx < tail;
+    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
+    const bool valid = act && R.stamp[(uint32_t)ent] == (uint32_t)(ent >> 32);
+    const uint32_t bal = __ballot_sync(kFull, valid);
+    __syncwarp();
+    if (valid) R.log[(w + __popc(bal & lanemask_lt(lane))) & R.cap_mask] = ent;
+    w += __popc(bal);
+    __syncwarp();
+  }
+  return w;
+}
+
+// -------------------------------------------------------------- bitmaps (RLT)
+// Register-resident LEAF / MARK words: lane l holds word l (B <= 1024).
+struct RegBits {
+  uint32_t lw, mw;
+  __device__ __forceinline__ void load(const uint32_t* leaf, const uint32_t* mark, uint32_t nw,
+                                       uint32_t lane) {
+    lw = lane < nw ? leaf[lane] : 0u;
+    mw = lane < nw ? mark[lane] : 0u;
+  }
+  __device__ __forceinline__ void store(uint32_t* leaf, uint32_t* mark, uint32_t nw, uint32_t lane) {
+    if (lane < nw) {
+      leaf[lane] = lw;
+      mark[lane] = mw;
+    }
+  }
+  __device__ __forceinline__ void leaf_set(uint32_t s, uint32_t lane) { if (lane == (s >> 5)) lw |= 1u << (s & 31); }
+  __device__ __forceinline__ void leaf_clr(uint32_t s, uint32_t lane) { if (lane == (s >> 5)) lw &= ~(1u << (s & 31)); }
+  __device__ __forceinline__ void mark_set(uint32_t s, uint32_t lane) { if (lane == (s >> 5)) mw |= 1u << (s & 31); }
+  __device__ __forceinline__ void mark_clr(uint32_t s, uint32_t lane) { if (lane == (s >> 5)) mw &= ~(1u << (s & 31)); }
+  __device__ __forceinline__ bool mark_test(uint32_t s) const {
+    return (__shfl_sync(kFull, mw, s >> 5) >> (s & 31)) & 1u;
+  }
+  __device__ __forceinline__ void mark_clear_all_w(uint32_t) { mw = 0u; }
+  // |U| for U = LEAF (& ~MARK) minus bit p; per-lane count and inclusive scan
+  __device__ __forceinline__ uint32_t count(uint32_t p, bool use_mark, uint32_t lane, uint32_t& c,
+                                            uint32_t& incl) const {
+    uint32_t u = use_mark ? (lw & ~mw) : lw;
+    if (lane == (p >> 5)) u &= ~(1u << (p & 31));
+    c = __popc(u);
+    uint32_t v = c;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, v, s);
+      if (lane >= (uint32_t)s) v += y;
+    }
+    incl = v;
+    return __shfl_sync(kFull, v, 31);
+  }
+  __device__ __forceinline__ uint32_t select(uint32_t p, bool use_mark, uint32_t lane, uint32_t c,
+                                             uint32_t incl, uint32_t idx) const {
+    const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
+    uint32_t u = use_mark ? (lw & ~mw) : lw;
+    if (lane == (p >> 5)) u &= ~(1u << (p & 31));
+    const uint32_t rem = idx - (incl - c);
+    const uint32_t bit = (lane == owner) ? select_bit(u, rem) : 0u;
+    return __shfl_sync(kFull, lane * 32 + bit, owner);
+  }
+};
+
+// Memory-resident bitmaps (B > 1024): every lane scans a contiguous chunk of words.
+struct MemBits {
+  uint32_t* leaf;
+  uint32_t* mark;
+  uint32_t nw;
+  __device__ __forceinline__ void upd(uint32_t* a, uint32_t s, bool set, uint32_t lane) {
+    __syncwarp();
+    if (lane == 0) {
+      if (set) atomicOr(a + (s >> 5), 1u << (s & 31));
+      else atomicAnd(a + (s >> 5), ~(1u << (s & 31)));
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void leaf_set(uint32_t s, uint32_t lane) { upd(leaf, s, true, lane); }
+  __device__ __forceinline__ void leaf_clr(uint32_t s, uint32_t lane) { upd(leaf, s, false, lane); }
+  __device__ __forceinline__ void mark_set(uint32_t s, uint32_t lane) { upd(mark, s, true, lane); }
+  __device__ __forceinline__ void mark_clr(uint32_t s, uint32_t lane) { upd(mark, s, false, lane); }
+  __device__ __forceinline__ bool mark_test(uint32_t s) const { return (mark[s >> 5] >> (s & 31)) & 1u; }
+  __device__ __forceinline__ void mark_clear_all_w(uint32_t lane) {
+    __syncwarp();
+    for (uint32_t i = lane; i < nw; i += 32) mark[i] = 0u;
+    __syncwarp();
+  }
+  __device__ __forceinline__ uint32_t word(uint32_t wi, uint32_t p, bool use_mark) const {
+    uint32_t u = leaf[wi];
+    if (use_mark) u &= ~mark[wi];
+    if (wi == (p >> 5)) u &= ~(1u << (p & 31));
+    return u;
+  }
+  __device__ __forceinline__ uint32_t count(uint32_t p, bool use_mark, uint32_t lane, uint32_t& c,
+                                            uint32_t& incl) const {
+    const uint32_t wpl = (nw + 31) >> 5;
+    const uint32_t w0 = lane * wpl, w1 = min(nw, w0 + wpl);
+    uint32_t cc = 0;
+    for (uint32_t wi = w0; wi < w1; ++wi) cc += __popc(word(wi, p, use_mark));
+    uint32_t v = cc;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, v, s);
+      if (lane >= (uint32_t)s) v += y;
+    }
+    c = cc;
+    incl = v;
+    return __shfl_sync(kFull, v, 31);
+  }
+  __device__ __forceinline__ uint32_t select(uint32_t p, bool use_mark, uint32_t lane, uint32_t c,
+                                             uint32_t incl, uint32_t idx) const {
+    const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
+    uint32_t slot = 0;
+    if (lane == owner) {
+      const uint32_t wpl = (nw + 31) >> 5;
+      uint32_t rem = idx - (incl - c);
+      for (uint32_t wi = lane * wpl;; ++wi) {
+        const uint32_t u = word(wi, p, use_mark);
+        const uint32_t pc = __popc(u);
+        if (rem < pc) {
+          slot = wi * 32 + select_bit(u, rem);
+          break;
+        }
+        rem -= pc;
+      }
+    }
+    return __shfl_sync(kFull, slot, owner);
+  }
+};
+
+// Per-warp (worker) scalar and sequential state of one trial.
+struct WorkerRegs {
+  uint32_t size, cntT, used, wq, lhead, ltail;
+  uint64_t e;                      // RLT draw counter e_i
+  uint32_t c_ins, c_evict, c_draws, c_resets, c_fb;
+};
+
+// RLT misses of one chunk (Alg. 1 l.6-17, path order).  Serial over the
+// misses; lane r ends up holding the slot of miss cb + r.
+template <typename Bits, typename Idx>
+__device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, const RecencyLog& R,
+                                          WorkerRegs& wr, uint32_t B, uint32_t cnt, uint32_t cb,
+                                          Idx p0, uint32_t& pslot, uint32_t fallback,
+                                          bool use_list, uint64_t K, uint32_t worker,
+                                          uint64_t& rbuf, uint64_t& ebase, uint32_t lane,
+                                          uint32_t& my_slot, uint32_t& my_ev) {
+  const Idx NIL = Nil<Idx>::empty;
+#pragma unroll 1
+  for (uint32_t r = 0; r < cnt; ++r) {
+    const uint32_t q = cb + r;
+    // Alg. 1 l.6-9: mark t (t is not cached, hence not in T)
+    if (wr.cntT == B) {
+      bits.mark_clear_all_w(lane);
+      wr.cntT = 1;
+      ++wr.c_resets;
+    } else {
+      ++wr.cntT;
+    }
+    uint32_t slot, ev = 0;
+    if (wr.size < B) {
+      slot = wr.size++;
+    } else {
+      uint32_t c, incl;
+      bool use_mark = true, draw = true;
+      uint32_t total = bits.count(pslot, true, lane, c, incl);
+      uint32_t v = 0;
+      if (total == 0) {   // U = {} (A5)
+        ++wr.c_fb;
+        if (fallback == KVR_RLT_EARLY_RESET) {
+          bits.mark_clear_all_w(lane);
+          wr.cntT = 1;
+          ++wr.c_resets;
+        } else if (fallback == KVR_RLT_UNIFORM_LEAF) {
+          use_mark = false;
+        } else {
+          draw = false;
+          v = log_first_valid(R, wr.lhead, wr.ltail, lane);
+        }
+        if (draw) total = bits.count(pslot, use_mark, lane, c, incl);
+      }
+      if (draw) {
+        if (wr.e - ebase >= 32) {   // refill 32 counter-based draws, one per lane
+          ebase = wr.e;
+          rbuf = philox_r64(K, ebase + lane, worker, 1u);
+        }
+        const uint64_t rr = __shfl_sync(kFull, rbuf, (uint32_t)(wr.e - ebase));
+        ++wr.e;
+        ++wr.c_draws;
+        v = bits.select(pslot, use_mark, lane, c, incl, (uint32_t)pick_index(rr, total));
+      }
+      // Evict(S, v): parent loses a child (may become a leaf), v leaves T
+      const Idx pv = S.parent[v];
+      if (pv != NIL) {
+        const Idx nc = (Idx)(S.nchild[pv] - 1);
+        __syncwarp();
+        if (lane == 0) S.nchild[pv] = nc;
+        __syncwarp();
+        if (nc == 0) bits.leaf_set(pv, lane);
+      }
+      bits.leaf_clr(v, lane);
+      if (bits.mark_test(v)) {
+        bits.mark_clr(v, lane);
+        --wr.cntT;
+      }
+      ++wr.c_evict;
+      slot = v;
+      ev = 1;
+    }
+    // Load(S, t): new marked leaf; its parent stops being a leaf
+    bits.leaf_set(slot, lane);
+    bits.mark_set(slot, lane);
+    if (q == 0) {
+      if (p0 != NIL) {
+        const Idx nc = S.nchild[p0];
+        __syncwarp();
+        if (lane == 0) S.nchild[p0] = (Idx)(nc + 1);
+        __syncwarp();
+        if (nc == 0) bits.leaf_clr(p0, lane);
+      }
+    } else {
+      bits.leaf_clr(pslot, lane);
+    }
+    if (use_list) {   // LRU_MARKED fallback reads the log: stamp the reused slot now
+      __syncwarp();
+      if (lane == 0) R.stamp[slot] = wr.wq;
+      __syncwarp();
+    }
+    if (lane == r) {
+      my_slot = slot;
+      my_ev = ev;
+    }
+    pslot = slot;
+  }
+}
+
+// occupancy targets: 128 threads (W<=4) 4 CTAs/SM, 256 (W<=8) 3 CTAs/SM, else 1
+template <int kMaxThreads>
+struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 3 : 1); };
 
 template <typename Idx, bool kGlobal, int kMaxThreads>
-__global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_constant__ ReplayParams p) {
+__global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
+    replay_kernel(const __grid_constant__ ReplayParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const Idx NIL = (Idx)~(Idx)0;
+  const Idx NIL = Nil<Idx>::empty;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t W = p.W, B = p.B;
   const WorkerLayout& L = p.lay;
@@ -238,10 +449,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
 
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem);
   uint8_t* stage = smem + align16(sizeof(Ctrl));
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(stage + (size_t)kNumStages * p.stage_bytes +
+                                                  (size_t)w * p.scratch_bytes);
+  uint8_t* sbase = stage + (size_t)kNumStages * p.stage_bytes + (size_t)W * p.scratch_bytes;
   uint8_t* wbase = kGlobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
-                           : stage + (size_t)kNumStages * p.stage_bytes + (size_t)w * L.bytes;
+                           : sbase + (size_t)w * L.bytes;
   const WorkerView<Idx> S = make_view<Idx>(wbase, L);
-  double* fifo = reinterpret_cast<double*>(p.fifo + ((size_t)blockIdx.x * W + w) * p.ring * kFifoRecBytes);
+  uint8_t* abase = p.aux_base + ((size_t)blockIdx.x * W + w) * p.aux.bytes;
+  double* fifo = reinterpret_cast<double*>(abase + p.aux.off_fifo);
+  RecencyLog R;
+  R.log = reinterpret_cast<uint64_t*>(abase + p.aux.off_log);
+  R.stamp = reinterpret_cast<uint32_t*>(abase + p.aux.off_stamp);
+  R.cap_mask = p.aux.log_cap - 1;
 
   if (tid == 0) {
     for (uint32_t b = 0; b < kNumStages; ++b) mbar_init(&ctrl->mbar[b], 1);
@@ -250,6 +469,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
   __syncthreads();
 
   uint64_t gq = 0;   // queries staged by this CTA so far (drives buffer index and parity)
+#pragma unroll 1
   for (;;) {
     if (tid == 0) {
       const uint32_t tt = atomicAdd(p.work_counter, 1u);
@@ -267,6 +487,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
     const bool rlt = pol.eviction == KVR_EVICT_RLT;
     const bool use_list = !rlt || pol.rlt_fallback == KVR_RLT_LRU_MARKED;
     const bool lbgr = pol.router == KVR_ROUTE_LBGR;
+    const uint32_t router = pol.router, fallback = pol.rlt_fallback;
     const bool recorded = trial < p.record_trials;
     kvr_query_record* rec = recorded ? p.records + (size_t)trial * p.rec_stride : nullptr;
     uint64_t* vlog = (recorded && p.victims) ? p.victims + (size_t)trial * p.victims_per_trial : nullptr;
@@ -277,13 +498,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
       S.leaf[i] = 0;
       S.mark[i] = 0;
     }
-    uint32_t size = 0, cntT = 0, fh = 0, fn = 0;
-    Idx head = NIL, tail = NIL;
-    double P = 0.0, F = 0.0, Pt = 0.0, front_c = 0.0;
+    if (use_list)
+      for (uint32_t i = lane; i < B; i += 32) R.stamp[i] = 0;
+    WorkerRegs wr;
+    wr.size = 0; wr.cntT = 0; wr.used = 0; wr.wq = 0; wr.lhead = 0; wr.ltail = 0; wr.e = 0;
+    wr.c_ins = 0; wr.c_evict = 0; wr.c_draws = 0; wr.c_resets = 0; wr.c_fb = 0;
+    uint32_t fh = 0, fn = 0, c_q = 0, c_maxp = 0;
+    uint64_t c_probes = 0, c_hit = 0, c_in = 0;
+    double P = 0.0, F = 0.0, Pt = 0.0;
     double th0 = pol.theta0[0], th1 = pol.theta0[1], th2 = pol.theta0[2], th3 = pol.theta0[3];
-    uint64_t k = 0, e = 0;
-    uint64_t c_probes = 0, c_ins = 0, c_evict = 0, c_draws = 0, c_resets = 0, c_fb = 0;
-    uint64_t c_hit = 0, c_in = 0, c_q = 0, c_maxp = 0;
+    uint64_t k = 0;
+    // front record of the pending FIFO, prefetched into registers
+    double fr_c = 0, fr_a = 0, fr_E = 0, fr_f0 = 0, fr_f1 = 0, fr_f2 = 0, fr_C = 0;
+    uint64_t fr_ka = 0;
+    uint64_t rbuf = 0, ebase = ~0ull >> 1;
     if (tid == 0) {
       ctrl->sum_lat = 0.0;
       ctrl->sum_ttft = 0.0;
@@ -302,9 +530,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
                         pol.router <= KVR_ROUTE_RANDOM && pol.rho > 0.0 && pol.rho <= 1.0 &&
                         pol.delta_t_ms > 0.0;
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
+    const uint32_t Nrun = pol_ok ? N : 0;
 
     // staging prologue: queries 0 .. kNumStages-2
-    const uint32_t Nrun = pol_ok ? N : 0;
     uint32_t issued = min(Nrun, kNumStages - 1);
     uint64_t pf_off = 0;
     uint32_t pf_n = 0;
@@ -330,6 +558,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
     __syncthreads();
 
     uint32_t consumed = 0;
+#pragma unroll 1
     for (uint32_t j = 0; j < Nrun; ++j) {
       const uint64_t g = gq + j;
       const uint32_t buf = (uint32_t)(g % kNumStages);
@@ -343,58 +572,65 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
       const uint32_t q = bt * n_in;
 
       // ---- 1. catch-up (A11: tick before completion before routing) ----
-      for (;;) {
-        if (lbgr) {
-          const double tau = (double)(k + 1) * pol.delta_t_ms;
-          if (tau <= a && (fn == 0 || tau <= front_c)) {
-            Pt = pol.rho * Pt;
-            ++k;
+      {
+        const double rho = pol.rho, dt = pol.delta_t_ms;
+#pragma unroll 1
+        for (;;) {
+          if (lbgr) {
+            const double tau = (double)(k + 1) * dt;
+            if (tau <= a && (fn == 0 || tau <= fr_c)) {
+              Pt = rho * Pt;
+              ++k;
+              continue;
+            }
+          }
+          if (fn != 0 && fr_c <= a) {
+            fh = (fh + 1 == p.ring) ? 0 : fh + 1;
+            --fn;
+            if (lbgr) {
+              // OnlineUpdate (A8): NLMS on the squared residual
+              const double E = fr_c - fr_a;
+              const double res = E - fr_E;
+              const double f3 = 1.0;
+              double s = fr_f0 * fr_f0;
+              s = s + fr_f1 * fr_f1;
+              s = s + fr_f2 * fr_f2;
+              s = s + f3 * f3;
+              const double gstep = (pol.mu * res) / (1.0 + s);
+              th0 = th0 + gstep * fr_f0;
+              th1 = th1 + gstep * fr_f1;
+              th2 = th2 + gstep * fr_f2;
+              th3 = th3 + gstep * f3;
+              // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
+              uint64_t kap = k - fr_ka;
+              double pw = 1.0, bb = rho;
+#pragma unroll 1
+              while (kap) {
+                if (kap & 1) pw = pw * bb;
+                bb = bb * bb;
+                kap >>= 1;
+              }
+              Pt = Pt - fr_C * pw;
+              if (Pt < 0.0) Pt = 0.0;
+            }
+            if (fn) {
+              const double* r = fifo + (size_t)fh * 8;
+              fr_c = r[0]; fr_a = r[1]; fr_E = r[2]; fr_f0 = r[3]; fr_f1 = r[4]; fr_f2 = r[5];
+              fr_C = r[6]; fr_ka = (uint64_t)__double_as_longlong(r[7]);
+            }
             continue;
           }
+          break;
         }
-        if (fn != 0 && front_c <= a) {
-          const double* r = fifo + (size_t)fh * 8;
-          fh = (fh + 1 == p.ring) ? 0 : fh + 1;
-          --fn;
-          if (lbgr) {
-            const double rc = r[0], ra = r[1], rE = r[2], f0 = r[3], f1 = r[4], f2 = r[5], rC = r[6];
-            const uint64_t ka = __double_as_longlong(r[7]);
-            // OnlineUpdate (A8): NLMS on the squared residual
-            const double E = rc - ra;
-            const double res = E - rE;
-            const double f3 = 1.0;
-            double s = f0 * f0;
-            s = s + f1 * f1;
-            s = s + f2 * f2;
-            s = s + f3 * f3;
-            const double gstep = (pol.mu * res) / (1.0 + s);
-            th0 = th0 + gstep * f0;
-            th1 = th1 + gstep * f1;
-            th2 = th2 + gstep * f2;
-            th3 = th3 + gstep * f3;
-            // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
-            uint64_t kap = k - ka;
-            double pw = 1.0, bb = pol.rho;
-            while (kap) {
-              if (kap & 1) pw = pw * bb;
-              bb = bb * bb;
-              kap >>= 1;
-            }
-            Pt = Pt - rC * pw;
-            if (Pt < 0.0) Pt = 0.0;
-          }
-          if (fn) front_c = fifo[(size_t)fh * 8];
-          continue;
-        }
-        break;
       }
 
       // ---- 2. longest cached prefix over the input (ballot of 32 probes) ----
       uint32_t m = 0;
+#pragma unroll 1
       for (uint32_t base = 0; base < n_in; base += 32) {
         const uint32_t d = base + lane;
         bool hit = false;
-        if (d < n_in) hit = table_lookup<Idx>(S, tmask, H[d]) != NIL;
+        if (d < n_in) hit = tbl_find<Idx>(S, tmask, H[d]) != NIL;
         const uint32_t bal = __ballot_sync(kFull, hit);
         if (bal == kFull) {
           m = base + 32;
@@ -420,7 +656,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
         dd = dd + th2 * f2;
         dd = dd + th3 * f3;
         score = (Chat + Pt) + dd;
-      } else if (pol.router == KVR_ROUTE_STATIC_LINEAR) {
+      } else if (router == KVR_ROUTE_STATIC_LINEAR) {
         score = (pol.w_load * (double)fn) - (pol.w_hit * (x / (double)q));
       }
       const uint32_t par = j & 1;
@@ -451,7 +687,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
 
       // ---- 4. argmin over workers (every warp computes the same i*) ----
       uint32_t best = 0;
-      if (pol.router == KVR_ROUTE_LBGR || pol.router == KVR_ROUTE_STATIC_LINEAR) {
+      if (router == KVR_ROUTE_LBGR || router == KVR_ROUTE_STATIC_LINEAR) {
         double v = lane < W ? ctrl->score[par][lane] : INFINITY;
         uint32_t bi = lane;
 #pragma unroll
@@ -464,7 +700,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
           }
         }
         best = bi;
-      } else if (pol.router == KVR_ROUTE_THRESHOLD) {   // A16
+      } else if (router == KVR_ROUTE_THRESHOLD) {   // A16
         const uint32_t np = lane < W ? ctrl->npend[par][lane] : 0xffffffffu;
         const uint32_t mh = lane < W ? ctrl->mhit[par][lane] : 0u;
         const uint32_t mx = __reduce_max_sync(kFull, lane < W ? np : 0u);
@@ -475,7 +711,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
           const uint32_t mmax = __reduce_max_sync(kFull, mh);
           best = __ffs(__ballot_sync(kFull, lane < W && mh == mmax)) - 1;
         }
-      } else if (pol.router == KVR_ROUTE_ROUND_ROBIN) {
+      } else if (router == KVR_ROUTE_ROUND_ROBIN) {
         best = j % W;
       } else {
         best = (uint32_t)pick_index(philox_r64(K, j, 0xffffffffu, 2u), W);
@@ -491,21 +727,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
         }
         continue;
       }
-      uint64_t D = ctrl->digest;
-      D = fmix64(D ^ (uint64_t)j);
-      D = fmix64(D ^ (uint64_t)best);
-      D = fmix64(D ^ (uint64_t)m);
-      uint64_t vc = ctrl->vcursor;
-      const uint64_t vc0 = vc;
-      uint32_t nv = 0;
+      ++wr.wq;
+      // log room for this query's n entries (Leaf-LRU order)
+      if (use_list && wr.ltail - wr.lhead + n > p.aux.log_cap)
+        wr.ltail = log_compact(R, wr.lhead, wr.ltail, lane);
+      const uint32_t ltail0 = wr.ltail;
 
       // full-path cached prefix kf (hits of Gamma_j; m covers the input part)
       uint32_t kf = m;
       if (m == n_in) {
+#pragma unroll 1
         for (uint32_t base = n_in; base < n; base += 32) {
           const uint32_t d = base + lane;
           bool hit = false;
-          if (d < n) hit = table_lookup<Idx>(S, tmask, H[d]) != NIL;
+          if (d < n) hit = tbl_find<Idx>(S, tmask, H[d]) != NIL;
           const uint32_t bal = __ballot_sync(kFull, hit);
           if (bal == kFull) {
             kf = base + 32;
@@ -517,142 +752,130 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
         if (kf > n) kf = n;
       }
 
-      Idx seg = NIL;
-      Idx pslot = NIL;
-      for (uint32_t base = 0; base < n; base += 32) {
-        const uint32_t d0 = base + lane;
-        Idx myslot = NIL;
-        if (d0 < kf) myslot = table_lookup<Idx>(S, tmask, H[d0]);
-        const uint32_t cnt = min(32u, n - base);
-        for (uint32_t l = 0; l < cnt; ++l) {
-          const uint32_t d = base + l;
-          if (d < kf) {
-            // ---- hit (Alg. 1 l.10-11): mark, refresh recency ----
-            const Idx s = (Idx)__shfl_sync(kFull, (uint32_t)myslot, l);
-            if (rlt && !bit_test(S.mark, s)) {
-              if (cntT == B) {   // |T|+1 = B+1 -> T = {t} (Alg. 1 l.8-9)
-                __syncwarp();
-                for (uint32_t i = lane; i < nwords; i += 32) S.mark[i] = 0;
-                __syncwarp();
-                cntT = 1;
-                ++c_resets;
-              } else {
-                ++cntT;
-              }
-              bit_set(S.mark, s, lane);
-            }
-            if (use_list) {
-              list_unlink<Idx>(S, s, head, tail, lane);
-              list_insert_seg<Idx>(S, s, head, tail, seg, lane);
-            }
-            pslot = s;
-            continue;
-          }
-          // ---- miss: mark t, evict if full, load t ----
-          const uint64_t t = H[d];
-          if (rlt) {
-            if (cntT == B) {
-              __syncwarp();
-              for (uint32_t i = lane; i < nwords; i += 32) S.mark[i] = 0;
-              __syncwarp();
-              cntT = 1;
-              ++c_resets;
-            } else {
-              ++cntT;
-            }
-          }
-          Idx slot;
-          if (size == B) {
-            Idx v;
-            if (!rlt) {
-              v = head;   // Leaf-LRU: least recent (stamp, -depth) is the list head (A7)
-            } else {
-              uint32_t lc, inc;
-              bool use_mark = true;
-              uint32_t total = rlt_count(S.leaf, S.mark, nwords, (uint32_t)pslot, true, lane, lc, inc);
-              bool draw = true;
-              if (total == 0) {   // U empty (A5)
-                ++c_fb;
-                if (pol.rlt_fallback == KVR_RLT_EARLY_RESET) {
-                  __syncwarp();
-                  for (uint32_t i = lane; i < nwords; i += 32) S.mark[i] = 0;
-                  __syncwarp();
-                  cntT = 1;
-                  ++c_resets;
-                } else if (pol.rlt_fallback == KVR_RLT_UNIFORM_LEAF) {
-                  use_mark = false;
-                } else {
-                  draw = false;
-                }
-                if (draw)
-                  total = rlt_count(S.leaf, S.mark, nwords, (uint32_t)pslot, use_mark, lane, lc, inc);
-              }
-              if (draw) {
-                const uint64_t r = philox_r64(K, e, best, 1u);
-                ++e;
-                ++c_draws;
-                const uint32_t idx = (uint32_t)pick_index(r, total);
-                v = (Idx)rlt_select(S.leaf, S.mark, nwords, (uint32_t)pslot, use_mark, lane, lc, inc, idx);
-              } else {
-                v = head;   // LRU over leaves != parent(t) = list head
-              }
-            }
-            // ---- Evict(S, v) ----
-            const uint64_t vkey = S.key[v];
-            table_delete<Idx>(S, tmask, vkey, v, lane);
-            if (use_list) list_unlink<Idx>(S, v, head, tail, lane);
-            const Idx pv = S.parent[v];
-            if (pv != NIL) {
-              const Idx nc = (Idx)(S.nchild[pv] - 1);
-              __syncwarp();
-              if (lane == 0) S.nchild[pv] = nc;
-              __syncwarp();
-              if (nc == 0) bit_set(S.leaf, pv, lane);
-            }
-            bit_clear(S.leaf, v, lane);
-            if (rlt && bit_test(S.mark, v)) {
-              bit_clear(S.mark, v, lane);
-              --cntT;
-            }
-            ++c_evict;
-            D = fmix64(D ^ vkey);
-            if (vlog) {
-              if (vc < p.victims_per_trial) {
-                if (lane == 0) vlog[vc] = vkey;
-              } else if (lane == 0) {
-                atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
-              }
-            }
-            ++vc;
-            ++nv;
-            slot = v;
-          } else {
-            slot = (Idx)size;
-            ++size;
-          }
-          // ---- Load(S, t) ----
-          __syncwarp();
-          if (lane == 0) {
-            S.key[slot] = t;
-            S.parent[slot] = pslot;
-            S.nchild[slot] = 0;
-          }
-          __syncwarp();
-          bit_set(S.leaf, slot, lane);
-          if (pslot != NIL) {
-            const Idx nc = S.nchild[pslot];
-            __syncwarp();
-            if (lane == 0) S.nchild[pslot] = (Idx)(nc + 1);
-            __syncwarp();
-            if (nc == 0) bit_clear(S.leaf, pslot, lane);
-          }
-          if (rlt) bit_set(S.mark, slot, lane);
-          table_insert<Idx>(S, tmask, t, slot, lane);
-          if (use_list) list_insert_seg<Idx>(S, slot, head, tail, seg, lane);
-          ++c_ins;
-          pslot = slot;
+      // ---- hits: marks (Alg. 1 l.6-9), recency stamps, log entries ----
+      Idx p0 = NIL;
+#pragma unroll 1
+      for (uint32_t base = 0; base < kf; base += 32) {
+        const uint32_t d = base + lane;
+        const bool act = d < kf;
+        const Idx s = act ? tbl_find<Idx>(S, tmask, H[d]) : NIL;
+        if (act && use_list) {
+          R.stamp[s] = wr.wq;
+          R.log[(ltail0 + (n - 1 - d)) & R.cap_mask] = ((uint64_t)wr.wq << 32) | (uint32_t)s;
         }
+        if (rlt) {
+          const bool um = act && !((S.mark[(uint32_t)s >> 5] >> ((uint32_t)s & 31)) & 1u);
+          const uint32_t u = __ballot_sync(kFull, um);
+          const uint32_t need = B + 1 - wr.cntT;   // the need-th unmarked hit resets T
+          const uint32_t nact = min(32u, kf - base);
+          if ((uint32_t)__popc(u) >= need) {
+            const uint32_t rr = select_bit(u, need - 1);
+            __syncwarp();
+            for (uint32_t i = lane; i < nwords; i += 32) S.mark[i] = 0u;
+            __syncwarp();
+            if (act && lane >= rr) atomicOr(&S.mark[(uint32_t)s >> 5], 1u << ((uint32_t)s & 31));
+            wr.cntT = nact - rr;
+            ++wr.c_resets;
+          } else {
+            if (um) atomicOr(&S.mark[(uint32_t)s >> 5], 1u << ((uint32_t)s & 31));
+            wr.cntT += __popc(u);
+          }
+        }
+        p0 = (Idx)__shfl_sync(kFull, (uint32_t)s, min(31u, kf - 1 - base));
       }
+      __syncwarp();
+
+      // ---- misses: victims, then lane-parallel apply, 32 misses per chunk ----
+      const uint32_t M = n - kf;
+      const uint32_t size0 = wr.size;
+      const uint32_t nfree = B - size0;
+      const uint32_t nev = M > nfree ? M - nfree : 0u;
+      if (!rlt && nev) {   // Leaf-LRU: the nev least recently used nodes, in order
+        wr.lhead = log_take(R, wr.lhead, ltail0, nev, scratch, lane);
+      }
+      RegBits rb;
+      MemBits mb;
+      mb.leaf = S.leaf;
+      mb.mark = S.mark;
+      mb.nw = nwords;
+      const bool regbits = nwords <= 32;
+      __syncwarp();
+      if (rlt && regbits && M) rb.load(S.leaf, S.mark, nwords, lane);
+      uint64_t V = 0;
+      uint32_t pslot = (uint32_t)p0, prev_last = (uint32_t)p0;
+      const uint64_t vc = ctrl->vcursor;
+      uint32_t used_add = 0;
+#pragma unroll 1
+      for (uint32_t cb = 0; cb < M; cb += 32) {
+        const uint32_t cnt = min(32u, M - cb);
+        uint32_t my_slot = 0, my_ev = 0;
+        if (rlt) {
+          if (regbits)
+            rlt_chunk<RegBits, Idx>(rb, S, R, wr, B, cnt, cb, p0, pslot, fallback, use_list, K,
+                                    best, rbuf, ebase, lane, my_slot, my_ev);
+          else
+            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, cnt, cb, p0, pslot, fallback, use_list, K,
+                                    best, rbuf, ebase, lane, my_slot, my_ev);
+        } else {
+          const uint32_t qq = cb + lane;
+          if (qq < nfree) {
+            my_slot = size0 + qq;
+          } else if (lane < cnt) {
+            my_slot = scratch[qq - nfree];
+            my_ev = 1;
+          }
+        }
+        // lane-parallel apply of this chunk
+        const uint32_t qq = cb + lane;
+        const bool act = lane < cnt;
+        const uint64_t t = act ? H[kf + qq] : 0ull;
+        __syncwarp();
+        if (act && my_ev) {
+          const uint64_t vkey = S.key[my_slot];
+          tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
+          V ^= fmix64(vkey ^ ((uint64_t)(qq - nfree + 1) * kPosMul));
+          if (vlog) {
+            const uint64_t vi = vc + (qq - nfree);
+            if (vi < p.victims_per_trial) vlog[vi] = vkey;
+          }
+        }
+        const uint32_t up = __shfl_up_sync(kFull, my_slot, 1);
+        const uint32_t par_slot = lane == 0 ? prev_last : up;
+        __syncwarp();
+        if (act) {
+          S.key[my_slot] = t;
+          if (rlt) {
+            S.parent[my_slot] = (Idx)par_slot;
+            S.nchild[my_slot] = (Idx)(qq + 1 < M ? 1 : 0);
+          }
+          if (use_list) {
+            if (!rlt) R.stamp[my_slot] = wr.wq;
+            R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] =
+                ((uint64_t)wr.wq << 32) | my_slot;
+          }
+        }
+        __syncwarp();
+        const uint32_t claimed = act ? tbl_insert<Idx>(S, tmask, t, (Idx)my_slot) : 0u;
+        used_add += __popc(__ballot_sync(kFull, claimed != 0));
+        prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
+        pslot = prev_last;
+        __syncwarp();
+      }
+      if (!rlt) {
+        wr.size = min(B, size0 + M);
+        wr.c_evict += nev;
+      }
+      if (rlt && regbits && M) rb.store(S.leaf, S.mark, nwords, lane);
+      wr.c_ins += M;
+      wr.used += used_add;
+      if (use_list) wr.ltail = ltail0 + n;
+      if (wr.used > (L.T >> 2) * 3) {
+        tbl_rebuild<Idx>(S, L.T, wr.size, lane);
+        wr.used = wr.size;
+      }
+      // order-sensitive victim combination V (XOR over lanes)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
 
       // ---- accounting: Eq. 1 truth, Eq. 2, FIFO single server (A12, A20) ----
       const uint32_t h = bt * m;
@@ -669,20 +892,24 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
       {
         const uint32_t slotf = (fh + fn >= p.ring) ? fh + fn - p.ring : fh + fn;
         double* r = fifo + (size_t)slotf * 8;
+        const double rE = lbgr ? score : 0.0, r0 = lbgr ? f0 : 0.0, r1 = lbgr ? f1 : 0.0,
+                     r2 = lbgr ? f2 : 0.0, rC = lbgr ? Chat : 0.0;
         double val = 0.0;
         switch (lane) {
           case 0: val = comp; break;
           case 1: val = a; break;
-          case 2: val = lbgr ? score : 0.0; break;
-          case 3: val = lbgr ? f0 : 0.0; break;
-          case 4: val = lbgr ? f1 : 0.0; break;
-          case 5: val = lbgr ? f2 : 0.0; break;
-          case 6: val = lbgr ? Chat : 0.0; break;
+          case 2: val = rE; break;
+          case 3: val = r0; break;
+          case 4: val = r1; break;
+          case 5: val = r2; break;
+          case 6: val = rC; break;
           case 7: val = __longlong_as_double((long long)k); break;
           default: break;
         }
         if (lane < 8) r[lane] = val;
-        if (fn == 0) front_c = comp;
+        if (fn == 0) {
+          fr_c = comp; fr_a = a; fr_E = rE; fr_f0 = r0; fr_f1 = r1; fr_f2 = r2; fr_C = rC; fr_ka = k;
+        }
         ++fn;
         if (fn > c_maxp) c_maxp = fn;
       }
@@ -690,24 +917,31 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
       c_hit += h;
       c_in += q;
       ++c_q;
-      D = fmix64(D ^ (uint64_t)nv);
       if (lane == 0) {
+        uint64_t D = ctrl->digest;   // decision digest
+        D = fmix64(D ^ (uint64_t)j);
+        D = fmix64(D ^ (uint64_t)best);
+        D = fmix64(D ^ (uint64_t)m);
+        D = fmix64(D ^ (uint64_t)nev);
+        D = fmix64(D ^ V);
+        ctrl->digest = D;
         ctrl->sum_lat = ctrl->sum_lat + lat;
         ctrl->sum_ttft = ctrl->sum_ttft + ttft;
         if (lat > ctrl->max_lat) ctrl->max_lat = lat;
-        ctrl->digest = D;
-        ctrl->vcursor = vc;
+        ctrl->vcursor = vc + nev;
+        if (vlog && vc + nev > p.victims_per_trial)
+          atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
         if (rec) {
-          kvr_query_record R;
-          R.worker = best;
-          R.hit_tokens = h;
-          R.n_victims = nv;
-          R._pad = 0;
-          R.ttft_ms = ttft;
-          R.latency_ms = lat;
-          R.score = (lbgr || pol.router == KVR_ROUTE_STATIC_LINEAR) ? score : 0.0;
-          R.victim_offset = vc0;
-          rec[j] = R;
+          kvr_query_record Rq;
+          Rq.worker = best;
+          Rq.hit_tokens = h;
+          Rq.n_victims = nev;
+          Rq._pad = 0;
+          Rq.ttft_ms = ttft;
+          Rq.latency_ms = lat;
+          Rq.score = (lbgr || router == KVR_ROUTE_STATIC_LINEAR) ? score : 0.0;
+          Rq.victim_offset = vc;
+          rec[j] = Rq;
         }
         if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
       }
@@ -724,11 +958,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
     gq += issued;
     if (lane == 0) {
       atomicAdd(&ctrl->cnt[0], (unsigned long long)c_probes);
-      atomicAdd(&ctrl->cnt[1], (unsigned long long)c_ins);
-      atomicAdd(&ctrl->cnt[2], (unsigned long long)c_evict);
-      atomicAdd(&ctrl->cnt[3], (unsigned long long)c_draws);
-      atomicAdd(&ctrl->cnt[4], (unsigned long long)c_resets);
-      atomicAdd(&ctrl->cnt[5], (unsigned long long)c_fb);
+      atomicAdd(&ctrl->cnt[1], (unsigned long long)wr.c_ins);
+      atomicAdd(&ctrl->cnt[2], (unsigned long long)wr.c_evict);
+      atomicAdd(&ctrl->cnt[3], (unsigned long long)wr.c_draws);
+      atomicAdd(&ctrl->cnt[4], (unsigned long long)wr.c_resets);
+      atomicAdd(&ctrl->cnt[5], (unsigned long long)wr.c_fb);
       atomicAdd(&ctrl->cnt[6], (unsigned long long)c_hit);
       atomicAdd(&ctrl->cnt[7], (unsigned long long)c_in);
       atomicAdd(&ctrl->cnt[8], (unsigned long long)c_q);
@@ -738,33 +972,33 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
     }
     __syncthreads();
     if (tid == 0) {
-      kvr_trial_result R;
-      R.probes = ctrl->cnt[0];
-      R.inserted_blocks = ctrl->cnt[1];
-      R.evictions = ctrl->cnt[2];
-      R.rlt_draws = ctrl->cnt[3];
-      R.rlt_resets = ctrl->cnt[4];
-      R.rlt_fallbacks = ctrl->cnt[5];
-      R.hit_tokens = ctrl->cnt[6];
-      R.input_tokens = ctrl->cnt[7];
-      R.queries = ctrl->cnt[8];
-      R.max_pending = ctrl->cnt[9];
-      R.decision_digest = ctrl->digest;
-      R.sum_latency_ms = ctrl->sum_lat;
-      R.sum_ttft_ms = ctrl->sum_ttft;
-      R.max_latency_ms = ctrl->max_lat;
+      kvr_trial_result Rr;
+      Rr.probes = ctrl->cnt[0];
+      Rr.inserted_blocks = ctrl->cnt[1];
+      Rr.evictions = ctrl->cnt[2];
+      Rr.rlt_draws = ctrl->cnt[3];
+      Rr.rlt_resets = ctrl->cnt[4];
+      Rr.rlt_fallbacks = ctrl->cnt[5];
+      Rr.hit_tokens = ctrl->cnt[6];
+      Rr.input_tokens = ctrl->cnt[7];
+      Rr.queries = ctrl->cnt[8];
+      Rr.max_pending = ctrl->cnt[9];
+      Rr.decision_digest = ctrl->digest;
+      Rr.sum_latency_ms = ctrl->sum_lat;
+      Rr.sum_ttft_ms = ctrl->sum_ttft;
+      Rr.max_latency_ms = ctrl->max_lat;
       double mk = 0.0, lc = 0.0, sl = 0.0;
       for (uint32_t i = 0; i < W; ++i) {   // makespan max_i P_i, in worker order
         if (ctrl->P[i] > mk) mk = ctrl->P[i];
         if (ctrl->F[i] > lc) lc = ctrl->F[i];
         sl = sl + ctrl->P[i];
       }
-      R.makespan_ms = mk;
-      R.last_completion_ms = lc;
-      R.sum_load_ms = sl;
-      R.status = (int32_t)ctrl->status;
-      R._pad = 0;
-      p.results[trial] = R;
+      Rr.makespan_ms = mk;
+      Rr.last_completion_ms = lc;
+      Rr.sum_load_ms = sl;
+      Rr.status = (int32_t)ctrl->status;
+      Rr._pad = 0;
+      p.results[trial] = Rr;
     }
     if (p.hist)
       for (uint32_t b = tid; b < p.bins; b += blockDim.x)
@@ -775,10 +1009,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) replay_kernel(const __grid_con
 
 static const void* kernel_for(uint32_t tier, uint32_t W) {
   if (tier == 1) {
+    if (W <= 4) return (const void*)replay_kernel<uint16_t, false, 128>;
     if (W <= 8) return (const void*)replay_kernel<uint16_t, false, 256>;
     if (W <= 16) return (const void*)replay_kernel<uint16_t, false, 512>;
     return (const void*)replay_kernel<uint16_t, false, 1024>;
   }
+  if (W <= 4) return (const void*)replay_kernel<uint32_t, true, 128>;
   if (W <= 8) return (const void*)replay_kernel<uint32_t, true, 256>;
   if (W <= 16) return (const void*)replay_kernel<uint32_t, true, 512>;
   return (const void*)replay_kernel<uint32_t, true, 1024>;

@@ -7,17 +7,18 @@ lengths, output sizes and arrival times, shaped like the paper's workloads
 (``kvr_trace_load``) and the CPU oracle (``kvro_chain`` / ``kvro_run``)
 consume the same ``RawTrace``; each side chains the keys itself.
 
-Recipes (scaled ×1/2 so that every complete path fits a 512-block cache, A1):
+Recipes (token lengths scaled x1/4 so that a 512-block cache holds tens of queries,
+as the paper's 200k-token cache does):
 
 * ``gsp``    Generated Shared Prefix: group g has length
-             {256,512,1024,2048,4096}[g mod 5] tokens, the first
+             {128,256,512,1024,2048}[g mod 5] tokens, the first
              floor(ceil(r*len)/16) blocks shared by the group, the rest unique.
 * ``mt``     multi-turn (ShareGPT / UltraChat shaped): client c has
              {2,4,6,8}[c mod 4] rounds; all clients share a floor(32*r)-block
              system prompt; round k's input is the previous complete path plus
-             32 new blocks (512 tokens); rounds stay in order, clients interleave.
+             16 new blocks (256 tokens); rounds stay in order, clients interleave.
 * ``ld``     long-document QA (Loogle shaped): doc d has
-             {512,1024,2048,4096}[d mod 4] tokens; Q_d questions of 4 unique
+             {256,512,1024,2048}[d mod 4] tokens; Q_d questions of 4 unique
              blocks each.
 * ``drift``  drifting popularity (config 3, "evolving patterns" P:10): group
              rank ~ Zipf(s) over G groups, the rank->group map rotates by G/64
@@ -40,8 +41,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 BLOCK_TOKENS = 16
-GSP_LENGTHS = (256, 512, 1024, 2048, 4096)
-LD_LENGTHS = (512, 1024, 2048, 4096)
+GSP_LENGTHS = (128, 256, 512, 1024, 2048)
+LD_LENGTHS = (256, 512, 1024, 2048)
 MT_ROUNDS = (2, 4, 6, 8)
 
 
@@ -177,7 +178,7 @@ def ld(docs: int, questions: int, seed: int, W: int = 4, util: float = 0.8,
 
 
 def mt(clients: int, ratio: float, seed: int, W: int = 4, util: float = 0.8,
-       user_blocks: int = 32, out_tokens: int = 4, rounds: Sequence[int] = MT_ROUNDS,
+       user_blocks: int = 16, out_tokens: int = 4, rounds: Sequence[int] = MT_ROUNDS,
        name: str = "mt") -> RawTrace:
     rng = _rng(seed)
     sp = int(np.floor(32 * ratio))

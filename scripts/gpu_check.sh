@@ -1,6 +1,6 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -40 > gpurun_out/t1_tests.log
-tail -5 gpurun_out/t1_tests.log
-timeout 300 python __graft_entry__.py smoke > gpurun_out/t1_smoke.log 2>&1; tail -3 gpurun_out/t1_smoke.log
-timeout 600 python bench.py --queries 20000 --trials 1024 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/t1_bench.log 2>&1; tail -5 gpurun_out/t1_bench.log
+# usage: bash scripts/gpu_check.sh [tag]   (runs on the GPU box)
+tag=${1:-t}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 900 python -m pytest tests/ -x -q -m gpu > gpurun_out/${tag}_tests.log 2>&1; tail -3 gpurun_out/${tag}_tests.log
+timeout 300 python __graft_entry__.py smoke > gpurun_out/${tag}_smoke.log 2>&1; tail -2 gpurun_out/${tag}_smoke.log
+timeout 900 python bench.py > gpurun_out/${tag}_bench.log 2>&1; tail -3 gpurun_out/${tag}_bench.log
