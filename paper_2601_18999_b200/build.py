@@ -31,27 +31,34 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "kvr.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
+PROF_LIB = os.path.join(PKG, "libkvr_prof.so")
+
+
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """libkvr.so; with profile=True the phase-profiling variant libkvr_prof.so
+    (-DKVR_PHASE_PROFILE, clock64 per replay phase; used by scripts/, never by tests)."""
+    lib = PROF_LIB if profile else LIB
+    if not force and not stale(lib):
+        return lib
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"]
+    if profile:
+        cmd.append("-DKVR_PHASE_PROFILE")
     cmd += [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

@@ -48,8 +48,8 @@ struct WorkerLayout {
 inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   WorkerLayout L{};
   L.B = B;
-  uint32_t T = 2;
-  while (T < 2 * B) T <<= 1;     // load factor <= 1/2 (tombstones rebuilt at 3/4)
+  uint32_t T = 4;
+  while (T < 4 * B) T <<= 1;     // live load <= 1/4; rebuilt when live + tombstones > 1/2
   L.T = T;
   L.nwords = (B + 31) / 32;
   L.idx_bytes = idx_bytes;
@@ -139,5 +139,7 @@ cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, 
 cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W);
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
                           cudaStream_t s);
+// phase profiler (profiling build, -DKVR_PHASE_PROFILE); cudaErrorNotSupported otherwise
+cudaError_t phase_cycles(unsigned long long* out16, int reset);
 
 }  // namespace kvr

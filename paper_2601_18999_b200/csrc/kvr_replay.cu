@@ -33,6 +33,22 @@
 
 namespace kvr {
 
+#ifdef KVR_PHASE_PROFILE
+// Phase profiler (profiling build only): cycles per phase summed over warps,
+// phases >= 5 only for the chosen warp i*.
+__device__ unsigned long long g_phase_cycles[16];
+#define KVR_T0(v) unsigned long long v = clock64()
+#define KVR_ACC(ph, v)                                                     \
+  do {                                                                     \
+    unsigned long long _n = clock64();                                     \
+    if (lane == 0) atomicAdd(&g_phase_cycles[ph], _n - (v));               \
+    v = _n;                                                                \
+  } while (0)
+#else
+#define KVR_T0(v) (void)0
+#define KVR_ACC(ph, v) (void)0
+#endif
+
 template <typename Idx>
 struct Nil {
   static constexpr Idx empty = (Idx)~(Idx)0;
@@ -128,7 +144,9 @@ template <typename Idx>
 __device__ __noinline__ void tbl_rebuild(const WorkerView<Idx>& S, uint32_t T, uint32_t size,
                                          uint32_t lane) {
   __syncwarp();
-  for (uint32_t i = lane; i < T; i += 32) S.table[i] = Nil<Idx>::empty;
+  uint4* t4 = reinterpret_cast<uint4*>(S.table);   // 16-B stores (T * sizeof(Idx) % 16 == 0)
+  const uint32_t n4 = (uint32_t)(T * sizeof(Idx) / 16);
+  for (uint32_t i = lane; i < n4; i += 32) t4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
   __syncwarp();
   for (uint32_t s = lane; s < size; s += 32) tbl_insert<Idx>(S, T - 1, S.key[s], (Idx)s);
   __syncwarp();
@@ -236,29 +254,34 @@ struct RegBits {
     return (__shfl_sync(kFull, mw, s >> 5) >> (s & 31)) & 1u;
   }
   __device__ __forceinline__ void mark_clear_all_w(uint32_t) { mw = 0u; }
-  // |U| for U = LEAF (& ~MARK) minus bit p; per-lane count and inclusive scan
+  // |U| for U = LEAF (& ~MARK) minus bit p.  The per-lane popcounts (0..32) are
+  // prefix-summed bit-sliced: six independent ballots, then popcounts under the
+  // lane mask — no dependent shuffle chain.
   __device__ __forceinline__ uint32_t count(uint32_t p, bool use_mark, uint32_t lane, uint32_t& c,
                                             uint32_t& incl) const {
     uint32_t u = use_mark ? (lw & ~mw) : lw;
     if (lane == (p >> 5)) u &= ~(1u << (p & 31));
     c = __popc(u);
-    uint32_t v = c;
+    const uint32_t le = lane == 31 ? kFull : (2u << lane) - 1u;
+    uint32_t tot = 0, inc = 0;
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, v, s);
-      if (lane >= (uint32_t)s) v += y;
+    for (int b = 0; b < 6; ++b) {
+      const uint32_t bal = __ballot_sync(kFull, (c >> b) & 1u);
+      tot += (uint32_t)__popc(bal) << b;
+      inc += (uint32_t)__popc(bal & le) << b;
     }
-    incl = v;
-    return __shfl_sync(kFull, v, 31);
+    incl = inc;
+    return tot;
   }
+  // idx-th element of U in slot order; bit 31 of the result = MARK bit of that slot
   __device__ __forceinline__ uint32_t select(uint32_t p, bool use_mark, uint32_t lane, uint32_t c,
                                              uint32_t incl, uint32_t idx) const {
     const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
     uint32_t u = use_mark ? (lw & ~mw) : lw;
     if (lane == (p >> 5)) u &= ~(1u << (p & 31));
-    const uint32_t rem = idx - (incl - c);
-    const uint32_t bit = (lane == owner) ? select_bit(u, rem) : 0u;
-    return __shfl_sync(kFull, lane * 32 + bit, owner);
+    const uint32_t bit = select_bit(u, idx - (incl - c));
+    const uint32_t packed = (lane * 32 + bit) | (((mw >> bit) & 1u) << 31);
+    return __shfl_sync(kFull, packed, owner);
   }
 };
 
@@ -318,13 +341,64 @@ struct MemBits {
         const uint32_t u = word(wi, p, use_mark);
         const uint32_t pc = __popc(u);
         if (rem < pc) {
-          slot = wi * 32 + select_bit(u, rem);
+          const uint32_t bit = select_bit(u, rem);
+          slot = (wi * 32 + bit) | (((mark[wi] >> bit) & 1u) << 31);
           break;
         }
         rem -= pc;
       }
     }
     return __shfl_sync(kFull, slot, owner);
+  }
+};
+
+// one RLT draw per lane (counter n = e + lane); out of line: runs once per 32 draws
+__device__ __noinline__ uint64_t philox_refill(uint64_t K, uint64_t n, uint32_t worker) {
+  return philox_r64(K, n, worker, 1u);
+}
+
+// Register bitmaps plus an incrementally maintained prefix count of
+// U = LEAF & ~MARK & ~{p}: in the common eviction step U only loses the victim
+// (its slot is immediately refilled by the new, marked leaf) and possibly gains
+// the victim's parent when that becomes an unmarked leaf, so the per-lane
+// inclusive counts are patched with two compares instead of a full recount.
+struct RegU {
+  RegBits b;
+  uint32_t incl, total;
+  bool dirty;
+  __device__ __forceinline__ void recount(uint32_t p, uint32_t lane) {
+    uint32_t c;
+    total = b.count(p, true, lane, c, incl);
+    dirty = false;
+  }
+  // idx-th element of U (requires !dirty): the owner lane's word and exclusive
+  // count are broadcast, every lane tests whether bit `lane` of that word is the
+  // wanted one, and a ballot names it (no serial bit-select chain)
+  __device__ __forceinline__ uint32_t pick(uint32_t p, uint32_t lane, uint32_t idx) const {
+    const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
+    uint32_t u = b.lw & ~b.mw;
+    if (lane == (p >> 5)) u &= ~(1u << (p & 31));
+    const uint32_t base = incl - (uint32_t)__popc(u);
+    const uint32_t ou = __shfl_sync(kFull, u, owner);
+    const uint32_t rem = idx - __shfl_sync(kFull, base, owner);
+    const bool hit = ((ou >> lane) & 1u) && (uint32_t)__popc(ou & lanemask_lt(lane)) == rem;
+    return owner * 32 + (__ffs(__ballot_sync(kFull, hit)) - 1);
+  }
+  // U loses v (slot v now holds the new marked leaf: LEAF bit stays, MARK bit set)
+  __device__ __forceinline__ void evict_refill(uint32_t v, uint32_t lane) {
+    if (lane >= (v >> 5)) --incl;
+    --total;
+    b.mark_set(v, lane);
+  }
+  // pv became a leaf; it joins U iff unmarked and not the excluded parent p
+  __device__ __forceinline__ void parent_leaf(uint32_t pv, uint32_t p, uint32_t lane) {
+    const bool own = lane == (pv >> 5);
+    const bool add = __ballot_sync(kFull, own && !((b.mw >> (pv & 31)) & 1u)) != 0u && pv != p;
+    b.leaf_set(pv, lane);
+    if (add) {
+      if (lane >= (pv >> 5)) ++incl;
+      ++total;
+    }
   }
 };
 
@@ -364,6 +438,7 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
       bool use_mark = true, draw = true;
       uint32_t total = bits.count(pslot, true, lane, c, incl);
       uint32_t v = 0;
+      bool vmarked = false;
       if (total == 0) {   // U = {} (A5)
         ++wr.c_fb;
         if (fallback == KVR_RLT_EARLY_RESET) {
@@ -375,6 +450,7 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
         } else {
           draw = false;
           v = log_first_valid(R, wr.lhead, wr.ltail, lane);
+          vmarked = bits.mark_test(v);
         }
         if (draw) total = bits.count(pslot, use_mark, lane, c, incl);
       }
@@ -386,7 +462,10 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
         const uint64_t rr = __shfl_sync(kFull, rbuf, (uint32_t)(wr.e - ebase));
         ++wr.e;
         ++wr.c_draws;
-        v = bits.select(pslot, use_mark, lane, c, incl, (uint32_t)pick_index(rr, total));
+        const uint32_t sel = bits.select(pslot, use_mark, lane, c, incl,
+                                         (uint32_t)pick_index(rr, total));
+        v = sel & 0x7fffffffu;
+        vmarked = (sel >> 31) != 0;
       }
       // Evict(S, v): parent loses a child (may become a leaf), v leaves T
       const Idx pv = S.parent[v];
@@ -398,7 +477,7 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
         if (nc == 0) bits.leaf_set(pv, lane);
       }
       bits.leaf_clr(v, lane);
-      if (bits.mark_test(v)) {
+      if (vmarked) {
         bits.mark_clr(v, lane);
         --wr.cntT;
       }
@@ -433,9 +512,124 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
   }
 }
 
-// occupancy targets: 128 threads (W<=4) 4 CTAs/SM, 256 (W<=8) 3 CTAs/SM, else 1
+// occupancy targets (shared memory allows ~4 CTAs/SM at W<=4 and 2 at W<=8):
+// 128 threads -> 4 CTAs/SM (128 regs), 256 -> 2 (128 regs), else 1
 template <int kMaxThreads>
-struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 3 : 1); };
+struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 2 : 1); };
+
+// RLT misses with register bitmaps and incremental U counts (B <= 1024).  Same
+// semantics as rlt_chunk; fallbacks and resets fall back to full recounts.
+template <typename Idx>
+__device__ __forceinline__ void rlt_chunk_reg(RegU& U, const WorkerView<Idx>& S, const RecencyLog& R,
+                                              WorkerRegs& wr, uint32_t B, uint32_t cnt, uint32_t cb,
+                                              Idx p0, uint32_t& pslot, uint32_t fallback,
+                                              uint64_t K, uint32_t worker, uint64_t& rbuf,
+                                              uint32_t& ri, uint32_t lane, uint32_t& my_slot,
+                                              uint32_t& my_ev, bool use_list) {
+  const Idx NIL = Nil<Idx>::empty;
+#pragma unroll 1
+  for (uint32_t r = 0; r < cnt; ++r) {
+    const uint32_t q = cb + r;
+    if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t
+      U.b.mark_clear_all_w(lane);
+      wr.cntT = 1;
+      ++wr.c_resets;
+      U.dirty = true;
+    } else {
+      ++wr.cntT;
+    }
+    uint32_t slot, ev = 0;
+    if (wr.size < B) {
+      slot = wr.size++;
+      U.b.leaf_set(slot, lane);   // new marked leaf: not in U
+      U.b.mark_set(slot, lane);
+    } else {
+      if (U.dirty) U.recount(pslot, lane);
+      uint32_t v;
+      bool vmarked = false, generic = false;
+      if (U.total == 0) {   // U = {} (A5)
+        ++wr.c_fb;
+        if (fallback == KVR_RLT_EARLY_RESET) {
+          U.b.mark_clear_all_w(lane);
+          wr.cntT = 1;
+          ++wr.c_resets;
+          U.recount(pslot, lane);
+        } else {
+          generic = true;
+        }
+      }
+      if (!generic || fallback == KVR_RLT_UNIFORM_LEAF) {
+        if (ri == 32) {   // refill 32 counter-based draws e .. e+31, one per lane
+          rbuf = philox_refill(K, wr.e + lane, worker);
+          ri = 0;
+        }
+        const uint64_t rr = __shfl_sync(kFull, rbuf, ri);
+        ++ri;
+        ++wr.e;
+        ++wr.c_draws;
+        if (!generic) {
+          v = U.pick(pslot, lane, (uint32_t)pick_index(rr, U.total));
+        } else {   // UNIFORM_LEAF: uniform over leaves != p, marks ignored
+          uint32_t c, incl;
+          const uint32_t tot = U.b.count(pslot, false, lane, c, incl);
+          const uint32_t sel =
+              U.b.select(pslot, false, lane, c, incl, (uint32_t)pick_index(rr, tot));
+          v = sel & 0x7fffffffu;
+          vmarked = (sel >> 31) != 0;
+        }
+      } else {   // LRU_MARKED: least recently used leaf != p, no draw
+        v = log_first_valid(R, wr.lhead, wr.ltail, lane);
+        vmarked = U.b.mark_test(v);
+      }
+      const Idx pv = S.parent[v];
+      // (uniform stores: every lane writes the same value after the warp-wide load)
+      if (!generic) {
+        U.evict_refill(v, lane);
+        if (pv != NIL) {
+          const Idx nc = (Idx)(S.nchild[pv] - 1);
+          __syncwarp();
+          S.nchild[pv] = nc;
+          if (nc == 0) U.parent_leaf(pv, pslot, lane);
+        }
+      } else {
+        U.b.leaf_clr(v, lane);
+        if (vmarked) {
+          U.b.mark_clr(v, lane);
+          --wr.cntT;
+        }
+        if (pv != NIL) {
+          const Idx nc = (Idx)(S.nchild[pv] - 1);
+          __syncwarp();
+          S.nchild[pv] = nc;
+          if (nc == 0) U.b.leaf_set(pv, lane);
+        }
+        U.b.leaf_set(v, lane);
+        U.b.mark_set(v, lane);
+        U.dirty = true;
+      }
+      ++wr.c_evict;
+      slot = v;
+      ev = 1;
+    }
+    // the new node's parent stops being a leaf (it is excluded or marked: U unchanged)
+    if (q == 0) {
+      if (p0 != NIL) {
+        const Idx nc = S.nchild[p0];
+        __syncwarp();
+        S.nchild[p0] = (Idx)(nc + 1);
+        if (nc == 0) U.b.leaf_clr(p0, lane);
+      }
+    } else {
+      U.b.leaf_clr(pslot, lane);
+    }
+    if (use_list) R.stamp[slot] = wr.wq;   // LRU_MARKED fallback reads the log
+    if (lane == r) {
+      my_slot = slot;
+      my_ev = ev;
+    }
+    pslot = slot;
+  }
+}
 
 template <typename Idx, bool kGlobal, int kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
@@ -512,6 +706,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     double fr_c = 0, fr_a = 0, fr_E = 0, fr_f0 = 0, fr_f1 = 0, fr_f2 = 0, fr_C = 0;
     uint64_t fr_ka = 0;
     uint64_t rbuf = 0, ebase = ~0ull >> 1;
+    uint32_t ri = 32;   // next unused draw of rbuf (register-bitmap path)
     if (tid == 0) {
       ctrl->sum_lat = 0.0;
       ctrl->sum_ttft = 0.0;
@@ -562,7 +757,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     for (uint32_t j = 0; j < Nrun; ++j) {
       const uint64_t g = gq + j;
       const uint32_t buf = (uint32_t)(g % kNumStages);
+      KVR_T0(tp);
       mbar_wait(&ctrl->mbar[buf], (uint32_t)((g / kNumStages) & 1));
+      KVR_ACC(0, tp);
       consumed = j + 1;
       const uint8_t* st = stage + (size_t)buf * p.stage_bytes;
       const QueryHdr hd = *reinterpret_cast<const QueryHdr*>(st);
@@ -577,11 +774,21 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 #pragma unroll 1
         for (;;) {
           if (lbgr) {
-            const double tau = (double)(k + 1) * dt;
-            if (tau <= a && (fn == 0 || tau <= fr_c)) {
-              Pt = rho * Pt;
-              ++k;
-              continue;
+            // every tick k' with (double)k'*dt <= min(a, c) comes first (A11); (double)k'*dt
+            // is monotone in k', so find the last such k' and apply the multiplications
+            // one by one (same rounding sequence as a per-tick loop)
+            const double lim = (fn == 0 || a < fr_c) ? a : fr_c;
+            const double est = lim / dt;
+            uint64_t kk = est < 1.8e19 ? (uint64_t)est : k;
+            if (kk < k) kk = k;
+            while ((double)(kk + 1) * dt <= lim) ++kk;
+            while (kk > k && (double)kk * dt > lim) --kk;
+            if (kk > k) {
+              if (Pt != 0.0) {
+#pragma unroll 1
+                for (uint64_t i = k; i < kk; ++i) Pt = rho * Pt;
+              }
+              k = kk;
             }
           }
           if (fn != 0 && fr_c <= a) {
@@ -624,6 +831,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         }
       }
 
+      KVR_ACC(1, tp);
       // ---- 2. longest cached prefix over the input (ballot of 32 probes) ----
       uint32_t m = 0;
 #pragma unroll 1
@@ -642,6 +850,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (m > n_in) m = n_in;
       c_probes += min(m + 1, n_in);
 
+      KVR_ACC(2, tp);
       // ---- 3. score (Eq. 4-5, A9) ----
       const double x = (double)(bt * m), y = (double)(q - bt * m);
       double score = 0.0, Chat = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
@@ -665,7 +874,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ctrl->mhit[par][w] = m;
         ctrl->npend[par][w] = fn;
       }
+      KVR_ACC(3, tp);
       __syncthreads();
+      KVR_ACC(4, tp);
       if (ctrl->abortf[par]) break;   // set by i* of query j-1 (written to the other parity)
       if (issued < Nrun) {
         if (tid == 0) {
@@ -717,6 +928,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         best = (uint32_t)pick_index(philox_r64(K, j, 0xffffffffu, 2u), W);
       }
 
+      KVR_ACC(5, tp);
       if (w != best) continue;
 
       // ================= warp i* : UpdateCache + accounting =================
@@ -752,6 +964,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         if (kf > n) kf = n;
       }
 
+      KVR_ACC(6, tp);
       // ---- hits: marks (Alg. 1 l.6-9), recency stamps, log entries ----
       Idx p0 = NIL;
 #pragma unroll 1
@@ -785,6 +998,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       __syncwarp();
 
+      KVR_ACC(7, tp);
       // ---- misses: victims, then lane-parallel apply, 32 misses per chunk ----
       const uint32_t M = n - kf;
       const uint32_t size0 = wr.size;
@@ -793,14 +1007,19 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (!rlt && nev) {   // Leaf-LRU: the nev least recently used nodes, in order
         wr.lhead = log_take(R, wr.lhead, ltail0, nev, scratch, lane);
       }
-      RegBits rb;
+      KVR_ACC(8, tp);
+      RegU ru;
       MemBits mb;
       mb.leaf = S.leaf;
       mb.mark = S.mark;
       mb.nw = nwords;
       const bool regbits = nwords <= 32;
       __syncwarp();
-      if (rlt && regbits && M) rb.load(S.leaf, S.mark, nwords, lane);
+      if (rlt && regbits && M) {
+        ru.b.load(S.leaf, S.mark, nwords, lane);
+        ru.dirty = true;
+        ru.incl = ru.total = 0;
+      }
       uint64_t V = 0;
       uint32_t pslot = (uint32_t)p0, prev_last = (uint32_t)p0;
       const uint64_t vc = ctrl->vcursor;
@@ -811,8 +1030,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         uint32_t my_slot = 0, my_ev = 0;
         if (rlt) {
           if (regbits)
-            rlt_chunk<RegBits, Idx>(rb, S, R, wr, B, cnt, cb, p0, pslot, fallback, use_list, K,
-                                    best, rbuf, ebase, lane, my_slot, my_ev);
+            rlt_chunk_reg<Idx>(ru, S, R, wr, B, cnt, cb, p0, pslot, fallback, K, best, rbuf, ri,
+                               lane, my_slot, my_ev, use_list);
           else
             rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, cnt, cb, p0, pslot, fallback, use_list, K,
                                     best, rbuf, ebase, lane, my_slot, my_ev);
@@ -825,6 +1044,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             my_ev = 1;
           }
         }
+        KVR_ACC(9, tp);
         // lane-parallel apply of this chunk
         const uint32_t qq = cb + lane;
         const bool act = lane < cnt;
@@ -860,16 +1080,17 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
         pslot = prev_last;
         __syncwarp();
+        KVR_ACC(10, tp);
       }
       if (!rlt) {
         wr.size = min(B, size0 + M);
         wr.c_evict += nev;
       }
-      if (rlt && regbits && M) rb.store(S.leaf, S.mark, nwords, lane);
+      if (rlt && regbits && M) ru.b.store(S.leaf, S.mark, nwords, lane);
       wr.c_ins += M;
       wr.used += used_add;
       if (use_list) wr.ltail = ltail0 + n;
-      if (wr.used > (L.T >> 2) * 3) {
+      if (wr.used > (L.T >> 1)) {
         tbl_rebuild<Idx>(S, L.T, wr.size, lane);
         wr.used = wr.size;
       }
@@ -877,6 +1098,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 #pragma unroll
       for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
 
+      KVR_ACC(11, tp);
       // ---- accounting: Eq. 1 truth, Eq. 2, FIFO single server (A12, A20) ----
       const uint32_t h = bt * m;
       const double hx = (double)h, hy = (double)(q - h);
@@ -946,6 +1168,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
       }
       __syncwarp();
+      KVR_ACC(12, tp);
     }
 
     // ---- end of trial ----
@@ -1031,6 +1254,21 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
                           cudaStream_t s) {
   void* args[] = {const_cast<ReplayParams*>(&p)};
   return cudaLaunchKernel(kernel_for(tier, p.W), dim3(grid), dim3(32 * p.W), args, smem, s);
+}
+
+cudaError_t phase_cycles(unsigned long long* out16, int reset) {
+#ifdef KVR_PHASE_PROFILE
+  cudaError_t e = cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[16] = {0};
+    e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return e;
+#else
+  (void)out16;
+  (void)reset;
+  return cudaErrorNotSupported;
+#endif
 }
 
 }  // namespace kvr

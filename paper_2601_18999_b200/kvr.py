@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libkvr.so")
+LIB_PATH = os.environ.get("KVR_LIB", os.path.join(_PKG, "libkvr.so"))
 
 EVICT_LRU, EVICT_RLT = 0, 1
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2

@@ -1,0 +1,56 @@
+"""Per-phase cycle breakdown of the replay kernel (profiling build libkvr_prof.so).
+
+usage: python scripts/phase_profile.py [queries] [trials]
+Phases 0-4 are summed over all warps; 5-12 only over the chosen warp i*.
+"""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2601_18999_b200 import build  # noqa: E402
+
+os.environ["KVR_LIB"] = build.build(profile=True)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2601_18999_b200 import kvr  # noqa: E402
+
+NAMES = ["stage wait", "catch-up", "match", "score", "barrier", "argmin", "upd prologue",
+         "hits", "LRU take", "RLT serial", "apply", "post/rebuild", "accounting"]
+
+nq = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
+nt = int(sys.argv[2]) if len(sys.argv) > 2 else 444
+trs = bench.build_traces(nq)
+dts = [kvr.DeviceTrace(t) for t in trs]
+L = kvr.lib()
+L.kvr_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
+L.kvr_debug_phase_cycles.restype = C.c_int32
+buf = np.zeros(16, dtype=np.uint64)
+for label, ev in (("RLT", 1), ("LRU", 0)):
+    t_of, _, keys = bench.trial_plan(0, nt)
+    sim = kvr.Simulator(8, 512, pending_ring=bench.RING)
+    pols = kvr.policies_array([kvr.Policy(eviction=ev) for _ in keys])
+    sim.run(dts, keys[:8], pols[:8], trial_trace=t_of[:8])     # warm-up
+    L.kvr_debug_phase_cycles(buf.ctypes.data, 1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = sim.run(dts, keys, pols, trial_trace=t_of)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    L.kvr_debug_phase_cycles(buf.ctypes.data, 1)
+    q = float(out.results["queries"].sum())
+    print(f"== {label}: {nt} trials x {nq} queries, {ms:.1f} ms, {q / ms / 1e3:.2f} M q-r/s, "
+          f"hit {out.results['hit_tokens'].sum() / out.results['input_tokens'].sum():.3f}, "
+          f"evict/q {out.results['evictions'].sum() / q:.1f}, probes/q {out.results['probes'].sum() / q:.1f}")
+    tot = 0
+    for i, n in enumerate(NAMES):
+        per = buf[i] / q / (8 if i <= 5 else 1)
+        if i > 5:
+            tot += per
+        print(f"  {i:2d} {n:14s} {per:10.0f} cycles/query{' (per warp)' if i <= 5 else ' (i*)'}")
+    print(f"  i* update total {tot:.0f} cycles/query")
