@@ -294,6 +294,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   p.bins = d_hist ? c.latency_hist_bins : 0;
   p.stage_bytes = (uint32_t)kvr::stage_bytes(max_n);
   p.scratch_bytes = (uint32_t)kvr::scratch_bytes(max_n);
+  p.max_n = max_n;
   p.aux = pl.aux;
   p.lay = pl.lay;
   p.truth = c.truth;

@@ -9,7 +9,9 @@
 
 namespace kvr {
 
-constexpr uint32_t kNumStages = 3;      // query staging ring depth (bulk-async copies)
+constexpr uint32_t kNumStages = 4;      // query staging ring depth (bulk-async copies)
+constexpr uint32_t kAhead = 2;          // queries staged ahead; a buffer lives 2 barriers
+                                        // after its query for the deferred apply
 constexpr uint32_t kMaxTraces = 64;     // traces per multi-trace launch
 constexpr uint32_t kFifoRecBytes = 64;  // one pending completion {c,a,E^,phi0..2,C^,k_a}
 constexpr uint32_t kMaxHistBins = 256;
@@ -42,7 +44,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 // LEAF / MARK bitmaps (RLT's marking set T is exactly the MARK bits, T in S).
 struct WorkerLayout {
   uint32_t B, T, nwords, idx_bytes;
-  size_t off_key, off_parent, off_nchild, off_table, off_leaf, off_mark, bytes;
+  size_t off_key, off_parent, off_nchild, off_table, off_leaf, off_mark, off_stamp, bytes;
 };
 
 inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
@@ -60,27 +62,27 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   L.off_table = o;  o = align16(o + (size_t)T * idx_bytes);
   L.off_leaf = o;   o = align16(o + (size_t)L.nwords * 4);
   L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);
+  L.off_stamp = o;  o = align16(o + (size_t)B * 2);     // Leaf-LRU recency stamps (u16)
   L.bytes = o;
   return L;
 }
 
 // Per-worker auxiliary state in global memory (L2-resident): the pending
-// completion FIFO, the Leaf-LRU recency log (append-only ring of (stamp, slot),
-// compacted when full) and the per-slot stamps that validate log entries.
+// completion FIFO and the Leaf-LRU recency log (append-only ring of (stamp, slot),
+// compacted when full; validated by the per-slot stamps of the worker state).
 struct AuxLayout {
   uint32_t ring, log_cap;
-  size_t off_fifo, off_stamp, off_log, bytes;
+  size_t off_fifo, off_log, bytes;
 };
 
 inline AuxLayout make_aux(uint32_t B, uint32_t ring, uint32_t max_n) {
   AuxLayout A{};
   A.ring = ring;
   uint32_t C = 64;
-  while (C < 2 * (B + max_n + 32)) C <<= 1;
+  while (C < 8 * (B + max_n + 32)) C <<= 1;
   A.log_cap = C;
   size_t o = 0;
   A.off_fifo = o;  o = align16(o + (size_t)ring * kFifoRecBytes);
-  A.off_stamp = o; o = align16(o + (size_t)B * 4);
   A.off_log = o;   o = align16(o + (size_t)C * 8);
   A.bytes = (o + 127) & ~(size_t)127;
   return A;
@@ -103,8 +105,19 @@ struct __align__(16) Ctrl {
 
 inline size_t ctrl_bytes() { return align16(sizeof(Ctrl)); }
 inline size_t stage_bytes(uint32_t max_n) { return align16(sizeof(QueryHdr) + 8 * ((size_t)max_n + 2)); }
-// per-warp scratch (u32 entries): LRU victims of one query
-inline size_t scratch_bytes(uint32_t max_n) { return align16(4 * ((size_t)max_n + 32)); }
+// Per-warp shared-memory block: the pending (deferred) apply of this worker's
+// last update, its per-miss slots, Leaf-LRU victims, the overlay victim bitmap
+// staging area, and the worker's trial counters.
+struct __align__(16) WarpSm {
+  double ttft, lat, score;
+  unsigned long long c_probes, c_hit, c_in;
+  uint32_t active, j, buf, n, kf, M, m, nev, h, ltail0, wq, p0;
+  uint32_t c_q, c_maxp, _pad[2];
+  uint32_t slot[4];                // [max_n] slots | [max_n] victims | [32] bitmap
+};
+inline size_t scratch_bytes(uint32_t max_n) {
+  return align16(sizeof(WarpSm) + 4 * (2 * (size_t)max_n + 32));
+}
 
 struct ReplayParams {
   TraceDev traces[kMaxTraces];
@@ -112,6 +125,7 @@ struct ReplayParams {
   uint32_t n_traces, n_trials, W, B;
   uint32_t ring, record_trials, rec_stride, bins;
   uint32_t stage_bytes, scratch_bytes;
+  uint32_t max_n, _pad1;
   WorkerLayout lay;
   AuxLayout aux;
   kvr_service_model truth;
@@ -128,8 +142,12 @@ struct ReplayParams {
   unsigned int* work_counter;
 };
 
+// exact table (bt * k) / 1000.0 for k = 0..max_n (the A9 feature scaling of integer token counts)
+inline size_t divtab_bytes(uint32_t max_n) { return align16(8 * ((size_t)max_n + 1)); }
+
 inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
-  return ctrl_bytes() + kNumStages * stage_bytes(max_n) + (size_t)W * scratch_bytes(max_n);
+  return ctrl_bytes() + kNumStages * stage_bytes(max_n) + (size_t)W * scratch_bytes(max_n) +
+         divtab_bytes(max_n);
 }
 
 // launchers (kvr_pack.cu / kvr_replay.cu)

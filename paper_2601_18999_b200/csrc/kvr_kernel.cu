@@ -1,4 +1,4 @@
-// kvr_replay.cu — the replay kernel: one CTA per trial (persistent over a work
+// kvr_kernel.cu — the replay kernel: one CTA per trial (persistent over a work
 // counter), one warp per worker.  Per query j (trace order, t = a_j):
 //   1. catch-up   (each warp, its worker): decay ticks merged with FIFO
 //                 completions -> NLMS OnlineUpdate + ReleaseLoad
@@ -8,24 +8,27 @@
 //   3. score      LBGR Eq. 4-5 / STATIC / THRESHOLD / RR / RANDOM
 //   -- one __syncthreads per query --
 //   4. argmin     (every warp, shuffle reduction; lowest index on ties, A15)
-//   5. update     (warp i* only): UpdateCache (Eq. 3)
-//        hits     lane-parallel: slot lookups, RLT marks with the |T|=B+1 reset
-//                 located by a ballot prefix count (Alg. 1 l.6-9), recency stamps
-//        misses   RLT (Alg. 1 l.12-17): the only serial chain — per eviction a
-//                 warp popcount scan over register-resident LEAF & ~MARK words
-//                 and one precomputed Philox draw (32 draws per lane batch);
-//                 Leaf-LRU: the e victims are the first e valid
-//                 entries of the recency log (batch select == sequential L-LRU)
-//        apply    lane-parallel: table deletes (tombstones), slot arrays,
-//                 table inserts (CAS), victim digest, log append
-//   6. accounting (warp i*): Eq. 1-2 truth, Eq. 6, FIFO latency / TTFT (A12-A14, A20)
-// while the other warps already run steps 1-3 of query j+1.  Query headers and
-// identities are staged in shared memory by 1-D bulk-async copies (TMA engine,
-// cp.async.bulk + mbarrier) kNumStages-1 queries ahead.
+//   5. update     (warp i* only), split in two:
+//      decide     UpdateCache (Eq. 3) decisions and every piece of
+//                 state the next decision needs: hit marks with the |T|=B+1
+//                 reset located by a ballot prefix count (Alg. 1 l.6-9);
+//                 RLT victims (Alg. 1 l.12-17) as the only serial chain —
+//                 register-resident LEAF/MARK words, incrementally patched
+//                 prefix counts of U, counter-based Philox draws (32 per lane
+//                 batch); Leaf-LRU victims = the first e valid
+//                 entries of the recency log; then Eq. 1-2 / Eq. 6 accounting
+//                 and the FIFO push (A12-A14, A20)
+//      apply      table deletes (tombstones) / inserts (CAS), slot arrays,
+//                 log append, digest, records — deferred until after the next
+//                 barrier, so it overlaps the other workers' next decisions.
+//                 Until then this warp matches through an overlay: the old
+//                 table minus this update's victims plus the query's own path.
+// Query headers and identities are staged in shared memory by 1-D bulk-async
+// copies (TMA engine: cp.async.bulk + mbarrier) two queries ahead.
 //
-// Scalar per-worker state (loads, theta, counters) is warp-uniform: every lane
-// holds the same value and executes the same fp64 operation; fp64 follows the
-// oracle's written operation order with -fmad=false and IEEE division.
+// Scalar per-worker state is warp-uniform: every lane holds the same value and
+// executes the same fp64 operation; fp64 follows the oracle's written
+// operation order, compiled with -fmad=false and IEEE division.
 #include <math.h>
 
 #include "kvr_device.cuh"
@@ -34,8 +37,7 @@
 namespace kvr {
 
 #ifdef KVR_PHASE_PROFILE
-// Phase profiler (profiling build only): cycles per phase summed over warps,
-// phases >= 5 only for the chosen warp i*.
+// Phase profiler (profiling build only): cycles per phase summed over warps.
 __device__ unsigned long long g_phase_cycles[16];
 #define KVR_T0(v) unsigned long long v = clock64()
 #define KVR_ACC(ph, v)                                                     \
@@ -48,6 +50,11 @@ __device__ unsigned long long g_phase_cycles[16];
 #define KVR_T0(v) (void)0
 #define KVR_ACC(ph, v) (void)0
 #endif
+
+// Dynamic shared memory of the replay kernel.  Every function derives its
+// shared-memory pointers from this array (never from pointer arguments) so the
+// compiler emits shared-space LDS/STS instead of generic LD/ST.
+extern __shared__ __align__(128) uint8_t kvr_dsmem[];
 
 template <typename Idx>
 struct Nil {
@@ -76,6 +83,28 @@ __device__ __forceinline__ WorkerView<Idx> make_view(uint8_t* base, const Worker
   v.mark = reinterpret_cast<uint32_t*>(base + L.off_mark);
   return v;
 }
+
+// dynamic shared memory map: [Ctrl][stages][WarpSm x W][divtab][workers x W] (tier 1)
+__device__ __forceinline__ size_t stage_off() { return align16(sizeof(Ctrl)); }
+__device__ __forceinline__ size_t warps_off(const ReplayParams& p) {
+  return stage_off() + (size_t)kNumStages * p.stage_bytes;
+}
+__device__ __forceinline__ size_t divtab_off(const ReplayParams& p) {
+  return warps_off(p) + (size_t)p.W * p.scratch_bytes;
+}
+__device__ __forceinline__ size_t workers_off(const ReplayParams& p) {
+  return divtab_off(p) + align16(8 * ((size_t)p.max_n + 1));
+}
+template <bool kGlobal>
+__device__ __forceinline__ uint8_t* worker_base(const ReplayParams& p, uint32_t w) {
+  if constexpr (kGlobal) return p.gstate + ((size_t)blockIdx.x * p.W + w) * p.lay.bytes;
+  else return kvr_dsmem + workers_off(p) + (size_t)w * p.lay.bytes;
+}
+__device__ __forceinline__ WarpSm* warp_sm(const ReplayParams& p, uint32_t w) {
+  return reinterpret_cast<WarpSm*>(kvr_dsmem + warps_off(p) + (size_t)w * p.scratch_bytes);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
 
 // ---------------------------------------------------------------- hash table
 template <typename Idx>
@@ -141,7 +170,7 @@ __device__ __forceinline__ uint32_t tbl_insert(const WorkerView<Idx>& S, uint32_
 
 // rebuild without tombstones (warp): clear, then re-insert every live slot
 template <typename Idx>
-__device__ __noinline__ void tbl_rebuild(const WorkerView<Idx>& S, uint32_t T, uint32_t size,
+__device__ __forceinline__ void tbl_rebuild(const WorkerView<Idx>& S, uint32_t T, uint32_t size,
                                          uint32_t lane) {
   __syncwarp();
   uint4* t4 = reinterpret_cast<uint4*>(S.table);   // 16-B stores (T * sizeof(Idx) % 16 == 0)
@@ -161,30 +190,31 @@ __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
   return b >= bins ? bins - 1 : (uint32_t)b;
 }
 
-__device__ __forceinline__ uint32_t lanemask_lt(uint32_t lane) { return (1u << lane) - 1u; }
-
 // ------------------------------------------------------- Leaf-LRU recency log
-// entry = stamp << 32 | slot; valid iff stamp[slot] == entry stamp.  The first
+// entry = stamp << 32 | slot; valid iff stamp[slot] == entry stamp (mod 2^16: a
+// stale entry never survives one compaction period, < 2^16 worker queries).  The first
 // e valid entries from the head are the e least-recently-used nodes in
 // (stamp, -depth) order because each query appends its path deepest first.
 struct RecencyLog {
   uint64_t* log;
-  uint32_t* stamp;
+  uint16_t* stamp;   // per slot, in the worker state (shared memory in tier 1)
   uint32_t cap_mask;
 };
 
 // take the first `need` valid entries in [head, tail) as victims -> out[0..need);
 // returns the new head (just past the last victim)
-__device__ __noinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
+__device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
                                           uint32_t need, uint32_t* out, uint32_t lane) {
   uint32_t k = 0, pos = head;
+  // software pipeline: the next window's entries are in flight while this one is filtered
+  uint64_t ent = (pos + lane < tail) ? R.log[(pos + lane) & R.cap_mask] : 0ull;
 #pragma unroll 1
   while (k < need && pos < tail) {
-    const uint32_t idx = pos + lane;
-    const bool act = idx < tail;
-    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
+    const uint32_t nxt = pos + 32 + lane;
+    const uint64_t ent_next = (nxt < tail) ? R.log[nxt & R.cap_mask] : 0ull;
+    const bool act = pos + lane < tail;
     const uint32_t slot = (uint32_t)ent;
-    const bool valid = act && R.stamp[slot] == (uint32_t)(ent >> 32);
+    const bool valid = act && R.stamp[slot] == (uint16_t)(ent >> 32);
     const uint32_t bal = __ballot_sync(kFull, valid);
     const uint32_t nv = __popc(bal);
     const uint32_t take = min(nv, need - k);
@@ -193,27 +223,28 @@ __device__ __noinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, ui
     k += take;
     if (take > 0 && k == need) pos += select_bit(bal, take - 1) + 1u;   // through the last victim
     else pos += 32u;
+    ent = ent_next;
   }
   __syncwarp();
   return pos;
 }
 
 // first valid entry from head (LRU over leaves != parent(t), fallback A5)
-__device__ __noinline__ uint32_t log_first_valid(const RecencyLog& R, uint32_t head, uint32_t tail,
+__device__ __forceinline__ uint32_t log_first_valid(const RecencyLog& R, uint32_t head, uint32_t tail,
                                                  uint32_t lane) {
 #pragma unroll 1
   for (;; head += 32) {
     const uint32_t idx = head + lane;
     const bool act = idx < tail;
     const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
-    const bool valid = act && R.stamp[(uint32_t)ent] == (uint32_t)(ent >> 32);
+    const bool valid = act && R.stamp[(uint32_t)ent] == (uint16_t)(ent >> 32);
     const uint32_t bal = __ballot_sync(kFull, valid);
     if (bal) return (uint32_t)__shfl_sync(kFull, (uint32_t)ent, __ffs(bal) - 1);
   }
 }
 
 // in-place order-preserving compaction of [head, tail): returns the new tail
-__device__ __noinline__ uint32_t log_compact(const RecencyLog& R, uint32_t head, uint32_t tail,
+__device__ __forceinline__ uint32_t log_compact(const RecencyLog& R, uint32_t head, uint32_t tail,
                                              uint32_t lane) {
   uint32_t w = head;
 #pragma unroll 1
@@ -221,7 +252,7 @@ __device__ __noinline__ uint32_t log_compact(const RecencyLog& R, uint32_t head,
     const uint32_t idx = r + lane;
     const bool act = idx < tail;
     const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
-    const bool valid = act && R.stamp[(uint32_t)ent] == (uint32_t)(ent >> 32);
+    const bool valid = act && R.stamp[(uint32_t)ent] == (uint16_t)(ent >> 32);
     const uint32_t bal = __ballot_sync(kFull, valid);
     __syncwarp();
     if (valid) R.log[(w + __popc(bal & lanemask_lt(lane))) & R.cap_mask] = ent;
@@ -409,21 +440,19 @@ struct WorkerRegs {
   uint32_t c_ins, c_evict, c_draws, c_resets, c_fb;
 };
 
-// RLT misses of one chunk (Alg. 1 l.6-17, path order).  Serial over the
-// misses; lane r ends up holding the slot of miss cb + r.
+// RLT decisions for misses [cb, cb+cnt), generic bitmaps (B > 1024).  Serial.
 template <typename Bits, typename Idx>
 __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, const RecencyLog& R,
                                           WorkerRegs& wr, uint32_t B, uint32_t cnt, uint32_t cb,
                                           Idx p0, uint32_t& pslot, uint32_t fallback,
                                           bool use_list, uint64_t K, uint32_t worker,
-                                          uint64_t& rbuf, uint64_t& ebase, uint32_t lane,
-                                          uint32_t& my_slot, uint32_t& my_ev) {
+                                          uint64_t& rbuf, uint32_t& ri, uint32_t lane,
+                                          uint32_t* slots, uint32_t& vbits) {
   const Idx NIL = Nil<Idx>::empty;
 #pragma unroll 1
   for (uint32_t r = 0; r < cnt; ++r) {
     const uint32_t q = cb + r;
-    // Alg. 1 l.6-9: mark t (t is not cached, hence not in T)
-    if (wr.cntT == B) {
+    if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t (t is not cached, not in T)
       bits.mark_clear_all_w(lane);
       wr.cntT = 1;
       ++wr.c_resets;
@@ -455,11 +484,12 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
         if (draw) total = bits.count(pslot, use_mark, lane, c, incl);
       }
       if (draw) {
-        if (wr.e - ebase >= 32) {   // refill 32 counter-based draws, one per lane
-          ebase = wr.e;
-          rbuf = philox_r64(K, ebase + lane, worker, 1u);
+        if (ri == 32) {
+          rbuf = philox_refill(K, wr.e + lane, worker);
+          ri = 0;
         }
-        const uint64_t rr = __shfl_sync(kFull, rbuf, (uint32_t)(wr.e - ebase));
+        const uint64_t rr = __shfl_sync(kFull, rbuf, ri);
+        ++ri;
         ++wr.e;
         ++wr.c_draws;
         const uint32_t sel = bits.select(pslot, use_mark, lane, c, incl,
@@ -467,13 +497,11 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
         v = sel & 0x7fffffffu;
         vmarked = (sel >> 31) != 0;
       }
-      // Evict(S, v): parent loses a child (may become a leaf), v leaves T
       const Idx pv = S.parent[v];
       if (pv != NIL) {
         const Idx nc = (Idx)(S.nchild[pv] - 1);
         __syncwarp();
-        if (lane == 0) S.nchild[pv] = nc;
-        __syncwarp();
+        S.nchild[pv] = nc;
         if (nc == 0) bits.leaf_set(pv, lane);
       }
       bits.leaf_clr(v, lane);
@@ -485,47 +513,33 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
       slot = v;
       ev = 1;
     }
-    // Load(S, t): new marked leaf; its parent stops being a leaf
     bits.leaf_set(slot, lane);
     bits.mark_set(slot, lane);
     if (q == 0) {
       if (p0 != NIL) {
         const Idx nc = S.nchild[p0];
         __syncwarp();
-        if (lane == 0) S.nchild[p0] = (Idx)(nc + 1);
-        __syncwarp();
+        S.nchild[p0] = (Idx)(nc + 1);
         if (nc == 0) bits.leaf_clr(p0, lane);
       }
     } else {
       bits.leaf_clr(pslot, lane);
     }
-    if (use_list) {   // LRU_MARKED fallback reads the log: stamp the reused slot now
-      __syncwarp();
-      if (lane == 0) R.stamp[slot] = wr.wq;
-      __syncwarp();
-    }
-    if (lane == r) {
-      my_slot = slot;
-      my_ev = ev;
-    }
+    if (use_list) R.stamp[slot] = wr.wq;
+    slots[q] = slot | (ev << 31);
+    if (ev && lane == (slot >> 5)) vbits |= 1u << (slot & 31);
     pslot = slot;
   }
 }
 
-// occupancy targets (shared memory allows ~4 CTAs/SM at W<=4 and 2 at W<=8):
-// 128 threads -> 4 CTAs/SM (128 regs), 256 -> 2 (128 regs), else 1
-template <int kMaxThreads>
-struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 2 : 1); };
-
-// RLT misses with register bitmaps and incremental U counts (B <= 1024).  Same
-// semantics as rlt_chunk; fallbacks and resets fall back to full recounts.
+// RLT decisions with register bitmaps and incremental U counts (B <= 1024).
 template <typename Idx>
 __device__ __forceinline__ void rlt_chunk_reg(RegU& U, const WorkerView<Idx>& S, const RecencyLog& R,
                                               WorkerRegs& wr, uint32_t B, uint32_t cnt, uint32_t cb,
                                               Idx p0, uint32_t& pslot, uint32_t fallback,
                                               uint64_t K, uint32_t worker, uint64_t& rbuf,
-                                              uint32_t& ri, uint32_t lane, uint32_t& my_slot,
-                                              uint32_t& my_ev, bool use_list) {
+                                              uint32_t& ri, uint32_t lane, uint32_t* slots,
+                                              uint32_t& vbits, bool use_list) {
   const Idx NIL = Nil<Idx>::empty;
 #pragma unroll 1
   for (uint32_t r = 0; r < cnt; ++r) {
@@ -610,6 +624,7 @@ __device__ __forceinline__ void rlt_chunk_reg(RegU& U, const WorkerView<Idx>& S,
       ++wr.c_evict;
       slot = v;
       ev = 1;
+      if (lane == (v >> 5)) vbits |= 1u << (v & 31);
     }
     // the new node's parent stops being a leaf (it is excluded or marked: U unchanged)
     if (q == 0) {
@@ -623,18 +638,308 @@ __device__ __forceinline__ void rlt_chunk_reg(RegU& U, const WorkerView<Idx>& S,
       U.b.leaf_clr(pslot, lane);
     }
     if (use_list) R.stamp[slot] = wr.wq;   // LRU_MARKED fallback reads the log
-    if (lane == r) {
-      my_slot = slot;
-      my_ev = ev;
-    }
+    slots[q] = slot | (ev << 31);
     pslot = slot;
   }
 }
 
+// floor(r64 * t / 2^64) for r64 = hi:lo and t < 2^32 (== __umul64hi(r64, t); A6)
+__device__ __forceinline__ uint32_t pick32(uint32_t lo, uint32_t hi, uint32_t t) {
+  return (uint32_t)(((uint64_t)hi * t + __umulhi(lo, t)) >> 32);
+}
+
+// All RLT miss decisions of one query (Alg. 1 l.6-17 in path order), register
+// bitmaps (B <= 1024).  Out of line so the serial chain gets its own register
+// allocation; state is copied in and out once per query.  Per lane l:
+//   lw, mw  LEAF / MARK word l;   uw  word l of U = LEAF & ~MARK & ~{p};
+//   incl    inclusive prefix count of U over words 0..l;   total = |U|.
+// The common eviction step is a handful of dependent instructions: the owner
+// word is popc(ballot(incl <= idx)), the bit inside it popc(ballot(rank_le <=
+// rem)); U loses the victim (its slot is refilled by the new, marked leaf) and
+// gains the victim's parent iff that became an unmarked leaf.  Resets and the
+// U = {} fallbacks (A5) recount from lw/mw.
+template <typename Idx, bool kGlobal, int kTag>
+__device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& wr_io,
+                                            uint32_t M, Idx p0, uint32_t fallback, uint64_t K,
+                                            uint32_t worker, uint64_t& rbuf_io, uint32_t& ri_io,
+                                            uint32_t lane, uint32_t& vbits_io, bool use_list) {
+  const Idx NIL = Nil<Idx>::empty;
+  const uint32_t B = p_.B, nwords = p_.lay.nwords;
+  uint8_t* wb = worker_base<kGlobal>(p_, worker);
+  const WorkerView<Idx> S = make_view<Idx>(wb, p_.lay);
+  RecencyLog R;
+  R.log = reinterpret_cast<uint64_t*>(p_.aux_base + ((size_t)blockIdx.x * p_.W + worker) * p_.aux.bytes +
+                                      p_.aux.off_log);
+  R.stamp = reinterpret_cast<uint16_t*>(wb + p_.lay.off_stamp);
+  R.cap_mask = p_.aux.log_cap - 1;
+  uint32_t* slots = warp_sm(p_, worker)->slot;
+  WorkerRegs wr = wr_io;
+  uint32_t rlo = (uint32_t)rbuf_io, rhi = (uint32_t)(rbuf_io >> 32);
+  uint32_t ri = ri_io, vbits = vbits_io, p = (uint32_t)p0;
+  RegBits rb;
+  rb.load(S.leaf, S.mark, nwords, lane);
+  const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;   // lanes <= lane
+  uint32_t uw = 0, incl = 0, total = 0;
+  bool dirty = true;
+  uint32_t q = 0;
+#pragma unroll 1
+  for (; q < M; ++q) {
+    if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t (t is not cached: not in T)
+      rb.mw = 0u;
+      wr.cntT = 1;
+      ++wr.c_resets;
+      dirty = true;
+    } else {
+      ++wr.cntT;
+    }
+    uint32_t slot, ev = 0;
+    if (wr.size < B) {
+      slot = wr.size++;   // new marked leaf: not in U
+      rb.leaf_set(slot, lane);
+      rb.mark_set(slot, lane);
+    } else {
+      if (dirty) {
+        uw = rb.lw & ~rb.mw;
+        if (lane == (p >> 5)) uw &= ~(1u << (p & 31));
+        uint32_t c;
+        total = rb.count(p, true, lane, c, incl);
+        dirty = false;
+      }
+      bool generic = false;
+      if (total == 0) {   // U = {} (A5)
+        ++wr.c_fb;
+        if (fallback == KVR_RLT_EARLY_RESET) {
+          rb.mw = 0u;
+          wr.cntT = 1;
+          ++wr.c_resets;
+          uw = rb.lw;
+          if (lane == (p >> 5)) uw &= ~(1u << (p & 31));
+          uint32_t c;
+          total = rb.count(p, true, lane, c, incl);
+        } else {
+          generic = true;
+        }
+      }
+      uint32_t v;
+      if (!generic) {
+        if (ri == 32) {   // 32 counter-based draws e .. e+31, one per lane
+          const uint64_t r = philox_refill(K, wr.e + lane, worker);
+          rlo = (uint32_t)r;
+          rhi = (uint32_t)(r >> 32);
+          ri = 0;
+        }
+        const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+        ++ri;
+        ++wr.e;
+        ++wr.c_draws;
+        const uint32_t idx = pick32(dlo, dhi, total);
+        const uint32_t owner = __popc(__ballot_sync(kFull, incl <= idx));
+        const uint32_t ou = __shfl_sync(kFull, uw, owner);
+        const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
+        const uint32_t bit = __popc(__ballot_sync(kFull, (uint32_t)__popc(ou & lmle) <= rem));
+        v = owner * 32 + bit;
+        // Evict(S, v) + Load(S, t) into slot v: LEAF stays, MARK set, U loses v
+        if (lane == owner) {
+          uw &= ~(1u << bit);
+          rb.mw |= 1u << bit;
+        }
+        if (lane >= owner) --incl;
+        --total;
+        const Idx pv = S.parent[v];
+        if (pv != NIL) {
+          const Idx nc = (Idx)(S.nchild[pv] - 1);
+          __syncwarp();
+          S.nchild[pv] = nc;   // uniform store
+          if (nc == 0) {       // pv became a leaf; joins U iff unmarked and != p
+            const uint32_t pw = (uint32_t)pv >> 5, pb = 1u << ((uint32_t)pv & 31);
+            const bool add = __ballot_sync(kFull, lane == pw && !(rb.mw & pb)) != 0u &&
+                             (uint32_t)pv != p;
+            if (lane == pw) {
+              rb.lw |= pb;
+              if (add) uw |= pb;
+            }
+            if (add) {
+              if (lane >= pw) ++incl;
+              ++total;
+            }
+          }
+        }
+      } else {
+        bool vmarked;
+        if (fallback == KVR_RLT_UNIFORM_LEAF) {   // uniform over leaves != p, marks ignored
+          if (ri == 32) {
+            const uint64_t r = philox_refill(K, wr.e + lane, worker);
+            rlo = (uint32_t)r;
+            rhi = (uint32_t)(r >> 32);
+            ri = 0;
+          }
+          const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+          ++ri;
+          ++wr.e;
+          ++wr.c_draws;
+          uint32_t c, inc2;
+          const uint32_t tot = rb.count(p, false, lane, c, inc2);
+          const uint32_t sel = rb.select(p, false, lane, c, inc2, pick32(dlo, dhi, tot));
+          v = sel & 0x7fffffffu;
+          vmarked = (sel >> 31) != 0;
+        } else {   // LRU_MARKED: least recently used leaf != p, no draw
+          v = log_first_valid(R, wr.lhead, wr.ltail, lane);
+          vmarked = rb.mark_test(v);
+        }
+        rb.leaf_clr(v, lane);
+        if (vmarked) {
+          rb.mark_clr(v, lane);
+          --wr.cntT;
+        }
+        const Idx pv = S.parent[v];
+        if (pv != NIL) {
+          const Idx nc = (Idx)(S.nchild[pv] - 1);
+          __syncwarp();
+          S.nchild[pv] = nc;
+          if (nc == 0) rb.leaf_set(pv, lane);
+        }
+        rb.leaf_set(v, lane);
+        rb.mark_set(v, lane);
+        dirty = true;
+      }
+      ++wr.c_evict;
+      slot = v;
+      ev = 1;
+      if (lane == (v >> 5)) vbits |= 1u << (v & 31);
+    }
+    // the new node's parent stops being a leaf (excluded as p, or marked: U unchanged)
+    if (q == 0) {
+      if (p0 != NIL) {
+        const Idx nc = S.nchild[p0];
+        __syncwarp();
+        S.nchild[p0] = (Idx)(nc + 1);
+        if (nc == 0) rb.leaf_clr(p0, lane);
+      }
+    } else {
+      rb.leaf_clr(p, lane);
+    }
+    if (use_list) R.stamp[slot] = (uint16_t)wr.wq;   // LRU_MARKED fallback reads the log
+    slots[q] = slot | (ev << 31);
+    p = slot;
+  }
+  rb.store(S.leaf, S.mark, nwords, lane);
+  wr_io = wr;
+  rbuf_io = ((uint64_t)rhi << 32) | rlo;
+  ri_io = ri;
+  vbits_io = vbits;
+}
+
+// Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
+// victim digest, ordered trial sums, records and histogram.
+template <typename Idx, bool kGlobal, int kTag>
+__device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr, uint32_t lane,
+                                          uint32_t w, bool rlt, bool use_list, bool lbgr_or_static,
+                                          kvr_query_record* rec, uint64_t* vlog) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(kvr_dsmem);
+  WarpSm* ws = warp_sm(p, w);
+  const uint8_t* stage = kvr_dsmem + stage_off();
+  uint8_t* wb = worker_base<kGlobal>(p, w);
+  const WorkerView<Idx> S = make_view<Idx>(wb, p.lay);
+  RecencyLog R;
+  R.log = reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
+                                      p.aux.off_log);
+  R.stamp = reinterpret_cast<uint16_t*>(wb + p.lay.off_stamp);
+  R.cap_mask = p.aux.log_cap - 1;
+  const uint32_t tmask = p.lay.T - 1;
+  const uint64_t* H = reinterpret_cast<const uint64_t*>(stage + (size_t)ws->buf * p.stage_bytes + 32);
+  H += (reinterpret_cast<const QueryHdr*>(stage + (size_t)ws->buf * p.stage_bytes)->block_off & 1);
+  const uint32_t n = ws->n, kf = ws->kf, M = ws->M, nev = ws->nev, wq = ws->wq, ltail0 = ws->ltail0;
+  const uint32_t nfree = M - nev;
+  const uint64_t vc = ctrl->vcursor;
+  uint64_t V = 0;
+  uint32_t used_add = 0, prev_last = ws->p0;
+#pragma unroll 1
+  for (uint32_t cb = 0; cb < M; cb += 32) {
+    const uint32_t cnt = min(32u, M - cb);
+    const uint32_t qq = cb + lane;
+    const bool act = lane < cnt;
+    const uint32_t sv = act ? ws->slot[qq] : 0u;
+    const uint32_t my_slot = sv & 0x7fffffffu;
+    const bool my_ev = (sv >> 31) != 0;
+    const uint64_t t = act ? H[kf + qq] : 0ull;
+    if (act && my_ev) {
+      const uint64_t vkey = S.key[my_slot];
+      tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
+      V ^= fmix64(vkey ^ ((uint64_t)(qq - nfree + 1) * kPosMul));
+      if (vlog) {
+        const uint64_t vi = vc + (qq - nfree);
+        if (vi < p.victims_per_trial) vlog[vi] = vkey;
+      }
+    }
+    const uint32_t up = __shfl_up_sync(kFull, my_slot, 1);
+    const uint32_t par_slot = lane == 0 ? prev_last : up;
+    __syncwarp();
+    if (act) {
+      S.key[my_slot] = t;
+      if (rlt) {
+        S.parent[my_slot] = (Idx)par_slot;
+        S.nchild[my_slot] = (Idx)(qq + 1 < M ? 1 : 0);
+      }
+      if (use_list) {
+        if (!rlt) R.stamp[my_slot] = wq;
+        R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] = ((uint64_t)wq << 32) | my_slot;
+      }
+    }
+    __syncwarp();
+    const uint32_t claimed = act ? tbl_insert<Idx>(S, tmask, t, (Idx)my_slot) : 0u;
+    used_add += __popc(__ballot_sync(kFull, claimed != 0));
+    prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
+    __syncwarp();
+  }
+  wr.used += used_add;
+  if (wr.used > (p.lay.T >> 1)) {
+    tbl_rebuild<Idx>(S, p.lay.T, wr.size, lane);
+    wr.used = wr.size;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  if (lane == 0) {
+    uint64_t D = ctrl->digest;   // decision digest
+    D = fmix64(D ^ (uint64_t)ws->j);
+    D = fmix64(D ^ (uint64_t)w);
+    D = fmix64(D ^ (uint64_t)ws->m);
+    D = fmix64(D ^ (uint64_t)nev);
+    D = fmix64(D ^ V);
+    ctrl->digest = D;
+    const double lat = ws->lat, ttft = ws->ttft;
+    ctrl->sum_lat = ctrl->sum_lat + lat;
+    ctrl->sum_ttft = ctrl->sum_ttft + ttft;
+    if (lat > ctrl->max_lat) ctrl->max_lat = lat;
+    ctrl->vcursor = vc + nev;
+    if (vlog && vc + nev > p.victims_per_trial)
+      atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
+    if (rec) {
+      kvr_query_record Rq;
+      Rq.worker = w;
+      Rq.hit_tokens = ws->h;
+      Rq.n_victims = nev;
+      Rq._pad = 0;
+      Rq.ttft_ms = ttft;
+      Rq.latency_ms = lat;
+      Rq.score = lbgr_or_static ? ws->score : 0.0;
+      Rq.victim_offset = vc;
+      rec[ws->j] = Rq;
+    }
+    if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
+    ws->active = 0;
+  }
+  __syncwarp();
+}
+
+// occupancy targets (shared memory allows ~4 CTAs/SM at W<=4 and 2 at W<=8):
+// 128 threads -> 4 CTAs/SM (128 regs), 256 -> 2 (128 regs), else 1
+template <int kMaxThreads>
+struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 2 : 1); };
+
 template <typename Idx, bool kGlobal, int kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     replay_kernel(const __grid_constant__ ReplayParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* smem = kvr_dsmem;
   const Idx NIL = Nil<Idx>::empty;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t W = p.W, B = p.B;
@@ -643,9 +948,14 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem);
   uint8_t* stage = smem + align16(sizeof(Ctrl));
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(stage + (size_t)kNumStages * p.stage_bytes +
-                                                  (size_t)w * p.scratch_bytes);
-  uint8_t* sbase = stage + (size_t)kNumStages * p.stage_bytes + (size_t)W * p.scratch_bytes;
+  WarpSm* ws = reinterpret_cast<WarpSm*>(stage + (size_t)kNumStages * p.stage_bytes +
+                                         (size_t)w * p.scratch_bytes);
+  uint32_t* slots = ws->slot;              // [max_n] slot | evicted << 31 per miss
+  uint32_t* victims = slots + p.max_n;     // [max_n] Leaf-LRU victims of one query
+  uint32_t* vmap = victims + p.max_n;      // [32] victim bitmap staging (overlay)
+  double* divtab = reinterpret_cast<double*>(stage + (size_t)kNumStages * p.stage_bytes +
+                                             (size_t)W * p.scratch_bytes);
+  uint8_t* sbase = reinterpret_cast<uint8_t*>(divtab) + align16(8 * ((size_t)p.max_n + 1));
   uint8_t* wbase = kGlobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
                            : sbase + (size_t)w * L.bytes;
   const WorkerView<Idx> S = make_view<Idx>(wbase, L);
@@ -653,8 +963,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
   double* fifo = reinterpret_cast<double*>(abase + p.aux.off_fifo);
   RecencyLog R;
   R.log = reinterpret_cast<uint64_t*>(abase + p.aux.off_log);
-  R.stamp = reinterpret_cast<uint32_t*>(abase + p.aux.off_stamp);
+  R.stamp = reinterpret_cast<uint16_t*>(wbase + L.off_stamp);
   R.cap_mask = p.aux.log_cap - 1;
+  const bool regbits = nwords <= 32;
 
   if (tid == 0) {
     for (uint32_t b = 0; b < kNumStages; ++b) mbar_init(&ctrl->mbar[b], 1);
@@ -682,9 +993,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     const bool use_list = !rlt || pol.rlt_fallback == KVR_RLT_LRU_MARKED;
     const bool lbgr = pol.router == KVR_ROUTE_LBGR;
     const uint32_t router = pol.router, fallback = pol.rlt_fallback;
+    const bool lbgr_or_static = lbgr || router == KVR_ROUTE_STATIC_LINEAR;
     const bool recorded = trial < p.record_trials;
     kvr_query_record* rec = recorded ? p.records + (size_t)trial * p.rec_stride : nullptr;
     uint64_t* vlog = (recorded && p.victims) ? p.victims + (size_t)trial * p.victims_per_trial : nullptr;
+    // deferred apply needs the overlay (register victim bitmap): B <= 1024
+    const bool defer = regbits;
 
     // ---- per-trial init: empty caches S_i^(0), P_i^(0) = 0 ----
     for (uint32_t i = lane; i < L.T; i += 32) S.table[i] = NIL;
@@ -697,16 +1011,20 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     WorkerRegs wr;
     wr.size = 0; wr.cntT = 0; wr.used = 0; wr.wq = 0; wr.lhead = 0; wr.ltail = 0; wr.e = 0;
     wr.c_ins = 0; wr.c_evict = 0; wr.c_draws = 0; wr.c_resets = 0; wr.c_fb = 0;
-    uint32_t fh = 0, fn = 0, c_q = 0, c_maxp = 0;
-    uint64_t c_probes = 0, c_hit = 0, c_in = 0;
+    uint32_t fh = 0, fn = 0;
     double P = 0.0, F = 0.0, Pt = 0.0;
     double th0 = pol.theta0[0], th1 = pol.theta0[1], th2 = pol.theta0[2], th3 = pol.theta0[3];
     uint64_t k = 0;
-    // front record of the pending FIFO, prefetched into registers
-    double fr_c = 0, fr_a = 0, fr_E = 0, fr_f0 = 0, fr_f1 = 0, fr_f2 = 0, fr_C = 0;
-    uint64_t fr_ka = 0;
-    uint64_t rbuf = 0, ebase = ~0ull >> 1;
-    uint32_t ri = 32;   // next unused draw of rbuf (register-bitmap path)
+    // front record of the pending FIFO: lane f < 8 holds field f; fr_c is uniform
+    double fr = 0.0, fr_c = 0.0;
+    uint64_t rbuf = 0;
+    uint32_t ri = 32;       // next unused draw of rbuf
+    uint32_t vbits = 0;     // victims of this warp's pending update (lane l: word l)
+    if (lane == 0) {
+      ws->active = 0;
+      ws->c_probes = 0; ws->c_hit = 0; ws->c_in = 0; ws->c_q = 0; ws->c_maxp = 0;
+    }
+    vmap[lane] = 0u;
     if (tid == 0) {
       ctrl->sum_lat = 0.0;
       ctrl->sum_ttft = 0.0;
@@ -719,6 +1037,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       for (int c = 0; c < 10; ++c) ctrl->cnt[c] = 0;
     }
     for (uint32_t b = tid; b < p.bins; b += blockDim.x) ctrl->hist[b] = 0;
+    // (bt*k)/1000.0 computed once per trial with the same IEEE division (A9)
+    for (uint32_t kk = tid; kk <= p.max_n; kk += blockDim.x) divtab[kk] = (double)(bt * kk) / 1000.0;
 
     // a per-trial policy from device memory is validated here (host validated the default)
     const bool pol_ok = pol.eviction <= KVR_EVICT_RLT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
@@ -727,8 +1047,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     const uint32_t Nrun = pol_ok ? N : 0;
 
-    // staging prologue: queries 0 .. kNumStages-2
-    uint32_t issued = min(Nrun, kNumStages - 1);
+    // staging prologue: queries 0 .. kAhead-1
+    uint32_t issued = min(Nrun, kAhead);
     uint64_t pf_off = 0;
     uint32_t pf_n = 0;
     if (tid == 0) {
@@ -786,7 +1106,14 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             if (kk > k) {
               if (Pt != 0.0) {
 #pragma unroll 1
-                for (uint64_t i = k; i < kk; ++i) Pt = rho * Pt;
+                uint32_t nt = (uint32_t)(kk - k);
+                for (; nt >= 4; nt -= 4) {
+                  Pt = rho * Pt;
+                  Pt = rho * Pt;
+                  Pt = rho * Pt;
+                  Pt = rho * Pt;
+                }
+                for (; nt; --nt) Pt = rho * Pt;
               }
               k = kk;
             }
@@ -795,21 +1122,25 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             fh = (fh + 1 == p.ring) ? 0 : fh + 1;
             --fn;
             if (lbgr) {
+              const double fa = __shfl_sync(kFull, fr, 1), fE = __shfl_sync(kFull, fr, 2);
+              const double f0 = __shfl_sync(kFull, fr, 3), f1 = __shfl_sync(kFull, fr, 4);
+              const double f2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
+              const uint64_t ka = (uint64_t)__double_as_longlong(__shfl_sync(kFull, fr, 7));
               // OnlineUpdate (A8): NLMS on the squared residual
-              const double E = fr_c - fr_a;
-              const double res = E - fr_E;
+              const double E = fr_c - fa;
+              const double res = E - fE;
               const double f3 = 1.0;
-              double s = fr_f0 * fr_f0;
-              s = s + fr_f1 * fr_f1;
-              s = s + fr_f2 * fr_f2;
+              double s = f0 * f0;
+              s = s + f1 * f1;
+              s = s + f2 * f2;
               s = s + f3 * f3;
               const double gstep = (pol.mu * res) / (1.0 + s);
-              th0 = th0 + gstep * fr_f0;
-              th1 = th1 + gstep * fr_f1;
-              th2 = th2 + gstep * fr_f2;
+              th0 = th0 + gstep * f0;
+              th1 = th1 + gstep * f1;
+              th2 = th2 + gstep * f2;
               th3 = th3 + gstep * f3;
               // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
-              uint64_t kap = k - fr_ka;
+              uint64_t kap = k - ka;
               double pw = 1.0, bb = rho;
 #pragma unroll 1
               while (kap) {
@@ -817,28 +1148,53 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
                 bb = bb * bb;
                 kap >>= 1;
               }
-              Pt = Pt - fr_C * pw;
+              Pt = Pt - fC * pw;
               if (Pt < 0.0) Pt = 0.0;
             }
             if (fn) {
-              const double* r = fifo + (size_t)fh * 8;
-              fr_c = r[0]; fr_a = r[1]; fr_E = r[2]; fr_f0 = r[3]; fr_f1 = r[4]; fr_f2 = r[5];
-              fr_C = r[6]; fr_ka = (uint64_t)__double_as_longlong(r[7]);
+              if (lane < 8) fr = fifo[(size_t)fh * 8 + lane];
+              fr_c = __shfl_sync(kFull, fr, 0);
             }
             continue;
           }
           break;
         }
       }
-
       KVR_ACC(1, tp);
+
       // ---- 2. longest cached prefix over the input (ballot of 32 probes) ----
+      // With a pending deferred apply, membership = path of that query (same
+      // position, same identity) or old table minus that update's victims.
+      const bool overlay = defer && ws->active;
+      const uint64_t* Hp = nullptr;
+      uint32_t np = 0;
+      if (overlay) {
+        const uint8_t* sp = stage + (size_t)ws->buf * p.stage_bytes;
+        Hp = reinterpret_cast<const uint64_t*>(sp + 32) +
+             (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
+        np = ws->n;
+      }
       uint32_t m = 0;
 #pragma unroll 1
       for (uint32_t base = 0; base < n_in; base += 32) {
         const uint32_t d = base + lane;
-        bool hit = false;
-        if (d < n_in) hit = tbl_find<Idx>(S, tmask, H[d]) != NIL;
+        bool hit = false, check = false;
+        uint32_t sidx = 0;
+        if (d < n_in) {
+          const uint64_t hh = H[d];
+          if (overlay && d < np && Hp[d] == hh) {
+            hit = true;
+          } else {
+            const Idx s = tbl_find<Idx>(S, tmask, hh);
+            hit = s != NIL;
+            check = overlay && hit;
+            sidx = (uint32_t)s;
+          }
+        }
+        if (overlay) {   // found in the old table but evicted by the pending update?
+          const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
+          if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
+        }
         const uint32_t bal = __ballot_sync(kFull, hit);
         if (bal == kFull) {
           m = base + 32;
@@ -848,16 +1204,16 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         break;
       }
       if (m > n_in) m = n_in;
-      c_probes += min(m + 1, n_in);
-
+      if (lane == 0) ws->c_probes += min(m + 1, n_in);
       KVR_ACC(2, tp);
+
       // ---- 3. score (Eq. 4-5, A9) ----
       const double x = (double)(bt * m), y = (double)(q - bt * m);
       double score = 0.0, Chat = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
       if (lbgr) {
         Chat = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
-        f0 = x / 1000.0;
-        f1 = y / 1000.0;
+        f0 = divtab[m];            // == x / 1000.0 (x = bt*m)
+        f1 = divtab[n_in - m];     // == y / 1000.0 (y = bt*(n_in-m))
         f2 = Pt / 1000.0;
         const double f3 = 1.0;
         double dd = th0 * f0;
@@ -912,12 +1268,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         }
         best = bi;
       } else if (router == KVR_ROUTE_THRESHOLD) {   // A16
-        const uint32_t np = lane < W ? ctrl->npend[par][lane] : 0xffffffffu;
+        const uint32_t npd = lane < W ? ctrl->npend[par][lane] : 0xffffffffu;
         const uint32_t mh = lane < W ? ctrl->mhit[par][lane] : 0u;
-        const uint32_t mx = __reduce_max_sync(kFull, lane < W ? np : 0u);
-        const uint32_t mn = __reduce_min_sync(kFull, np);
+        const uint32_t mx = __reduce_max_sync(kFull, lane < W ? npd : 0u);
+        const uint32_t mn = __reduce_min_sync(kFull, npd);
         if ((double)mx > pol.tau * (double)max(1u, mn)) {
-          best = __ffs(__ballot_sync(kFull, np == mn)) - 1;
+          best = __ffs(__ballot_sync(kFull, npd == mn)) - 1;
         } else {
           const uint32_t mmax = __reduce_max_sync(kFull, mh);
           best = __ffs(__ballot_sync(kFull, lane < W && mh == mmax)) - 1;
@@ -927,11 +1283,18 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       } else {
         best = (uint32_t)pick_index(philox_r64(K, j, 0xffffffffu, 2u), W);
       }
-
       KVR_ACC(5, tp);
+
+      // deferred apply of this warp's previous update (overlaps others' decisions)
+      if (ws->active) {
+        apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        vbits = 0;
+      }
+      KVR_ACC(6, tp);
+
       if (w != best) continue;
 
-      // ================= warp i* : UpdateCache + accounting =================
+      // ================= warp i* : UpdateCache decisions + accounting =================
       if (fn >= p.ring) {   // pending FIFO full -> trial status, stop (before Eq. 3)
         if (lane == 0) {
           ctrl->status = KVR_TRIAL_RING_OVERFLOW;
@@ -964,7 +1327,6 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         if (kf > n) kf = n;
       }
 
-      KVR_ACC(6, tp);
       // ---- hits: marks (Alg. 1 l.6-9), recency stamps, log entries ----
       Idx p0 = NIL;
 #pragma unroll 1
@@ -997,108 +1359,50 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         p0 = (Idx)__shfl_sync(kFull, (uint32_t)s, min(31u, kf - 1 - base));
       }
       __syncwarp();
-
       KVR_ACC(7, tp);
-      // ---- misses: victims, then lane-parallel apply, 32 misses per chunk ----
+
+      // ---- misses: decisions (victims and slots) ----
       const uint32_t M = n - kf;
       const uint32_t size0 = wr.size;
-      const uint32_t nfree = B - size0;
-      const uint32_t nev = M > nfree ? M - nfree : 0u;
-      if (!rlt && nev) {   // Leaf-LRU: the nev least recently used nodes, in order
-        wr.lhead = log_take(R, wr.lhead, ltail0, nev, scratch, lane);
-      }
-      KVR_ACC(8, tp);
-      RegU ru;
-      MemBits mb;
-      mb.leaf = S.leaf;
-      mb.mark = S.mark;
-      mb.nw = nwords;
-      const bool regbits = nwords <= 32;
-      __syncwarp();
-      if (rlt && regbits && M) {
-        ru.b.load(S.leaf, S.mark, nwords, lane);
-        ru.dirty = true;
-        ru.incl = ru.total = 0;
-      }
-      uint64_t V = 0;
-      uint32_t pslot = (uint32_t)p0, prev_last = (uint32_t)p0;
-      const uint64_t vc = ctrl->vcursor;
-      uint32_t used_add = 0;
-#pragma unroll 1
-      for (uint32_t cb = 0; cb < M; cb += 32) {
-        const uint32_t cnt = min(32u, M - cb);
-        uint32_t my_slot = 0, my_ev = 0;
-        if (rlt) {
-          if (regbits)
-            rlt_chunk_reg<Idx>(ru, S, R, wr, B, cnt, cb, p0, pslot, fallback, K, best, rbuf, ri,
-                               lane, my_slot, my_ev, use_list);
-          else
-            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, cnt, cb, p0, pslot, fallback, use_list, K,
-                                    best, rbuf, ebase, lane, my_slot, my_ev);
+      const uint32_t nfree = min(M, B - size0);
+      const uint32_t nev = M - nfree;
+      if (rlt) {
+        uint32_t pslot = (uint32_t)p0;
+        if (regbits) {
+          if (M) rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, wr, M, p0, fallback, K, w, rbuf, ri, lane, vbits,
+                                                      use_list);
         } else {
-          const uint32_t qq = cb + lane;
+          MemBits mb;
+          mb.leaf = S.leaf;
+          mb.mark = S.mark;
+          mb.nw = nwords;
+#pragma unroll 1
+          for (uint32_t cb = 0; cb < M; cb += 32)
+            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, min(32u, M - cb), cb, p0, pslot, fallback,
+                                    use_list, K, w, rbuf, ri, lane, slots, vbits);
+        }
+      } else {
+        // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
+        if (nev) wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
+#pragma unroll 1
+        for (uint32_t qq = lane; qq < M; qq += 32) {
+          uint32_t sv;
           if (qq < nfree) {
-            my_slot = size0 + qq;
-          } else if (lane < cnt) {
-            my_slot = scratch[qq - nfree];
-            my_ev = 1;
+            sv = size0 + qq;
+          } else {
+            const uint32_t v = victims[qq - nfree];
+            sv = v | 0x80000000u;
+            if (defer) atomicOr(&vmap[v >> 5], 1u << (v & 31));   // overlay bitmap
           }
+          slots[qq] = sv;
         }
-        KVR_ACC(9, tp);
-        // lane-parallel apply of this chunk
-        const uint32_t qq = cb + lane;
-        const bool act = lane < cnt;
-        const uint64_t t = act ? H[kf + qq] : 0ull;
-        __syncwarp();
-        if (act && my_ev) {
-          const uint64_t vkey = S.key[my_slot];
-          tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
-          V ^= fmix64(vkey ^ ((uint64_t)(qq - nfree + 1) * kPosMul));
-          if (vlog) {
-            const uint64_t vi = vc + (qq - nfree);
-            if (vi < p.victims_per_trial) vlog[vi] = vkey;
-          }
-        }
-        const uint32_t up = __shfl_up_sync(kFull, my_slot, 1);
-        const uint32_t par_slot = lane == 0 ? prev_last : up;
-        __syncwarp();
-        if (act) {
-          S.key[my_slot] = t;
-          if (rlt) {
-            S.parent[my_slot] = (Idx)par_slot;
-            S.nchild[my_slot] = (Idx)(qq + 1 < M ? 1 : 0);
-          }
-          if (use_list) {
-            if (!rlt) R.stamp[my_slot] = wr.wq;
-            R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] =
-                ((uint64_t)wr.wq << 32) | my_slot;
-          }
-        }
-        __syncwarp();
-        const uint32_t claimed = act ? tbl_insert<Idx>(S, tmask, t, (Idx)my_slot) : 0u;
-        used_add += __popc(__ballot_sync(kFull, claimed != 0));
-        prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
-        pslot = prev_last;
-        __syncwarp();
-        KVR_ACC(10, tp);
-      }
-      if (!rlt) {
-        wr.size = min(B, size0 + M);
+        wr.size = size0 + nfree;
         wr.c_evict += nev;
       }
-      if (rlt && regbits && M) ru.b.store(S.leaf, S.mark, nwords, lane);
       wr.c_ins += M;
-      wr.used += used_add;
-      if (use_list) wr.ltail = ltail0 + n;
-      if (wr.used > (L.T >> 1)) {
-        tbl_rebuild<Idx>(S, L.T, wr.size, lane);
-        wr.used = wr.size;
-      }
-      // order-sensitive victim combination V (XOR over lanes)
-#pragma unroll
-      for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+      __syncwarp();
+      KVR_ACC(8, tp);
 
-      KVR_ACC(11, tp);
       // ---- accounting: Eq. 1 truth, Eq. 2, FIFO single server (A12, A20) ----
       const uint32_t h = bt * m;
       const double hx = (double)h, hy = (double)(q - h);
@@ -1113,7 +1417,6 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       P = P + cost;
       {
         const uint32_t slotf = (fh + fn >= p.ring) ? fh + fn - p.ring : fh + fn;
-        double* r = fifo + (size_t)slotf * 8;
         const double rE = lbgr ? score : 0.0, r0 = lbgr ? f0 : 0.0, r1 = lbgr ? f1 : 0.0,
                      r2 = lbgr ? f2 : 0.0, rC = lbgr ? Chat : 0.0;
         double val = 0.0;
@@ -1128,50 +1431,41 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           case 7: val = __longlong_as_double((long long)k); break;
           default: break;
         }
-        if (lane < 8) r[lane] = val;
+        if (lane < 8) fifo[(size_t)slotf * 8 + lane] = val;
         if (fn == 0) {
-          fr_c = comp; fr_a = a; fr_E = rE; fr_f0 = r0; fr_f1 = r1; fr_f2 = r2; fr_C = rC; fr_ka = k;
+          fr = val;
+          fr_c = comp;
         }
         ++fn;
-        if (fn > c_maxp) c_maxp = fn;
       }
       if (lbgr) Pt = Pt + Chat;   // Eq. 6
-      c_hit += h;
-      c_in += q;
-      ++c_q;
-      if (lane == 0) {
-        uint64_t D = ctrl->digest;   // decision digest
-        D = fmix64(D ^ (uint64_t)j);
-        D = fmix64(D ^ (uint64_t)best);
-        D = fmix64(D ^ (uint64_t)m);
-        D = fmix64(D ^ (uint64_t)nev);
-        D = fmix64(D ^ V);
-        ctrl->digest = D;
-        ctrl->sum_lat = ctrl->sum_lat + lat;
-        ctrl->sum_ttft = ctrl->sum_ttft + ttft;
-        if (lat > ctrl->max_lat) ctrl->max_lat = lat;
-        ctrl->vcursor = vc + nev;
-        if (vlog && vc + nev > p.victims_per_trial)
-          atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
-        if (rec) {
-          kvr_query_record Rq;
-          Rq.worker = best;
-          Rq.hit_tokens = h;
-          Rq.n_victims = nev;
-          Rq._pad = 0;
-          Rq.ttft_ms = ttft;
-          Rq.latency_ms = lat;
-          Rq.score = (lbgr || router == KVR_ROUTE_STATIC_LINEAR) ? score : 0.0;
-          Rq.victim_offset = vc;
-          rec[j] = Rq;
-        }
-        if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
+      if (!rlt && defer && nev) {   // LRU overlay bitmap -> registers
+        vbits = vmap[lane];
+        vmap[lane] = 0u;
       }
+      if (lane == 0) {
+        ws->j = j; ws->buf = buf; ws->n = n; ws->kf = kf; ws->M = M; ws->m = m; ws->nev = nev;
+        ws->h = h; ws->ltail0 = ltail0; ws->wq = wr.wq; ws->p0 = (uint32_t)p0;
+        ws->ttft = ttft; ws->lat = lat; ws->score = score;
+        ws->c_hit += h; ws->c_in += q; ws->c_q += 1;
+        if (fn > ws->c_maxp) ws->c_maxp = fn;
+        ws->active = 1;
+      }
+      if (use_list) wr.ltail = ltail0 + n;
       __syncwarp();
-      KVR_ACC(12, tp);
+      if (!defer) {
+        apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        vbits = 0;
+      }
+      KVR_ACC(9, tp);
     }
 
     // ---- end of trial ----
+    __syncthreads();   // the previous query's deferred apply (ordered sums/digest) comes first
+    if (ws->active) {
+      apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+      vbits = 0;
+    }
     __syncthreads();
     // drain staged-but-unconsumed queries (only after an abort)
     for (uint32_t qd = consumed; qd < issued; ++qd) {
@@ -1180,16 +1474,16 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     }
     gq += issued;
     if (lane == 0) {
-      atomicAdd(&ctrl->cnt[0], (unsigned long long)c_probes);
+      atomicAdd(&ctrl->cnt[0], ws->c_probes);
       atomicAdd(&ctrl->cnt[1], (unsigned long long)wr.c_ins);
       atomicAdd(&ctrl->cnt[2], (unsigned long long)wr.c_evict);
       atomicAdd(&ctrl->cnt[3], (unsigned long long)wr.c_draws);
       atomicAdd(&ctrl->cnt[4], (unsigned long long)wr.c_resets);
       atomicAdd(&ctrl->cnt[5], (unsigned long long)wr.c_fb);
-      atomicAdd(&ctrl->cnt[6], (unsigned long long)c_hit);
-      atomicAdd(&ctrl->cnt[7], (unsigned long long)c_in);
-      atomicAdd(&ctrl->cnt[8], (unsigned long long)c_q);
-      atomicMax(&ctrl->cnt[9], (unsigned long long)c_maxp);
+      atomicAdd(&ctrl->cnt[6], ws->c_hit);
+      atomicAdd(&ctrl->cnt[7], ws->c_in);
+      atomicAdd(&ctrl->cnt[8], (unsigned long long)ws->c_q);
+      atomicMax(&ctrl->cnt[9], (unsigned long long)ws->c_maxp);
       ctrl->P[w] = P;
       ctrl->F[w] = F;
     }

@@ -18,11 +18,12 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2601_18999_b200 import kvr  # noqa: E402
 
-NAMES = ["stage wait", "catch-up", "match", "score", "barrier", "argmin", "upd prologue",
-         "hits", "LRU take", "RLT serial", "apply", "post/rebuild", "accounting"]
+NAMES = ["stage wait", "catch-up", "match", "score", "barrier", "argmin",
+         "deferred apply", "prologue+hits", "miss decisions", "accounting"]
 
 nq = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
 nt = int(sys.argv[2]) if len(sys.argv) > 2 else 444
+Wk = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 trs = bench.build_traces(nq)
 dts = [kvr.DeviceTrace(t) for t in trs]
 L = kvr.lib()
@@ -31,7 +32,7 @@ L.kvr_debug_phase_cycles.restype = C.c_int32
 buf = np.zeros(16, dtype=np.uint64)
 for label, ev in (("RLT", 1), ("LRU", 0)):
     t_of, _, keys = bench.trial_plan(0, nt)
-    sim = kvr.Simulator(8, 512, pending_ring=bench.RING)
+    sim = kvr.Simulator(Wk, 512, pending_ring=bench.RING)
     pols = kvr.policies_array([kvr.Policy(eviction=ev) for _ in keys])
     sim.run(dts, keys[:8], pols[:8], trial_trace=t_of[:8])     # warm-up
     L.kvr_debug_phase_cycles(buf.ctypes.data, 1)
@@ -44,13 +45,13 @@ for label, ev in (("RLT", 1), ("LRU", 0)):
     ms = e0.elapsed_time(e1)
     L.kvr_debug_phase_cycles(buf.ctypes.data, 1)
     q = float(out.results["queries"].sum())
-    print(f"== {label}: {nt} trials x {nq} queries, {ms:.1f} ms, {q / ms / 1e3:.2f} M q-r/s, "
+    print(f"== {label} W={Wk}: {nt} trials x {nq} queries, {ms:.1f} ms, {q / ms / 1e3:.2f} M q-r/s, "
           f"hit {out.results['hit_tokens'].sum() / out.results['input_tokens'].sum():.3f}, "
           f"evict/q {out.results['evictions'].sum() / q:.1f}, probes/q {out.results['probes'].sum() / q:.1f}")
     tot = 0
     for i, n in enumerate(NAMES):
-        per = buf[i] / q / (8 if i <= 5 else 1)
-        if i > 5:
+        per = buf[i] / q / (Wk if i <= 5 else 1)
+        if i > 6:
             tot += per
-        print(f"  {i:2d} {n:14s} {per:10.0f} cycles/query{' (per warp)' if i <= 5 else ' (i*)'}")
+        print(f"  {i:2d} {n:14s} {per:10.0f} cycles/query{' (per warp)' if i <= 6 else ' (i*)'}")
     print(f"  i* update total {tot:.0f} cycles/query")
