@@ -201,7 +201,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kvr", choices=["kvr", "reference"])
-    ap.add_argument("--ref-queries", type=int, default=1500)
+    ap.add_argument("--ref-queries", type=int, default=15000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--queries", type=int, default=N_QUERIES, help=argparse.SUPPRESS)
@@ -241,7 +241,8 @@ def main():
     buf["policies"].copy_(torch.from_numpy(pols.view(np.uint8)))
     buf["trial_trace"].copy_(torch.from_numpy(trace_of.view(np.int32)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    counters = torch.zeros(13, dtype=torch.int64, device=dev)
+    from paper_2601_18999_b200 import dist as kdist
+    summary = [None]
 
     def step(timed_ms):
         flush.fill_(1)                                     # L2 flush, outside the timed region
@@ -252,7 +253,9 @@ def main():
         e0.record(stream)
         sim.launch(dts, n_trials, buf, with_policies=True, stream=stream)
         if world > 1:   # the single NCCL reduce of summary counters
-            dist.reduce(counters, dst=0)
+            vec = kdist.summary_tensor(buf["results"], n_trials)
+            dist.reduce(vec, dst=0)
+            summary[0] = vec
         e1.record(stream)
         torch.cuda.synchronize()
         timed_ms.append(e0.elapsed_time(e1))
@@ -303,11 +306,14 @@ def main():
             "gpu_launches": args.steps * 1,
             "clocks": clk_s}
 
+    if world > 1 and rank == 0 and summary[0] is not None:
+        line["reduced_summary"] = dict(zip(kdist.SUMMARY_FIELDS,
+                                           [int(x) for x in summary[0].cpu().tolist()]))
     if rank == 0 and not args.no_e2e:
         line["e2e"] = e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args)
     if rank == 0 and not args.no_cpu_baseline:
         threads = max(1, min(os.cpu_count() or 1, 16))
-        nq = 1500
+        nq = args.ref_queries
         q, s = run_oracle_sample(traces, trace_of, evict, keys, nq, threads)
         line["cpu_baseline"] = {"value": q / s, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "sample": f"{threads} trials x first {nq} queries of the "
@@ -321,33 +327,41 @@ def main():
 
 def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):
     """Same metric through the public API with HOST buffers: per step the pinned raw
-    traces, keys and policies go host->device, kvr_trace_load packs them, kvr_sim_run_multi
-    replays, and the per-trial results come back device->host, all inside the timed region."""
+    traces, keys, policies and trial->trace map go host->device, kvr_trace_load packs
+    (validates, chains) them, kvr_sim_run_multi replays, and the per-trial results come
+    back device->host into pinned memory, all inside the timed region."""
     import torch
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator
 
     sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING)
     n = len(keys)
-    pinned = {}
-    h2d = 0
-    for i, t in enumerate(traces):
-        for name in ("arrival_ms", "n_in_blocks", "n_out_blocks", "out_tokens", "block_offsets",
-                     "block_keys"):
-            h2d += getattr(t, name).nbytes
-    h2d += keys.nbytes + pols.nbytes + trace_of.nbytes
+    host = [DeviceTrace.pin(t) for t in traces]                     # pinned, outside timing
+    h_keys = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    h_pols = torch.from_numpy(pols.view(np.uint8)).pin_memory()
+    h_tt = torch.from_numpy(trace_of.view(np.int32)).pin_memory()
+    h_res = torch.empty(n * 144, dtype=torch.uint8).pin_memory()
+    h2d = sum(int(v.numel() * v.element_size()) for hd in host for v in hd.values())
+    h2d += int(h_keys.numel() * 8 + h_pols.numel() + h_tt.numel() * 4)
     d2h = n * 144
     times = []
+    q = 0.0
     for it in range(2 + max(1, args.steps // 2)):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        dts = [DeviceTrace(t, device=dev, pinned=False) for t in traces]
-        out = sim.run(dts, keys, pols, trial_trace=trace_of, stream=stream)
+        dts = [DeviceTrace(t, device=dev, host=hd) for t, hd in zip(traces, host)]
+        b = sim.alloc(dts, n, 0, dev)
+        b["keys"].copy_(h_keys, non_blocking=True)
+        b["policies"].copy_(h_pols, non_blocking=True)
+        b["trial_trace"].copy_(h_tt, non_blocking=True)
+        sim.launch(dts, n, b, with_policies=True, stream=stream)
+        h_res.copy_(b["results"][: n * 144], non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         if it >= 2:
             times.append(e0.elapsed_time(e1))
-        q = float(out.results["queries"].sum())
+        from paper_2601_18999_b200.kvr import RESULT_DTYPE
+        q = float(h_res.numpy().view(RESULT_DTYPE)["queries"].sum())
         for d in dts:
             d.close()
     ms = float(np.mean(times))

@@ -274,26 +274,39 @@ def policies_array(pols: Sequence[Policy]) -> np.ndarray:
 class DeviceTrace:
     """Raw trace uploaded to torch device tensors and packed by kvr_trace_load."""
 
-    def __init__(self, raw, device="cuda", stream=None, pinned: bool = False):
+    FIELDS = (("arrival", "arrival_ms", np.float64, np.float64),
+              ("n_in", "n_in_blocks", np.uint32, np.int32),
+              ("n_out", "n_out_blocks", np.uint32, np.int32),
+              ("out_tokens", "out_tokens", np.uint32, np.int32),
+              ("offsets", "block_offsets", np.uint64, np.int64),
+              ("keys", "block_keys", np.uint64, np.int64))
+
+    @staticmethod
+    def pin(raw) -> dict:
+        """Pinned host copies of the raw trace arrays (for timed host->device uploads).
+        Unsigned arrays travel as same-width signed torch dtypes (bit patterns preserved)."""
+        import torch
+        out = {}
+        for attr, name, src, dst in DeviceTrace.FIELDS:
+            a = getattr(raw, name)
+            if attr == "keys" and len(a) == 0:
+                a = np.zeros(1, np.uint64)
+            out[attr] = torch.from_numpy(np.ascontiguousarray(a.astype(src)).view(dst)).pin_memory()
+        return out
+
+    def __init__(self, raw, device="cuda", stream=None, host: Optional[dict] = None):
         import torch
         self.raw = raw
         self.device = torch.device(device)
-        kw = dict(device=self.device, non_blocking=True)
-
-        def up(a, dt):
-            t = torch.from_numpy(np.ascontiguousarray(a).view(dt))
-            if pinned:
-                t = t.pin_memory()
-            return t.to(**kw)
-
-        # unsigned arrays travel as same-width signed torch dtypes (bit patterns preserved)
-        self.arrival = up(raw.arrival_ms.astype(np.float64), np.float64)
-        self.n_in = up(raw.n_in_blocks.astype(np.uint32), np.int32)
-        self.n_out = up(raw.n_out_blocks.astype(np.uint32), np.int32)
-        self.out_tokens = up(raw.out_tokens.astype(np.uint32), np.int32)
-        self.offsets = up(raw.block_offsets.astype(np.uint64), np.int64)
-        keys = raw.block_keys if len(raw.block_keys) else np.zeros(1, np.uint64)
-        self.keys = up(keys.astype(np.uint64), np.int64)
+        for attr, name, src, dst in self.FIELDS:
+            if host is not None:
+                t = host[attr]
+            else:
+                a = getattr(raw, name)
+                if attr == "keys" and len(a) == 0:
+                    a = np.zeros(1, np.uint64)
+                t = torch.from_numpy(np.ascontiguousarray(a.astype(src)).view(dst))
+            setattr(self, attr, t.to(device=self.device, non_blocking=True))
         d = kvr_trace_desc()
         d.n_queries = raw.n_queries
         d.block_tokens = raw.block_tokens
