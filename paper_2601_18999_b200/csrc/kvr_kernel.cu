@@ -684,6 +684,57 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
   uint32_t q = 0;
 #pragma unroll 1
   for (; q < M; ++q) {
+    // ---- fast segment: evictions with no mark reset, no refill, U != {}, q > 0 ----
+    // (victims are old nodes, so their parents are never the excluded p; the new
+    // node's parent p is the previous new node, marked, hence outside U)
+    if (q > 0 && wr.size == B && !dirty && wr.cntT < B && total > 0 && ri < 32) {
+      const uint32_t lim = min(M, min(q + (B - wr.cntT), q + (32u - ri)));
+#pragma unroll 1
+      for (; q < lim && total > 0; ++q) {
+        ++wr.cntT;
+        const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+        ++ri;
+        const uint32_t idx = pick32(dlo, dhi, total);
+        const uint32_t owner = __popc(__ballot_sync(kFull, incl <= idx));
+        const uint32_t ou = __shfl_sync(kFull, uw, owner);
+        const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
+        const uint32_t bit = __popc(__ballot_sync(kFull, (uint32_t)__popc(ou & lmle) <= rem));
+        const uint32_t v = owner * 32 + bit;
+        const uint32_t vb = 1u << bit;
+        if (lane == owner) {
+          uw &= ~vb;
+          rb.mw |= vb;
+          vbits |= vb;
+        }
+        if (lane >= owner) --incl;
+        --total;
+        const uint32_t pv = (uint32_t)S.parent[v];
+        const bool hasp = pv != (uint32_t)NIL;
+        const uint32_t pvs = hasp ? pv : 0u;
+        const Idx nc = (Idx)(S.nchild[pvs] - 1);
+        __syncwarp();
+        if (hasp) S.nchild[pvs] = nc;   // uniform store
+        const bool leafp = hasp && nc == 0;
+        const uint32_t pw = pvs >> 5, pb = 1u << (pvs & 31);
+        const bool add = __ballot_sync(kFull, leafp && lane == pw && !(rb.mw & pb)) != 0u;
+        if (leafp && lane == pw) {
+          rb.lw |= pb;
+          if (add) uw |= pb;
+        }
+        if (add) {
+          if (lane >= pw) ++incl;
+          ++total;
+        }
+        if (lane == (p >> 5)) rb.lw &= ~(1u << (p & 31));   // previous new node gets a child
+        if (use_list) R.stamp[v] = (uint16_t)wr.wq;
+        slots[q] = v | 0x80000000u;
+        p = v;
+        ++wr.e;
+        ++wr.c_draws;
+        ++wr.c_evict;
+      }
+      if (q >= M) break;
+    }
     if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t (t is not cached: not in T)
       rb.mw = 0u;
       wr.cntT = 1;
