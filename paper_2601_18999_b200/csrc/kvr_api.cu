@@ -329,8 +329,8 @@ kvr_status kvr_sim_run(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
 }
 
 /* profiling builds only (not declared in kvr.h): per-phase cycle sums */
-kvr_status kvr_debug_phase_cycles(uint64_t* out16, int reset) {
-  cudaError_t e = kvr::phase_cycles((unsigned long long*)out16, reset);
+kvr_status kvr_debug_phase_cycles(uint64_t* out32, int reset) {
+  cudaError_t e = kvr::phase_cycles((unsigned long long*)out32, reset);
   if (e != cudaSuccess) return cuda_fail(e, "phase profile");
   return KVR_OK;
 }

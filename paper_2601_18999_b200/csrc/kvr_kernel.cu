@@ -38,7 +38,7 @@ namespace kvr {
 
 #ifdef KVR_PHASE_PROFILE
 // Phase profiler (profiling build only): cycles per phase summed over warps.
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[32];
 #define KVR_T0(v) unsigned long long v = clock64()
 #define KVR_ACC(ph, v)                                                     \
   do {                                                                     \
@@ -46,9 +46,14 @@ __device__ unsigned long long g_phase_cycles[16];
     if (lane == 0) atomicAdd(&g_phase_cycles[ph], _n - (v));               \
     v = _n;                                                                \
   } while (0)
+#define KVR_CNT(ph, x)                                                     \
+  do {                                                                     \
+    if (lane == 0) atomicAdd(&g_phase_cycles[ph], (unsigned long long)(x)); \
+  } while (0)
 #else
 #define KVR_T0(v) (void)0
 #define KVR_ACC(ph, v) (void)0
+#define KVR_CNT(ph, x) (void)0
 #endif
 
 // Dynamic shared memory of the replay kernel.  Every function derives its
@@ -195,6 +200,8 @@ __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
 // stale entry never survives one compaction period, < 2^16 worker queries).  The first
 // e valid entries from the head are the e least-recently-used nodes in
 // (stamp, -depth) order because each query appends its path deepest first.
+constexpr int kLogDepth = 4;   // log windows (32 entries each) kept in flight
+
 struct RecencyLog {
   uint64_t* log;
   uint16_t* stamp;   // per slot, in the worker state (shared memory in tier 1)
@@ -206,27 +213,38 @@ struct RecencyLog {
 __device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
                                           uint32_t need, uint32_t* out, uint32_t lane) {
   uint32_t k = 0, pos = head;
-  // software pipeline: the next window's entries are in flight while this one is filtered
-  uint64_t ent = (pos + lane < tail) ? R.log[(pos + lane) & R.cap_mask] : 0ull;
-#pragma unroll 1
-  while (k < need && pos < tail) {
-    const uint32_t nxt = pos + 32 + lane;
-    const uint64_t ent_next = (nxt < tail) ? R.log[nxt & R.cap_mask] : 0ull;
-    const bool act = pos + lane < tail;
-    const uint32_t slot = (uint32_t)ent;
-    const bool valid = act && R.stamp[slot] == (uint16_t)(ent >> 32);
-    const uint32_t bal = __ballot_sync(kFull, valid);
-    const uint32_t nv = __popc(bal);
-    const uint32_t take = min(nv, need - k);
-    const uint32_t rank = __popc(bal & lanemask_lt(lane));
-    if (valid && rank < take) out[k + rank] = slot;
-    k += take;
-    if (take > 0 && k == need) pos += select_bit(bal, take - 1) + 1u;   // through the last victim
-    else pos += 32u;
-    ent = ent_next;
+  // software pipeline: kLogDepth windows of entries are in flight while one is filtered
+  uint64_t e[kLogDepth];
+#pragma unroll
+  for (int i = 0; i < kLogDepth; ++i) {
+    const uint32_t idx = pos + 32u * i + lane;
+    e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
   }
-  __syncwarp();
-  return pos;
+#pragma unroll 1
+  for (;;) {
+#pragma unroll
+    for (int i = 0; i < kLogDepth; ++i) {
+      if (k >= need || pos >= tail) {
+        __syncwarp();
+        return pos;
+      }
+      const bool act = pos + lane < tail;
+      const uint32_t slot = (uint32_t)e[i];
+      const bool valid = act && R.stamp[slot] == (uint16_t)(e[i] >> 32);
+      const uint32_t bal = __ballot_sync(kFull, valid);
+      const uint32_t take = min((uint32_t)__popc(bal), need - k);
+      const uint32_t rank = __popc(bal & lanemask_lt(lane));
+      if (valid && rank < take) out[k + rank] = slot;
+      k += take;
+      if (take > 0 && k == need) {
+        pos += select_bit(bal, take - 1) + 1u;   // through the last victim
+      } else {
+        const uint32_t idx = pos + 32u * kLogDepth + lane;
+        e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
+        pos += 32u;
+      }
+    }
+  }
 }
 
 // first valid entry from head (LRU over leaves != parent(t), fallback A5)
@@ -246,17 +264,29 @@ __device__ __forceinline__ uint32_t log_first_valid(const RecencyLog& R, uint32_
 // in-place order-preserving compaction of [head, tail): returns the new tail
 __device__ __forceinline__ uint32_t log_compact(const RecencyLog& R, uint32_t head, uint32_t tail,
                                              uint32_t lane) {
+  // kLogDepth windows per step: all loads and stamp gathers are independent, only
+  // the write cursor is serial.  Writes land below r + 32*kLogDepth (already read),
+  // so the in-place order-preserving copy never clobbers an unread entry.
   uint32_t w = head;
 #pragma unroll 1
-  for (uint32_t r = head; r < tail; r += 32) {
-    const uint32_t idx = r + lane;
-    const bool act = idx < tail;
-    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
-    const bool valid = act && R.stamp[(uint32_t)ent] == (uint16_t)(ent >> 32);
-    const uint32_t bal = __ballot_sync(kFull, valid);
+  for (uint32_t r = head; r < tail; r += 32u * kLogDepth) {
+    uint64_t e[kLogDepth];
+    bool v[kLogDepth];
+#pragma unroll
+    for (int i = 0; i < kLogDepth; ++i) {
+      const uint32_t idx = r + 32u * i + lane;
+      e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
+    }
+#pragma unroll
+    for (int i = 0; i < kLogDepth; ++i)
+      v[i] = (r + 32u * i + lane < tail) && R.stamp[(uint32_t)e[i]] == (uint16_t)(e[i] >> 32);
     __syncwarp();
-    if (valid) R.log[(w + __popc(bal & lanemask_lt(lane))) & R.cap_mask] = ent;
-    w += __popc(bal);
+#pragma unroll
+    for (int i = 0; i < kLogDepth; ++i) {
+      const uint32_t bal = __ballot_sync(kFull, v[i]);
+      if (v[i]) R.log[(w + __popc(bal & lanemask_lt(lane))) & R.cap_mask] = e[i];
+      w += __popc(bal);
+    }
     __syncwarp();
   }
   return w;
@@ -1341,6 +1371,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
+#ifdef KVR_PHASE_PROFILE
+      if (w == best && clock64() - tp > 200) {   // an apply on the critical path
+        KVR_CNT(16, clock64() - tp);
+        KVR_CNT(17, 1);
+      }
+#endif
       KVR_ACC(6, tp);
 
       if (w != best) continue;
@@ -1355,10 +1391,17 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       ++wr.wq;
       // log room for this query's n entries (Leaf-LRU order)
-      if (use_list && wr.ltail - wr.lhead + n > p.aux.log_cap)
+      if (use_list && wr.ltail - wr.lhead + n > p.aux.log_cap) {
+        KVR_T0(tc);
+        KVR_CNT(13, wr.ltail - wr.lhead);
         wr.ltail = log_compact(R, wr.lhead, wr.ltail, lane);
+        KVR_ACC(10, tc);
+        KVR_CNT(14, wr.ltail - wr.lhead);
+        KVR_CNT(15, 1);
+      }
       const uint32_t ltail0 = wr.ltail;
 
+      KVR_T0(tk);
       // full-path cached prefix kf (hits of Gamma_j; m covers the input part)
       uint32_t kf = m;
       if (m == n_in) {
@@ -1378,6 +1421,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         if (kf > n) kf = n;
       }
 
+      KVR_ACC(18, tk);
       // ---- hits: marks (Alg. 1 l.6-9), recency stamps, log entries ----
       Idx p0 = NIL;
 #pragma unroll 1
@@ -1410,6 +1454,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         p0 = (Idx)__shfl_sync(kFull, (uint32_t)s, min(31u, kf - 1 - base));
       }
       __syncwarp();
+      KVR_ACC(19, tk);
       KVR_ACC(7, tp);
 
       // ---- misses: decisions (victims and slots) ----
@@ -1434,7 +1479,13 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         }
       } else {
         // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
-        if (nev) wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
+        if (nev) {
+          KVR_T0(tt);
+          const uint32_t h0 = wr.lhead;
+          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
+          KVR_ACC(11, tt);
+          KVR_CNT(12, wr.lhead - h0);
+        }
 #pragma unroll 1
         for (uint32_t qq = lane; qq < M; qq += 32) {
           uint32_t sv;
@@ -1603,9 +1654,9 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
 
 cudaError_t phase_cycles(unsigned long long* out16, int reset) {
 #ifdef KVR_PHASE_PROFILE
-  cudaError_t e = cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * sizeof(unsigned long long));
+  cudaError_t e = cudaMemcpyFromSymbol(out16, g_phase_cycles, 32 * sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   }
   return e;

@@ -29,7 +29,7 @@ dts = [kvr.DeviceTrace(t) for t in trs]
 L = kvr.lib()
 L.kvr_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
 L.kvr_debug_phase_cycles.restype = C.c_int32
-buf = np.zeros(16, dtype=np.uint64)
+buf = np.zeros(32, dtype=np.uint64)
 for label, ev in (("RLT", 1), ("LRU", 0)):
     t_of, _, keys = bench.trial_plan(0, nt)
     sim = kvr.Simulator(Wk, 512, pending_ring=bench.RING)
@@ -55,3 +55,9 @@ for label, ev in (("RLT", 1), ("LRU", 0)):
             tot += per
         print(f"  {i:2d} {n:14s} {per:10.0f} cycles/query{' (per warp)' if i <= 6 else ' (i*)'}")
     print(f"  i* update total {tot:.0f} cycles/query")
+    nc = max(int(buf[15]), 1)
+    print(f"  LRU log: compactions {int(buf[15])} ({buf[10] / q:.0f} cycles/query, "
+          f"{buf[10] / nc:.0f} cycles each, len {buf[13] / nc:.0f} -> {buf[14] / nc:.0f}); "
+          f"take {buf[11] / q:.0f} cycles/query, {buf[12] / q:.1f} entries scanned/query")
+    print(f"  critical-path applies: {int(buf[17])} of {int(q)} queries, {buf[16] / max(int(buf[17]), 1):.0f} cycles each; "
+          f"kf {buf[18] / q:.0f}, hits loop {buf[19] / q:.0f} cycles/query")
