@@ -536,17 +536,19 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     if (lat > out->max_latency_ms) out->max_latency_ms = lat;
     out->queries++;
 
-    // 6. decision digest (DESIGN.md §3 "decision digest"): per query the index,
-    //    the chosen worker, its hit blocks, the victim count and an order-sensitive
-    //    combination of the victims, V = XOR_k fmix64(H_{v_k} ^ (k+1)*K).
+    // 6. decision digest (DESIGN.md §3 "decision digest"): per query a tuple hash
+    //    T_j of the index, the chosen worker, its hit blocks, the victim count and an
+    //    order-sensitive combination of the victims, V = XOR_k fmix64(H_{v_k} ^ (k+1)*K);
+    //    D = K + sum_j T_j mod 2^64 (order-independent across queries; K = trial key).
     uint64_t V = 0;
     for (size_t k = 0; k < ux.victims.size(); ++k)
       V ^= fmix64(ux.victims[k] ^ ((uint64_t)(k + 1) * K_POS));
-    D = fmix64(D ^ (uint64_t)j);
-    D = fmix64(D ^ (uint64_t)best);
-    D = fmix64(D ^ (uint64_t)m[best]);
-    D = fmix64(D ^ (uint64_t)ux.victims.size());
-    D = fmix64(D ^ V);
+    uint64_t T = fmix64(K ^ (uint64_t)j);
+    T = fmix64(T ^ (uint64_t)best);
+    T = fmix64(T ^ (uint64_t)m[best]);
+    T = fmix64(T ^ (uint64_t)ux.victims.size());
+    T = fmix64(T ^ V);
+    D += T;
 
     if (records) {
       kvro_query_record& R = records[j];

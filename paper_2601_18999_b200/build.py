@@ -60,5 +60,15 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     return lib
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment build libkvr_<name>.so with extra -D flags (scripts only, via KVR_LIB)."""
+    lib = os.path.join(PKG, f"libkvr_{name}.so")
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"]
+    cmd += [f"-D{d}" for d in defines] + [os.path.join(CSRC, f) for f in SOURCES]
+    subprocess.run(cmd, check=True)
+    os.replace(lib + ".tmp", lib)
+    return lib
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

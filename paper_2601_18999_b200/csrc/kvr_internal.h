@@ -96,7 +96,7 @@ struct __align__(16) Ctrl {
   uint32_t npend[2][kMaxW];
   double P[kMaxW], F[kMaxW];
   double sum_lat, sum_ttft, max_lat;
-  unsigned long long digest, vcursor;
+  unsigned long long digest, dkey, vcursor;
   unsigned long long cnt[10];   // probes, inserted, evictions, draws, resets, fallbacks, hit, in, queries, maxpend
   kvr_policy pol;                      // this trial's policy
   uint32_t trial, status, abortf[2];   // abort flag double-buffered by query parity
@@ -110,6 +110,7 @@ inline size_t stage_bytes(uint32_t max_n) { return align16(sizeof(QueryHdr) + 8 
 // staging area, and the worker's trial counters.
 struct __align__(16) WarpSm {
   double ttft, lat, score;
+  unsigned long long vc;           // victim-log offset of the pending update
   unsigned long long c_probes, c_hit, c_in;
   uint32_t active, j, buf, n, kf, M, m, nev, h, ltail0, wq, p0;
   uint32_t c_q, c_maxp, _pad[2];

@@ -39,6 +39,7 @@ namespace kvr {
 #ifdef KVR_PHASE_PROFILE
 // Phase profiler (profiling build only): cycles per phase summed over warps.
 __device__ unsigned long long g_phase_cycles[32];
+__device__ unsigned long long g_trial_cycles[4096];   // per trial: kernel cycles of its CTA
 #define KVR_T0(v) unsigned long long v = clock64()
 #define KVR_ACC(ph, v)                                                     \
   do {                                                                     \
@@ -50,7 +51,9 @@ __device__ unsigned long long g_phase_cycles[32];
   do {                                                                     \
     if (lane == 0) atomicAdd(&g_phase_cycles[ph], (unsigned long long)(x)); \
   } while (0)
+#define KVR_RESET(v) v = clock64()
 #else
+#define KVR_RESET(v) (void)0
 #define KVR_T0(v) (void)0
 #define KVR_ACC(ph, v) (void)0
 #define KVR_CNT(ph, x) (void)0
@@ -418,51 +421,6 @@ __device__ __noinline__ uint64_t philox_refill(uint64_t K, uint64_t n, uint32_t 
   return philox_r64(K, n, worker, 1u);
 }
 
-// Register bitmaps plus an incrementally maintained prefix count of
-// U = LEAF & ~MARK & ~{p}: in the common eviction step U only loses the victim
-// (its slot is immediately refilled by the new, marked leaf) and possibly gains
-// the victim's parent when that becomes an unmarked leaf, so the per-lane
-// inclusive counts are patched with two compares instead of a full recount.
-struct RegU {
-  RegBits b;
-  uint32_t incl, total;
-  bool dirty;
-  __device__ __forceinline__ void recount(uint32_t p, uint32_t lane) {
-    uint32_t c;
-    total = b.count(p, true, lane, c, incl);
-    dirty = false;
-  }
-  // idx-th element of U (requires !dirty): the owner lane's word and exclusive
-  // count are broadcast, every lane tests whether bit `lane` of that word is the
-  // wanted one, and a ballot names it (no serial bit-select chain)
-  __device__ __forceinline__ uint32_t pick(uint32_t p, uint32_t lane, uint32_t idx) const {
-    const uint32_t owner = __ffs(__ballot_sync(kFull, incl > idx)) - 1;
-    uint32_t u = b.lw & ~b.mw;
-    if (lane == (p >> 5)) u &= ~(1u << (p & 31));
-    const uint32_t base = incl - (uint32_t)__popc(u);
-    const uint32_t ou = __shfl_sync(kFull, u, owner);
-    const uint32_t rem = idx - __shfl_sync(kFull, base, owner);
-    const bool hit = ((ou >> lane) & 1u) && (uint32_t)__popc(ou & lanemask_lt(lane)) == rem;
-    return owner * 32 + (__ffs(__ballot_sync(kFull, hit)) - 1);
-  }
-  // U loses v (slot v now holds the new marked leaf: LEAF bit stays, MARK bit set)
-  __device__ __forceinline__ void evict_refill(uint32_t v, uint32_t lane) {
-    if (lane >= (v >> 5)) --incl;
-    --total;
-    b.mark_set(v, lane);
-  }
-  // pv became a leaf; it joins U iff unmarked and not the excluded parent p
-  __device__ __forceinline__ void parent_leaf(uint32_t pv, uint32_t p, uint32_t lane) {
-    const bool own = lane == (pv >> 5);
-    const bool add = __ballot_sync(kFull, own && !((b.mw >> (pv & 31)) & 1u)) != 0u && pv != p;
-    b.leaf_set(pv, lane);
-    if (add) {
-      if (lane >= (pv >> 5)) ++incl;
-      ++total;
-    }
-  }
-};
-
 // Per-warp (worker) scalar and sequential state of one trial.
 struct WorkerRegs {
   uint32_t size, cntT, used, wq, lhead, ltail;
@@ -558,117 +516,6 @@ __device__ __forceinline__ void rlt_chunk(Bits& bits, const WorkerView<Idx>& S, 
     if (use_list) R.stamp[slot] = wr.wq;
     slots[q] = slot | (ev << 31);
     if (ev && lane == (slot >> 5)) vbits |= 1u << (slot & 31);
-    pslot = slot;
-  }
-}
-
-// RLT decisions with register bitmaps and incremental U counts (B <= 1024).
-template <typename Idx>
-__device__ __forceinline__ void rlt_chunk_reg(RegU& U, const WorkerView<Idx>& S, const RecencyLog& R,
-                                              WorkerRegs& wr, uint32_t B, uint32_t cnt, uint32_t cb,
-                                              Idx p0, uint32_t& pslot, uint32_t fallback,
-                                              uint64_t K, uint32_t worker, uint64_t& rbuf,
-                                              uint32_t& ri, uint32_t lane, uint32_t* slots,
-                                              uint32_t& vbits, bool use_list) {
-  const Idx NIL = Nil<Idx>::empty;
-#pragma unroll 1
-  for (uint32_t r = 0; r < cnt; ++r) {
-    const uint32_t q = cb + r;
-    if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t
-      U.b.mark_clear_all_w(lane);
-      wr.cntT = 1;
-      ++wr.c_resets;
-      U.dirty = true;
-    } else {
-      ++wr.cntT;
-    }
-    uint32_t slot, ev = 0;
-    if (wr.size < B) {
-      slot = wr.size++;
-      U.b.leaf_set(slot, lane);   // new marked leaf: not in U
-      U.b.mark_set(slot, lane);
-    } else {
-      if (U.dirty) U.recount(pslot, lane);
-      uint32_t v;
-      bool vmarked = false, generic = false;
-      if (U.total == 0) {   // U = {} (A5)
-        ++wr.c_fb;
-        if (fallback == KVR_RLT_EARLY_RESET) {
-          U.b.mark_clear_all_w(lane);
-          wr.cntT = 1;
-          ++wr.c_resets;
-          U.recount(pslot, lane);
-        } else {
-          generic = true;
-        }
-      }
-      if (!generic || fallback == KVR_RLT_UNIFORM_LEAF) {
-        if (ri == 32) {   // refill 32 counter-based draws e .. e+31, one per lane
-          rbuf = philox_refill(K, wr.e + lane, worker);
-          ri = 0;
-        }
-        const uint64_t rr = __shfl_sync(kFull, rbuf, ri);
-        ++ri;
-        ++wr.e;
-        ++wr.c_draws;
-        if (!generic) {
-          v = U.pick(pslot, lane, (uint32_t)pick_index(rr, U.total));
-        } else {   // UNIFORM_LEAF: uniform over leaves != p, marks ignored
-          uint32_t c, incl;
-          const uint32_t tot = U.b.count(pslot, false, lane, c, incl);
-          const uint32_t sel =
-              U.b.select(pslot, false, lane, c, incl, (uint32_t)pick_index(rr, tot));
-          v = sel & 0x7fffffffu;
-          vmarked = (sel >> 31) != 0;
-        }
-      } else {   // LRU_MARKED: least recently used leaf != p, no draw
-        v = log_first_valid(R, wr.lhead, wr.ltail, lane);
-        vmarked = U.b.mark_test(v);
-      }
-      const Idx pv = S.parent[v];
-      // (uniform stores: every lane writes the same value after the warp-wide load)
-      if (!generic) {
-        U.evict_refill(v, lane);
-        if (pv != NIL) {
-          const Idx nc = (Idx)(S.nchild[pv] - 1);
-          __syncwarp();
-          S.nchild[pv] = nc;
-          if (nc == 0) U.parent_leaf(pv, pslot, lane);
-        }
-      } else {
-        U.b.leaf_clr(v, lane);
-        if (vmarked) {
-          U.b.mark_clr(v, lane);
-          --wr.cntT;
-        }
-        if (pv != NIL) {
-          const Idx nc = (Idx)(S.nchild[pv] - 1);
-          __syncwarp();
-          S.nchild[pv] = nc;
-          if (nc == 0) U.b.leaf_set(pv, lane);
-        }
-        U.b.leaf_set(v, lane);
-        U.b.mark_set(v, lane);
-        U.dirty = true;
-      }
-      ++wr.c_evict;
-      slot = v;
-      ev = 1;
-      if (lane == (v >> 5)) vbits |= 1u << (v & 31);
-    }
-    // the new node's parent stops being a leaf (it is excluded or marked: U unchanged)
-    if (q == 0) {
-      if (p0 != NIL) {
-        const Idx nc = S.nchild[p0];
-        __syncwarp();
-        S.nchild[p0] = (Idx)(nc + 1);
-        if (nc == 0) U.b.leaf_clr(p0, lane);
-      }
-    } else {
-      U.b.leaf_clr(pslot, lane);
-    }
-    if (use_list) R.stamp[slot] = wr.wq;   // LRU_MARKED fallback reads the log
-    slots[q] = slot | (ev << 31);
     pslot = slot;
   }
 }
@@ -792,7 +639,7 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         if (fallback == KVR_RLT_EARLY_RESET) {
           rb.mw = 0u;
           wr.cntT = 1;
-          ++wr.c_resets;
+              ++wr.c_resets;
           uw = rb.lw;
           if (lane == (p >> 5)) uw &= ~(1u << (p & 31));
           uint32_t c;
@@ -911,7 +758,8 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
 }
 
 // Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
-// victim digest, ordered trial sums, records and histogram.
+// victim digest term and the query record (trial sums are added in query order
+// by the accounting step).
 template <typename Idx, bool kGlobal, int kTag>
 __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr, uint32_t lane,
                                           uint32_t w, bool rlt, bool use_list, bool lbgr_or_static,
@@ -931,7 +779,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr,
   H += (reinterpret_cast<const QueryHdr*>(stage + (size_t)ws->buf * p.stage_bytes)->block_off & 1);
   const uint32_t n = ws->n, kf = ws->kf, M = ws->M, nev = ws->nev, wq = ws->wq, ltail0 = ws->ltail0;
   const uint32_t nfree = M - nev;
-  const uint64_t vc = ctrl->vcursor;
+  const uint64_t vc = ws->vc;
   uint64_t V = 0;
   uint32_t used_add = 0, prev_last = ws->p0;
 #pragma unroll 1
@@ -980,20 +828,14 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr,
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
   if (lane == 0) {
-    uint64_t D = ctrl->digest;   // decision digest
-    D = fmix64(D ^ (uint64_t)ws->j);
-    D = fmix64(D ^ (uint64_t)w);
-    D = fmix64(D ^ (uint64_t)ws->m);
-    D = fmix64(D ^ (uint64_t)nev);
-    D = fmix64(D ^ V);
-    ctrl->digest = D;
+    // decision digest: D += T_j, order-independent across queries
+    uint64_t T = fmix64(ctrl->dkey ^ (uint64_t)ws->j);
+    T = fmix64(T ^ (uint64_t)w);
+    T = fmix64(T ^ (uint64_t)ws->m);
+    T = fmix64(T ^ (uint64_t)nev);
+    T = fmix64(T ^ V);
+    atomicAdd(&ctrl->digest, T);
     const double lat = ws->lat, ttft = ws->ttft;
-    ctrl->sum_lat = ctrl->sum_lat + lat;
-    ctrl->sum_ttft = ctrl->sum_ttft + ttft;
-    if (lat > ctrl->max_lat) ctrl->max_lat = lat;
-    ctrl->vcursor = vc + nev;
-    if (vlog && vc + nev > p.victims_per_trial)
-      atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
     if (rec) {
       kvr_query_record Rq;
       Rq.worker = w;
@@ -1006,7 +848,6 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr,
       Rq.victim_offset = vc;
       rec[ws->j] = Rq;
     }
-    if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
     ws->active = 0;
   }
   __syncwarp();
@@ -1081,6 +922,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // deferred apply needs the overlay (register victim bitmap): B <= 1024
     const bool defer = regbits;
 
+#ifdef KVR_PHASE_PROFILE
+    const unsigned long long t_trial0 = clock64();
+#endif
     // ---- per-trial init: empty caches S_i^(0), P_i^(0) = 0 ----
     for (uint32_t i = lane; i < L.T; i += 32) S.table[i] = NIL;
     for (uint32_t i = lane; i < nwords; i += 32) {
@@ -1111,6 +955,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       ctrl->sum_ttft = 0.0;
       ctrl->max_lat = 0.0;
       ctrl->digest = K;
+      ctrl->dkey = K;
       ctrl->vcursor = 0;
       ctrl->abortf[0] = 0;
       ctrl->abortf[1] = 0;
@@ -1154,22 +999,16 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     __syncthreads();
 
     uint32_t consumed = 0;
-#pragma unroll 1
-    for (uint32_t j = 0; j < Nrun; ++j) {
-      const uint64_t g = gq + j;
-      const uint32_t buf = (uint32_t)(g % kNumStages);
-      KVR_T0(tp);
-      mbar_wait(&ctrl->mbar[buf], (uint32_t)((g / kNumStages) & 1));
-      KVR_ACC(0, tp);
-      consumed = j + 1;
-      const uint8_t* st = stage + (size_t)buf * p.stage_bytes;
-      const QueryHdr hd = *reinterpret_cast<const QueryHdr*>(st);
-      const uint64_t* H = reinterpret_cast<const uint64_t*>(st + 32) + (hd.block_off & 1);
-      const double a = hd.arrival_ms;
-      const uint32_t n_in = hd.n_in, n = hd.n_in + hd.n_out;
-      const uint32_t q = bt * n_in;
 
-      // ---- 1. catch-up (A11: tick before completion before routing) ----
+    // ---- steps 1-3 of one query for this warp's worker ----
+    // Membership = the table, or the path Hp[0..np) (same position, same identity),
+    // minus the pending update's victims (register bitmap vbits) if minus_victims.
+    auto score_query = [&](const uint64_t* Hq, double aq, uint32_t nq_in, uint32_t qtok,
+                           const uint64_t* Hp, uint32_t np, bool minus_victims, uint32_t& m_o,
+                           double& score_o, double& Chat_o, double& f0_o, double& f1_o,
+                           double& f2_o) {
+      KVR_T0(tl);
+      // 1. catch-up (A11: tick before completion before routing)
       {
         const double rho = pol.rho, dt = pol.delta_t_ms;
 #pragma unroll 1
@@ -1178,7 +1017,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             // every tick k' with (double)k'*dt <= min(a, c) comes first (A11); (double)k'*dt
             // is monotone in k', so find the last such k' and apply the multiplications
             // one by one (same rounding sequence as a per-tick loop)
-            const double lim = (fn == 0 || a < fr_c) ? a : fr_c;
+            const double lim = (fn == 0 || aq < fr_c) ? aq : fr_c;
             const double est = lim / dt;
             uint64_t kk = est < 1.8e19 ? (uint64_t)est : k;
             if (kk < k) kk = k;
@@ -1186,8 +1025,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             while (kk > k && (double)kk * dt > lim) --kk;
             if (kk > k) {
               if (Pt != 0.0) {
-#pragma unroll 1
                 uint32_t nt = (uint32_t)(kk - k);
+#pragma unroll 1
                 for (; nt >= 4; nt -= 4) {
                   Pt = rho * Pt;
                   Pt = rho * Pt;
@@ -1199,27 +1038,27 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
               k = kk;
             }
           }
-          if (fn != 0 && fr_c <= a) {
+          if (fn != 0 && fr_c <= aq) {
             fh = (fh + 1 == p.ring) ? 0 : fh + 1;
             --fn;
             if (lbgr) {
               const double fa = __shfl_sync(kFull, fr, 1), fE = __shfl_sync(kFull, fr, 2);
-              const double f0 = __shfl_sync(kFull, fr, 3), f1 = __shfl_sync(kFull, fr, 4);
-              const double f2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
+              const double g0 = __shfl_sync(kFull, fr, 3), g1 = __shfl_sync(kFull, fr, 4);
+              const double g2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
               const uint64_t ka = (uint64_t)__double_as_longlong(__shfl_sync(kFull, fr, 7));
               // OnlineUpdate (A8): NLMS on the squared residual
               const double E = fr_c - fa;
               const double res = E - fE;
-              const double f3 = 1.0;
-              double s = f0 * f0;
-              s = s + f1 * f1;
-              s = s + f2 * f2;
-              s = s + f3 * f3;
+              const double g3 = 1.0;
+              double s = g0 * g0;
+              s = s + g1 * g1;
+              s = s + g2 * g2;
+              s = s + g3 * g3;
               const double gstep = (pol.mu * res) / (1.0 + s);
-              th0 = th0 + gstep * f0;
-              th1 = th1 + gstep * f1;
-              th2 = th2 + gstep * f2;
-              th3 = th3 + gstep * f3;
+              th0 = th0 + gstep * g0;
+              th1 = th1 + gstep * g1;
+              th2 = th2 + gstep * g2;
+              th3 = th3 + gstep * g3;
               // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
               uint64_t kap = k - ka;
               double pw = 1.0, bb = rho;
@@ -1241,11 +1080,84 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           break;
         }
       }
-      KVR_ACC(1, tp);
+      KVR_ACC(1, tl);
 
-      // ---- 2. longest cached prefix over the input (ballot of 32 probes) ----
-      // With a pending deferred apply, membership = path of that query (same
-      // position, same identity) or old table minus that update's victims.
+      // 2. longest cached prefix over the input (ballot of 32 probes)
+      uint32_t mm = 0;
+#pragma unroll 1
+      for (uint32_t base = 0; base < nq_in; base += 32) {
+        const uint32_t d = base + lane;
+        bool hit = false, check = false;
+        uint32_t sidx = 0;
+        if (d < nq_in) {
+          const uint64_t hh = Hq[d];
+          if (d < np && Hp[d] == hh) {
+            hit = true;
+          } else {
+            const Idx s = tbl_find<Idx>(S, tmask, hh);
+            hit = s != NIL;
+            check = minus_victims && hit;
+            sidx = (uint32_t)s;
+          }
+        }
+        if (minus_victims) {   // found in the old table but evicted by the pending update?
+          const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
+          if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
+        }
+        const uint32_t bal = __ballot_sync(kFull, hit);
+        if (bal == kFull) {
+          mm = base + 32;
+          continue;
+        }
+        mm = base + (__ffs(~bal) - 1);
+        break;
+      }
+      if (mm > nq_in) mm = nq_in;
+      KVR_ACC(2, tl);
+
+      // 3. score (Eq. 4-5, A9)
+      const double x = (double)(bt * mm), y = (double)(qtok - bt * mm);
+      double sc = 0.0, Ch = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0;
+      if (lbgr) {
+        Ch = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
+        h0 = divtab[mm];            // == x / 1000.0 (x = bt*m)
+        h1 = divtab[nq_in - mm];    // == y / 1000.0 (y = bt*(n_in-m))
+        h2 = Pt / 1000.0;
+        const double h3 = 1.0;
+        double dd = th0 * h0;
+        dd = dd + th1 * h1;
+        dd = dd + th2 * h2;
+        dd = dd + th3 * h3;
+        sc = (Ch + Pt) + dd;
+      } else if (router == KVR_ROUTE_STATIC_LINEAR) {
+        sc = (pol.w_load * (double)fn) - (pol.w_hit * (x / (double)qtok));
+      }
+      KVR_ACC(3, tl);
+      m_o = mm;
+      score_o = sc;
+      Chat_o = Ch;
+      f0_o = h0;
+      f1_o = h1;
+      f2_o = h2;
+    };
+#pragma unroll 1
+    for (uint32_t j = 0; j < Nrun; ++j) {
+      const uint64_t g = gq + j;
+      const uint32_t buf = (uint32_t)(g % kNumStages);
+      const uint32_t par = j & 1;
+      KVR_T0(tp);
+      mbar_wait(&ctrl->mbar[buf], (uint32_t)((g / kNumStages) & 1));
+      KVR_ACC(0, tp);
+      consumed = j + 1;
+      const uint8_t* st = stage + (size_t)buf * p.stage_bytes;
+      const QueryHdr hd = *reinterpret_cast<const QueryHdr*>(st);
+      const uint64_t* H = reinterpret_cast<const uint64_t*>(st + 32) + (hd.block_off & 1);
+      const double a = hd.arrival_ms;
+      const uint32_t n_in = hd.n_in, n = hd.n_in + hd.n_out;
+      const uint32_t q = bt * n_in;
+
+      // with a pending deferred apply, membership = path of that query or the old
+      // table minus that update's victims
       const bool overlay = defer && ws->active;
       const uint64_t* Hp = nullptr;
       uint32_t np = 0;
@@ -1255,63 +1167,16 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
              (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
         np = ws->n;
       }
-      uint32_t m = 0;
-#pragma unroll 1
-      for (uint32_t base = 0; base < n_in; base += 32) {
-        const uint32_t d = base + lane;
-        bool hit = false, check = false;
-        uint32_t sidx = 0;
-        if (d < n_in) {
-          const uint64_t hh = H[d];
-          if (overlay && d < np && Hp[d] == hh) {
-            hit = true;
-          } else {
-            const Idx s = tbl_find<Idx>(S, tmask, hh);
-            hit = s != NIL;
-            check = overlay && hit;
-            sidx = (uint32_t)s;
-          }
-        }
-        if (overlay) {   // found in the old table but evicted by the pending update?
-          const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
-          if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
-        }
-        const uint32_t bal = __ballot_sync(kFull, hit);
-        if (bal == kFull) {
-          m = base + 32;
-          continue;
-        }
-        m = base + (__ffs(~bal) - 1);
-        break;
-      }
-      if (m > n_in) m = n_in;
-      if (lane == 0) ws->c_probes += min(m + 1, n_in);
-      KVR_ACC(2, tp);
-
-      // ---- 3. score (Eq. 4-5, A9) ----
-      const double x = (double)(bt * m), y = (double)(q - bt * m);
-      double score = 0.0, Chat = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
-      if (lbgr) {
-        Chat = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
-        f0 = divtab[m];            // == x / 1000.0 (x = bt*m)
-        f1 = divtab[n_in - m];     // == y / 1000.0 (y = bt*(n_in-m))
-        f2 = Pt / 1000.0;
-        const double f3 = 1.0;
-        double dd = th0 * f0;
-        dd = dd + th1 * f1;
-        dd = dd + th2 * f2;
-        dd = dd + th3 * f3;
-        score = (Chat + Pt) + dd;
-      } else if (router == KVR_ROUTE_STATIC_LINEAR) {
-        score = (pol.w_load * (double)fn) - (pol.w_hit * (x / (double)q));
-      }
-      const uint32_t par = j & 1;
+      uint32_t m;
+      double score, Chat, f0, f1, f2;
+      score_query(H, a, n_in, q, Hp, np, overlay, m, score, Chat, f0, f1, f2);
       if (lane == 0) {
         ctrl->score[par][w] = score;
         ctrl->mhit[par][w] = m;
         ctrl->npend[par][w] = fn;
+        ws->c_probes += min(m + 1, n_in);
       }
-      KVR_ACC(3, tp);
+      KVR_RESET(tp);
       __syncthreads();
       KVR_ACC(4, tp);
       if (ctrl->abortf[par]) break;   // set by i* of query j-1 (written to the other parity)
@@ -1457,55 +1322,14 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       KVR_ACC(19, tk);
       KVR_ACC(7, tp);
 
-      // ---- misses: decisions (victims and slots) ----
       const uint32_t M = n - kf;
       const uint32_t size0 = wr.size;
       const uint32_t nfree = min(M, B - size0);
       const uint32_t nev = M - nfree;
-      if (rlt) {
-        uint32_t pslot = (uint32_t)p0;
-        if (regbits) {
-          if (M) rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, wr, M, p0, fallback, K, w, rbuf, ri, lane, vbits,
-                                                      use_list);
-        } else {
-          MemBits mb;
-          mb.leaf = S.leaf;
-          mb.mark = S.mark;
-          mb.nw = nwords;
-#pragma unroll 1
-          for (uint32_t cb = 0; cb < M; cb += 32)
-            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, min(32u, M - cb), cb, p0, pslot, fallback,
-                                    use_list, K, w, rbuf, ri, lane, slots, vbits);
-        }
-      } else {
-        // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
-        if (nev) {
-          KVR_T0(tt);
-          const uint32_t h0 = wr.lhead;
-          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
-          KVR_ACC(11, tt);
-          KVR_CNT(12, wr.lhead - h0);
-        }
-#pragma unroll 1
-        for (uint32_t qq = lane; qq < M; qq += 32) {
-          uint32_t sv;
-          if (qq < nfree) {
-            sv = size0 + qq;
-          } else {
-            const uint32_t v = victims[qq - nfree];
-            sv = v | 0x80000000u;
-            if (defer) atomicOr(&vmap[v >> 5], 1u << (v & 31));   // overlay bitmap
-          }
-          slots[qq] = sv;
-        }
-        wr.size = size0 + nfree;
-        wr.c_evict += nev;
-      }
-      wr.c_ins += M;
-      __syncwarp();
-      KVR_ACC(8, tp);
 
       // ---- accounting: Eq. 1 truth, Eq. 2, FIFO single server (A12, A20) ----
+      // (needs only the hits; done before the decisions so that the next query's
+      // catch-up can run ahead of them)
       const uint32_t h = bt * m;
       const double hx = (double)h, hy = (double)(q - h);
       const double pre = (p.truth.alpha_cached_ms * hx) + (p.truth.alpha_miss_ms * hy);
@@ -1541,6 +1365,67 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ++fn;
       }
       if (lbgr) Pt = Pt + Chat;   // Eq. 6
+      // trial sums in query order, victim-log offsets (prefix sums of n_victims)
+      uint64_t vc = 0;
+      if (lane == 0) {
+        ctrl->sum_lat = ctrl->sum_lat + lat;
+        ctrl->sum_ttft = ctrl->sum_ttft + ttft;
+        if (lat > ctrl->max_lat) ctrl->max_lat = lat;
+        if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
+        if (fn > ws->c_maxp) ws->c_maxp = fn;   // before any catch-up for j+1
+        vc = ctrl->vcursor;
+        ctrl->vcursor = vc + nev;
+        if (vlog && vc + nev > p.victims_per_trial)
+          atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
+      }
+      KVR_ACC(9, tp);
+
+      // ---- misses: decisions (victims and slots) ----
+      if (rlt) {
+        uint32_t pslot = (uint32_t)p0;
+        if (regbits) {
+          if (M) rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, wr, M, p0, fallback, K, w, rbuf, ri, lane,
+                                                      vbits, use_list);
+        } else {
+          MemBits mb;
+          mb.leaf = S.leaf;
+          mb.mark = S.mark;
+          mb.nw = nwords;
+#pragma unroll 1
+          for (uint32_t cb = 0; cb < M; cb += 32)
+            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, min(32u, M - cb), cb, p0, pslot, fallback,
+                                    use_list, K, w, rbuf, ri, lane, slots, vbits);
+        }
+      } else {
+        // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
+        if (nev) {
+          KVR_T0(tt);
+#ifdef KVR_PHASE_PROFILE
+          const uint32_t h0 = wr.lhead;
+#endif
+          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
+          KVR_ACC(11, tt);
+          KVR_CNT(12, wr.lhead - h0);
+        }
+#pragma unroll 1
+        for (uint32_t qq = lane; qq < M; qq += 32) {
+          uint32_t sv;
+          if (qq < nfree) {
+            sv = size0 + qq;
+          } else {
+            const uint32_t v = victims[qq - nfree];
+            sv = v | 0x80000000u;
+            if (defer) atomicOr(&vmap[v >> 5], 1u << (v & 31));   // overlay bitmap
+          }
+          slots[qq] = sv;
+        }
+        wr.size = size0 + nfree;
+        wr.c_evict += nev;
+      }
+      wr.c_ins += M;
+      __syncwarp();
+      KVR_ACC(8, tp);
+
       if (!rlt && defer && nev) {   // LRU overlay bitmap -> registers
         vbits = vmap[lane];
         vmap[lane] = 0u;
@@ -1548,9 +1433,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (lane == 0) {
         ws->j = j; ws->buf = buf; ws->n = n; ws->kf = kf; ws->M = M; ws->m = m; ws->nev = nev;
         ws->h = h; ws->ltail0 = ltail0; ws->wq = wr.wq; ws->p0 = (uint32_t)p0;
-        ws->ttft = ttft; ws->lat = lat; ws->score = score;
+        ws->ttft = ttft; ws->lat = lat; ws->score = score; ws->vc = vc;
         ws->c_hit += h; ws->c_in += q; ws->c_q += 1;
-        if (fn > ws->c_maxp) ws->c_maxp = fn;
         ws->active = 1;
       }
       if (use_list) wr.ltail = ltail0 + n;
@@ -1559,11 +1443,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
-      KVR_ACC(9, tp);
     }
 
     // ---- end of trial ----
-    __syncthreads();   // the previous query's deferred apply (ordered sums/digest) comes first
+    __syncthreads();   // all warps are past their last query before the final applies
     if (ws->active) {
       apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
       vbits = 0;
@@ -1618,6 +1501,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       Rr.status = (int32_t)ctrl->status;
       Rr._pad = 0;
       p.results[trial] = Rr;
+#ifdef KVR_PHASE_PROFILE
+      if (trial < 4096) g_trial_cycles[trial] = clock64() - t_trial0;
+#endif
     }
     if (p.hist)
       for (uint32_t b = tid; b < p.bins; b += blockDim.x)
@@ -1654,6 +1540,8 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
 
 cudaError_t phase_cycles(unsigned long long* out16, int reset) {
 #ifdef KVR_PHASE_PROFILE
+  if (reset == 2)   // per-trial cycles (4096 entries)
+    return cudaMemcpyFromSymbol(out16, g_trial_cycles, 4096 * sizeof(unsigned long long));
   cudaError_t e = cudaMemcpyFromSymbol(out16, g_phase_cycles, 32 * sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
     unsigned long long z[32] = {0};

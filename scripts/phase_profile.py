@@ -11,7 +11,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2601_18999_b200 import build  # noqa: E402
 
-os.environ["KVR_LIB"] = build.build(profile=True)
+_defs = [d for d in os.environ.get("KVR_DEFS", "").split(",") if d]
+os.environ["KVR_LIB"] = (build.build_variant("prof_x", ["KVR_PHASE_PROFILE"] + _defs) if _defs
+                         else build.build(profile=True))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -61,3 +63,11 @@ for label, ev in (("RLT", 1), ("LRU", 0)):
           f"take {buf[11] / q:.0f} cycles/query, {buf[12] / q:.1f} entries scanned/query")
     print(f"  critical-path applies: {int(buf[17])} of {int(q)} queries, {buf[16] / max(int(buf[17]), 1):.0f} cycles each; "
           f"kf {buf[18] / q:.0f}, hits loop {buf[19] / q:.0f} cycles/query")
+    tc = np.zeros(4096, dtype=np.uint64)
+    L.kvr_debug_phase_cycles(tc.ctypes.data, 2)
+    tq = tc[:nt].astype(np.float64) / nq
+    print(f"  per-trial cycles/query: min {tq.min():.0f} median {np.median(tq):.0f} "
+          f"p90 {np.percentile(tq, 90):.0f} max {tq.max():.0f}; wall {ms * 1.965e6 / nq:.0f}")
+    for ti in range(3):
+        sel = tq[t_of == ti]
+        print(f"    trace {ti}: median {np.median(sel):.0f} max {sel.max():.0f}")

@@ -39,7 +39,7 @@ def test_config2_bench_launch_sampled(kvr, oracle_mod):
     assert np.all(out.results["queries"] == bench.N_QUERIES)
     cfg = oracle_mod.OracleConfig(W=bench.W_WORKERS, capacity_blocks=bench.B_BLOCKS,
                                   pending_ring=bench.RING)
-    for t in (0, 4, 1023):      # RLT r=0.3, LRU r=0.5, last trial
+    for t in (0, 400, 700, 1023):      # RLT r=0.3, RLT r=0.9, LRU r=0.5, LRU r=0.9 (last)
         o = oracle_mod.run(cfg, trs[t_of[t]], oracle_mod.OraclePolicy(eviction=int(ev[t])),
                            int(keys[t]))
         assert o.rc == 0
