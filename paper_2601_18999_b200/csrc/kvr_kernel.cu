@@ -566,18 +566,33 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
     // node's parent p is the previous new node, marked, hence outside U)
     if (q > 0 && wr.size == B && !dirty && wr.cntT < B && total > 0 && ri < 32) {
       const uint32_t lim = min(M, min(q + (B - wr.cntT), q + (32u - ri)));
+      uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
 #pragma unroll 1
       for (; q < lim && total > 0; ++q) {
         ++wr.cntT;
-        const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
         ++ri;
         const uint32_t idx = pick32(dlo, dhi, total);
+        // the next draw's broadcast is off the chain (lane 0 when this was the last)
+        dlo = __shfl_sync(kFull, rlo, ri & 31);
+        dhi = __shfl_sync(kFull, rhi, ri & 31);
         const uint32_t owner = __popc(__ballot_sync(kFull, incl <= idx));
+        // speculative, while the bit is selected: lane l fetches for slot owner*32+l
+        // its parent, the parent's child count and the parent's MARK word, so the
+        // chosen bit's values arrive by three independent shuffles
+        uint32_t sp = (uint32_t)S.parent[owner * 32 + lane];
+        const bool sok = sp < B;            // NIL (root child) or padding slot
+        sp = sok ? sp : 0u;
+        const uint32_t snc = (uint32_t)S.nchild[sp];
+        const uint32_t smw = __shfl_sync(kFull, rb.mw, sp >> 5);
         const uint32_t ou = __shfl_sync(kFull, uw, owner);
         const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
         const uint32_t bit = __popc(__ballot_sync(kFull, (uint32_t)__popc(ou & lmle) <= rem));
         const uint32_t v = owner * 32 + bit;
         const uint32_t vb = 1u << bit;
+        const uint32_t pv = __shfl_sync(kFull, sp, bit);
+        const bool hasp = __shfl_sync(kFull, (uint32_t)sok, bit) != 0u;
+        const uint32_t nc = __shfl_sync(kFull, snc, bit) - 1u;
+        const uint32_t pmw = __shfl_sync(kFull, smw, bit);
         if (lane == owner) {
           uw &= ~vb;
           rb.mw |= vb;
@@ -585,15 +600,10 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         }
         if (lane >= owner) --incl;
         --total;
-        const uint32_t pv = (uint32_t)S.parent[v];
-        const bool hasp = pv != (uint32_t)NIL;
-        const uint32_t pvs = hasp ? pv : 0u;
-        const Idx nc = (Idx)(S.nchild[pvs] - 1);
-        __syncwarp();
-        if (hasp) S.nchild[pvs] = nc;   // uniform store
+        if (hasp) S.nchild[pv] = (Idx)nc;   // uniform store (every lane read its value above)
         const bool leafp = hasp && nc == 0;
-        const uint32_t pw = pvs >> 5, pb = 1u << (pvs & 31);
-        const bool add = __ballot_sync(kFull, leafp && lane == pw && !(rb.mw & pb)) != 0u;
+        const uint32_t pw = pv >> 5, pb = 1u << (pv & 31);
+        const bool add = leafp && !(pmw & pb);   // pv != v: the victim's MARK bit is irrelevant
         if (leafp && lane == pw) {
           rb.lw |= pb;
           if (add) uw |= pb;
