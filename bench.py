@@ -202,6 +202,20 @@ def config_json(args):
             "l2": "inputs larger than L2 (3 packed traces ~250 MB) + 256 MB L2 flush between steps"}
 
 
+NCU_CAPTURE = os.path.join(ROOT, "profiles", "r1_bench_replay_ncu.json")
+
+
+def ncu_capture(args):
+    """DRAM traffic per launch of the replay kernel from the committed `ncu --set full`
+    capture of this exact launch (scripts/profile_bench.sh); None for other sizes."""
+    if args.queries != N_QUERIES or args.trials != TRIALS_PER_GPU or not os.path.exists(NCU_CAPTURE):
+        return None
+    with open(NCU_CAPTURE) as f:
+        d = json.load(f)
+    d["src"] = os.path.relpath(NCU_CAPTURE, ROOT) + " (ncu --set full, one launch)"
+    return d
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -287,6 +301,7 @@ def main():
 
     # roofline of the dominant kernel (the replay kernel is the whole step)
     pk = peaks()
+    prof = ncu_capture(args)
     clk_s = clk.summary()
     f_mhz = clk_s["sm_mhz"] or pk["sm_max_mhz"]
     smem_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6 / 1e9        # GB/s at max clock
@@ -302,7 +317,10 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
             "config": config_json(args),
             "roofline": {"bound": "smem", "achieved": achieved_smem, "peak": smem_peak,
-                         "unit": "GB/s", "frac": achieved_smem / smem_peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved_smem / smem_peak,
+                         "traffic": prof.get("traffic_bytes_per_launch") if prof else None,
+                         "traffic_src": prof.get("src") if prof else None,
+                         "smem_actual_frac_ncu": prof.get("smem_actual_frac_of_peak") if prof else None,
                          "peak_src": "148 SM x 128 B/clk x sm_max_mhz (DESIGN.md §6)",
                          "hbm_trace": {"achieved": achieved_hbm, "peak": pk["hbm_gbs"],
                                        "frac": achieved_hbm / pk["hbm_gbs"],

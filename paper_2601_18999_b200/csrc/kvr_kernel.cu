@@ -566,6 +566,8 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
     // node's parent p is the previous new node, marked, hence outside U)
     if (q > 0 && wr.size == B && !dirty && wr.cntT < B && total > 0 && ri < 32) {
       const uint32_t lim = min(M, min(q + (B - wr.cntT), q + (32u - ri)));
+      KVR_T0(tfast);
+      KVR_CNT(26, 0u - q);
       uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
 #pragma unroll 1
       for (; q < lim && total > 0; ++q) {
@@ -575,7 +577,9 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         // the next draw's broadcast is off the chain (lane 0 when this was the last)
         dlo = __shfl_sync(kFull, rlo, ri & 31);
         dhi = __shfl_sync(kFull, rhi, ri & 31);
-        const uint32_t owner = __popc(__ballot_sync(kFull, incl <= idx));
+        // first lane whose inclusive count exceeds idx (incl is nondecreasing over
+        // lanes); CREDUX.MIN is ~2x faster than VOTE+POPC on the chain
+        const uint32_t owner = __reduce_min_sync(kFull, incl > idx ? lane : 32u);
         // speculative, while the bit is selected: lane l fetches for slot owner*32+l
         // its parent, the parent's child count and the parent's MARK word, so the
         // chosen bit's values arrive by three independent shuffles
@@ -586,7 +590,7 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         const uint32_t smw = __shfl_sync(kFull, rb.mw, sp >> 5);
         const uint32_t ou = __shfl_sync(kFull, uw, owner);
         const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
-        const uint32_t bit = __popc(__ballot_sync(kFull, (uint32_t)__popc(ou & lmle) <= rem));
+        const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
         const uint32_t v = owner * 32 + bit;
         const uint32_t vb = 1u << bit;
         const uint32_t pv = __shfl_sync(kFull, sp, bit);
@@ -620,6 +624,8 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         ++wr.c_draws;
         ++wr.c_evict;
       }
+      KVR_ACC(25, tfast);
+      KVR_CNT(26, q);
       if (q >= M) break;
     }
     if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t (t is not cached: not in T)

@@ -63,6 +63,9 @@ for label, ev in (("RLT", 1), ("LRU", 0)):
           f"take {buf[11] / q:.0f} cycles/query, {buf[12] / q:.1f} entries scanned/query")
     print(f"  critical-path applies: {int(buf[17])} of {int(q)} queries, {buf[16] / max(int(buf[17]), 1):.0f} cycles each; "
           f"kf {buf[18] / q:.0f}, hits loop {buf[19] / q:.0f} cycles/query")
+    if buf[25]:
+        print(f"  RLT fast segment: {buf[25] / q:.0f} cycles/query, {int(buf[26]) % (1 << 32)} iterations "
+              f"(mod 2^32), {buf[25] / max(1, int(buf[26]) % (1 << 32)):.0f} cycles/iteration")
     tc = np.zeros(4096, dtype=np.uint64)
     L.kvr_debug_phase_cycles(tc.ctypes.data, 2)
     tq = tc[:nt].astype(np.float64) / nq
