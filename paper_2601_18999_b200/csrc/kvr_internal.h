@@ -105,6 +105,13 @@ struct __align__(16) Ctrl {
 
 inline size_t ctrl_bytes() { return align16(sizeof(Ctrl)); }
 inline size_t stage_bytes(uint32_t max_n) { return align16(sizeof(QueryHdr) + 8 * ((size_t)max_n + 2)); }
+// Per-warp (worker) scalar and sequential state of one trial.
+struct WorkerRegs {
+  uint32_t size, cntT, used, wq, lhead, ltail;
+  uint64_t e;                      // RLT draw counter e_i
+  uint32_t c_ins, c_evict, c_draws, c_resets, c_fb;
+};
+
 // Per-warp shared-memory block: the pending (deferred) apply of this worker's
 // last update, its per-miss slots, Leaf-LRU victims, the overlay victim bitmap
 // staging area, and the worker's trial counters.
@@ -114,6 +121,9 @@ struct __align__(16) WarpSm {
   unsigned long long c_probes, c_hit, c_in;
   uint32_t active, j, buf, n, kf, M, m, nev, h, ltail0, wq, p0;
   uint32_t c_q, c_maxp, _pad[2];
+  WorkerRegs x;                    // RLT decision state in/out, e_i and counters
+  uint32_t x_ri, _pad2[3];         // next unused draw of x_rbuf
+  unsigned long long x_rbuf[32];   // RLT: 32 counter-based draws, one per lane
   uint32_t slot[4];                // [max_n] slots | [max_n] victims | [32] bitmap
 };
 inline size_t scratch_bytes(uint32_t max_n) {

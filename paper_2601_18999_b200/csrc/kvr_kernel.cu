@@ -213,16 +213,23 @@ struct RecencyLog {
 
 // take the first `need` valid entries in [head, tail) as victims -> out[0..need);
 // returns the new head (just past the last victim)
-__device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
-                                          uint32_t need, uint32_t* out, uint32_t lane) {
-  uint32_t k = 0, pos = head;
-  // software pipeline: kLogDepth windows of entries are in flight while one is filtered
-  uint64_t e[kLogDepth];
+// the first kLogDepth windows from `head` (entries are validated against the stamps
+// at take time)
+__device__ __forceinline__ void log_preload(const RecencyLog& R, uint32_t head, uint32_t tail,
+                                            uint32_t lane, uint64_t (&e)[kLogDepth]) {
 #pragma unroll
   for (int i = 0; i < kLogDepth; ++i) {
-    const uint32_t idx = pos + 32u * i + lane;
+    const uint32_t idx = head + 32u * i + lane;
     e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
   }
+}
+
+// e: log_preload(R, head, tail, ...) (the log between head and tail unchanged since)
+__device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
+                                          uint32_t need, uint32_t* out, uint32_t lane,
+                                          uint64_t (&e)[kLogDepth]) {
+  uint32_t k = 0, pos = head;
+  // software pipeline: kLogDepth windows of entries are in flight while one is filtered
 #pragma unroll 1
   for (;;) {
 #pragma unroll
@@ -421,12 +428,6 @@ __device__ __noinline__ uint64_t philox_refill(uint64_t K, uint64_t n, uint32_t 
   return philox_r64(K, n, worker, 1u);
 }
 
-// Per-warp (worker) scalar and sequential state of one trial.
-struct WorkerRegs {
-  uint32_t size, cntT, used, wq, lhead, ltail;
-  uint64_t e;                      // RLT draw counter e_i
-  uint32_t c_ins, c_evict, c_draws, c_resets, c_fb;
-};
 
 // RLT decisions for misses [cb, cb+cnt), generic bitmaps (B > 1024).  Serial.
 template <typename Bits, typename Idx>
@@ -536,10 +537,9 @@ __device__ __forceinline__ uint32_t pick32(uint32_t lo, uint32_t hi, uint32_t t)
 // gains the victim's parent iff that became an unmarked leaf.  Resets and the
 // U = {} fallbacks (A5) recount from lw/mw.
 template <typename Idx, bool kGlobal, int kTag>
-__device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& wr_io,
-                                            uint32_t M, Idx p0, uint32_t fallback, uint64_t K,
-                                            uint32_t worker, uint64_t& rbuf_io, uint32_t& ri_io,
-                                            uint32_t lane, uint32_t& vbits_io, bool use_list) {
+__device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, Idx p0,
+                                            uint32_t fallback, uint64_t K, uint32_t worker,
+                                            uint32_t lane, bool use_list) {
   const Idx NIL = Nil<Idx>::empty;
   const uint32_t B = p_.B, nwords = p_.lay.nwords;
   uint8_t* wb = worker_base<kGlobal>(p_, worker);
@@ -549,10 +549,25 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
                                       p_.aux.off_log);
   R.stamp = reinterpret_cast<uint16_t*>(wb + p_.lay.off_stamp);
   R.cap_mask = p_.aux.log_cap - 1;
-  uint32_t* slots = warp_sm(p_, worker)->slot;
-  WorkerRegs wr = wr_io;
-  uint32_t rlo = (uint32_t)rbuf_io, rhi = (uint32_t)(rbuf_io >> 32);
-  uint32_t ri = ri_io, vbits = vbits_io, p = (uint32_t)p0;
+  // state in and out through the warp's shared-memory block (no by-reference
+  // arguments: they would put the caller's registers in local memory)
+  WarpSm* ws = warp_sm(p_, worker);
+  uint32_t* slots = ws->slot;
+  uint32_t* vmap = ws->slot + 2 * p_.max_n;
+  // registers: size, |T| and e_i only; counters are bumped in shared memory (draws
+  // = the change of e_i, evictions are counted by the caller), the log cursors and
+  // recency stamp are read there on the rare paths that need them
+  struct {
+    uint32_t size, cntT;
+    uint64_t e;
+  } wr;
+  wr.size = ws->x.size;
+  wr.cntT = ws->x.cntT;
+  wr.e = ws->x.e;
+  const uint32_t wq = use_list ? ws->x.wq : 0u;
+  const uint64_t rb_in = ws->x_rbuf[lane];
+  uint32_t rlo = (uint32_t)rb_in, rhi = (uint32_t)(rb_in >> 32);
+  uint32_t ri = ws->x_ri, vbits = 0, p = (uint32_t)p0;
   RegBits rb;
   rb.load(S.leaf, S.mark, nwords, lane);
   const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;   // lanes <= lane
@@ -617,12 +632,10 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
           ++total;
         }
         if (lane == (p >> 5)) rb.lw &= ~(1u << (p & 31));   // previous new node gets a child
-        if (use_list) R.stamp[v] = (uint16_t)wr.wq;
+        if (use_list) R.stamp[v] = (uint16_t)wq;
         slots[q] = v | 0x80000000u;
         p = v;
         ++wr.e;
-        ++wr.c_draws;
-        ++wr.c_evict;
       }
       KVR_ACC(25, tfast);
       KVR_CNT(26, q);
@@ -631,7 +644,7 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
     if (wr.cntT == B) {   // Alg. 1 l.8-9 at the mark of t (t is not cached: not in T)
       rb.mw = 0u;
       wr.cntT = 1;
-      ++wr.c_resets;
+      if (lane == 0) ++ws->x.c_resets;
       dirty = true;
     } else {
       ++wr.cntT;
@@ -651,11 +664,11 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
       }
       bool generic = false;
       if (total == 0) {   // U = {} (A5)
-        ++wr.c_fb;
+        if (lane == 0) ++ws->x.c_fb;
         if (fallback == KVR_RLT_EARLY_RESET) {
           rb.mw = 0u;
           wr.cntT = 1;
-              ++wr.c_resets;
+              if (lane == 0) ++ws->x.c_resets;
           uw = rb.lw;
           if (lane == (p >> 5)) uw &= ~(1u << (p & 31));
           uint32_t c;
@@ -675,7 +688,6 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
         ++ri;
         ++wr.e;
-        ++wr.c_draws;
         const uint32_t idx = pick32(dlo, dhi, total);
         const uint32_t owner = __popc(__ballot_sync(kFull, incl <= idx));
         const uint32_t ou = __shfl_sync(kFull, uw, owner);
@@ -720,14 +732,13 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
           const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
           ++ri;
           ++wr.e;
-          ++wr.c_draws;
           uint32_t c, inc2;
           const uint32_t tot = rb.count(p, false, lane, c, inc2);
           const uint32_t sel = rb.select(p, false, lane, c, inc2, pick32(dlo, dhi, tot));
           v = sel & 0x7fffffffu;
           vmarked = (sel >> 31) != 0;
         } else {   // LRU_MARKED: least recently used leaf != p, no draw
-          v = log_first_valid(R, wr.lhead, wr.ltail, lane);
+          v = log_first_valid(R, ws->x.lhead, ws->x.ltail, lane);
           vmarked = rb.mark_test(v);
         }
         rb.leaf_clr(v, lane);
@@ -746,7 +757,6 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
         rb.mark_set(v, lane);
         dirty = true;
       }
-      ++wr.c_evict;
       slot = v;
       ev = 1;
       if (lane == (v >> 5)) vbits |= 1u << (v & 31);
@@ -762,24 +772,31 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, WorkerRegs& 
     } else {
       rb.leaf_clr(p, lane);
     }
-    if (use_list) R.stamp[slot] = (uint16_t)wr.wq;   // LRU_MARKED fallback reads the log
+    if (use_list) R.stamp[slot] = (uint16_t)wq;   // LRU_MARKED fallback reads the log
     slots[q] = slot | (ev << 31);
     p = slot;
   }
   rb.store(S.leaf, S.mark, nwords, lane);
-  wr_io = wr;
-  rbuf_io = ((uint64_t)rhi << 32) | rlo;
-  ri_io = ri;
-  vbits_io = vbits;
+  __syncwarp();
+  if (lane == 0) {
+    ws->x.c_draws += (uint32_t)(wr.e - ws->x.e);   // one draw per e_i step
+    ws->x.size = wr.size;
+    ws->x.cntT = wr.cntT;
+    ws->x.e = wr.e;
+    ws->x_ri = ri;
+  }
+  ws->x_rbuf[lane] = ((uint64_t)rhi << 32) | rlo;
+  vmap[lane] = vbits;   // victims of this update -> overlay bitmap (read back by the caller)
+  __syncwarp();
 }
 
 // Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
 // victim digest term and the query record (trial sums are added in query order
 // by the accounting step).
 template <typename Idx, bool kGlobal, int kTag>
-__device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr, uint32_t lane,
-                                          uint32_t w, bool rlt, bool use_list, bool lbgr_or_static,
-                                          kvr_query_record* rec, uint64_t* vlog) {
+__device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, uint32_t w, bool rlt,
+                                          bool use_list, bool lbgr_or_static, kvr_query_record* rec,
+                                          uint64_t* vlog) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(kvr_dsmem);
   WarpSm* ws = warp_sm(p, w);
   const uint8_t* stage = kvr_dsmem + stage_off();
@@ -836,10 +853,10 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr,
     prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
     __syncwarp();
   }
-  wr.used += used_add;
-  if (wr.used > (p.lay.T >> 1)) {
-    tbl_rebuild<Idx>(S, p.lay.T, wr.size, lane);
-    wr.used = wr.size;
+  uint32_t used = ws->x.used + used_add;   // live + tombstone table entries
+  if (used > (p.lay.T >> 1)) {
+    tbl_rebuild<Idx>(S, p.lay.T, ws->x.size, lane);
+    used = ws->x.size;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
@@ -865,6 +882,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, WorkerRegs& wr,
       rec[ws->j] = Rq;
     }
     ws->active = 0;
+    ws->x.used = used;
   }
   __syncwarp();
 }
@@ -949,17 +967,22 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     }
     if (use_list)
       for (uint32_t i = lane; i < B; i += 32) R.stamp[i] = 0;
-    WorkerRegs wr;
-    wr.size = 0; wr.cntT = 0; wr.used = 0; wr.wq = 0; wr.lhead = 0; wr.ltail = 0; wr.e = 0;
-    wr.c_ins = 0; wr.c_evict = 0; wr.c_draws = 0; wr.c_resets = 0; wr.c_fb = 0;
+    // The worker's scalar cache state (size, |T|, log cursors, e_i, counters) lives in
+    // its shared-memory block ws->x; the chosen warp works on a register copy for
+    // the duration of its update (nothing of it stays live across the query loop).
+    if (lane == 0) {
+      WorkerRegs w0;
+      w0.size = 0; w0.cntT = 0; w0.used = 0; w0.wq = 0; w0.lhead = 0; w0.ltail = 0; w0.e = 0;
+      w0.c_ins = 0; w0.c_evict = 0; w0.c_draws = 0; w0.c_resets = 0; w0.c_fb = 0;
+      ws->x = w0;
+      ws->x_ri = 32;   // next unused draw of the batch (none yet)
+    }
     uint32_t fh = 0, fn = 0;
     double P = 0.0, F = 0.0, Pt = 0.0;
     double th0 = pol.theta0[0], th1 = pol.theta0[1], th2 = pol.theta0[2], th3 = pol.theta0[3];
     uint64_t k = 0;
     // front record of the pending FIFO: lane f < 8 holds field f; fr_c is uniform
     double fr = 0.0, fr_c = 0.0;
-    uint64_t rbuf = 0;
-    uint32_t ri = 32;       // next unused draw of rbuf
     uint32_t vbits = 0;     // victims of this warp's pending update (lane l: word l)
     if (lane == 0) {
       ws->active = 0;
@@ -1016,6 +1039,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
     uint32_t consumed = 0;
 
+    const double pol_inv_dt = 1.0 / pol.delta_t_ms;
     // ---- steps 1-3 of one query for this warp's worker ----
     // Membership = the table, or the path Hp[0..np) (same position, same identity),
     // minus the pending update's victims (register bitmap vbits) if minus_victims.
@@ -1026,7 +1050,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       KVR_T0(tl);
       // 1. catch-up (A11: tick before completion before routing)
       {
-        const double rho = pol.rho, dt = pol.delta_t_ms;
+        const double rho = pol.rho, dt = pol.delta_t_ms, inv_dt = pol_inv_dt;
 #pragma unroll 1
         for (;;) {
           if (lbgr) {
@@ -1034,7 +1058,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             // is monotone in k', so find the last such k' and apply the multiplications
             // one by one (same rounding sequence as a per-tick loop)
             const double lim = (fn == 0 || aq < fr_c) ? aq : fr_c;
-            const double est = lim / dt;
+            const double est = lim * inv_dt;   // a guess only: the loops below make it exact
             uint64_t kk = est < 1.8e19 ? (uint64_t)est : k;
             if (kk < k) kk = k;
             while ((double)(kk + 1) * dt <= lim) ++kk;
@@ -1217,18 +1241,17 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       // ---- 4. argmin over workers (every warp computes the same i*) ----
       uint32_t best = 0;
       if (router == KVR_ROUTE_LBGR || router == KVR_ROUTE_STATIC_LINEAR) {
+        // first minimum = lowest lane holding the smallest order-preserving key of
+        // the fp64 score (-0 folded into +0, which the fp compare treats as equal);
+        // three uniform-datapath reductions instead of a 5-round shuffle tournament
         double v = lane < W ? ctrl->score[par][lane] : INFINITY;
-        uint32_t bi = lane;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const double v2 = __shfl_xor_sync(kFull, v, o);
-          const uint32_t b2 = __shfl_xor_sync(kFull, bi, o);
-          if (v2 < v || (v2 == v && b2 < bi)) {
-            v = v2;
-            bi = b2;
-          }
-        }
-        best = bi;
+        if (v == 0.0) v = 0.0;
+        const uint64_t bits = (uint64_t)__double_as_longlong(v);
+        const uint64_t key = (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+        const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
+        const uint32_t mhi = __reduce_min_sync(kFull, khi);
+        const uint32_t mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xffffffffu);
+        best = __reduce_min_sync(kFull, (khi == mhi && klo == mlo) ? lane : 32u);
       } else if (router == KVR_ROUTE_THRESHOLD) {   // A16
         const uint32_t npd = lane < W ? ctrl->npend[par][lane] : 0xffffffffu;
         const uint32_t mh = lane < W ? ctrl->mhit[par][lane] : 0u;
@@ -1249,7 +1272,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
       // deferred apply of this warp's previous update (overlaps others' decisions)
       if (ws->active) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
 #ifdef KVR_PHASE_PROFILE
@@ -1263,6 +1286,17 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (w != best) continue;
 
       // ================= warp i* : UpdateCache decisions + accounting =================
+      __syncwarp();
+      // register copy of the scalars this update changes (written back at the end);
+      // counters and e_i are bumped in shared memory
+      struct {
+        uint32_t size, cntT, wq, lhead, ltail;
+      } wr;
+      wr.size = ws->x.size;
+      wr.cntT = ws->x.cntT;
+      wr.wq = ws->x.wq;
+      wr.lhead = ws->x.lhead;
+      wr.ltail = ws->x.ltail;
       if (fn >= p.ring) {   // pending FIFO full -> trial status, stop (before Eq. 3)
         if (lane == 0) {
           ctrl->status = KVR_TRIAL_RING_OVERFLOW;
@@ -1326,7 +1360,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             __syncwarp();
             if (act && lane >= rr) atomicOr(&S.mark[(uint32_t)s >> 5], 1u << ((uint32_t)s & 31));
             wr.cntT = nact - rr;
-            ++wr.c_resets;
+            if (lane == 0) ++ws->x.c_resets;
           } else {
             if (um) atomicOr(&S.mark[(uint32_t)s >> 5], 1u << ((uint32_t)s & 31));
             wr.cntT += __popc(u);
@@ -1357,6 +1391,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       const double lat = comp - a;
       F = comp;
       P = P + cost;
+      KVR_T0(ta);
       {
         const uint32_t slotf = (fh + fn >= p.ring) ? fh + fn - p.ring : fh + fn;
         const double rE = lbgr ? score : 0.0, r0 = lbgr ? f0 : 0.0, r1 = lbgr ? f1 : 0.0,
@@ -1381,6 +1416,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ++fn;
       }
       if (lbgr) Pt = Pt + Chat;   // Eq. 6
+      KVR_ACC(27, ta);
       // trial sums in query order, victim-log offsets (prefix sums of n_victims)
       uint64_t vc = 0;
       if (lane == 0) {
@@ -1394,23 +1430,54 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         if (vlog && vc + nev > p.victims_per_trial)
           atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_VICTIM_LOG_FULL);
       }
+      KVR_ACC(28, ta);
       KVR_ACC(9, tp);
 
       // ---- misses: decisions (victims and slots) ----
       if (rlt) {
         uint32_t pslot = (uint32_t)p0;
         if (regbits) {
-          if (M) rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, wr, M, p0, fallback, K, w, rbuf, ri, lane,
-                                                      vbits, use_list);
+          if (M) {
+            __syncwarp();
+            if (lane == 0) {
+              ws->x.size = wr.size;
+              ws->x.cntT = wr.cntT;
+              ws->x.wq = wr.wq;
+              ws->x.lhead = wr.lhead;
+              ws->x.ltail = wr.ltail;
+            }
+            __syncwarp();
+            rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, M, p0, fallback, K, w, lane, use_list);
+            wr.size = ws->x.size;
+            wr.cntT = ws->x.cntT;
+            if (lane == 0) ws->x.c_evict += nev;
+          }
         } else {
           MemBits mb;
           mb.leaf = S.leaf;
           mb.mark = S.mark;
           mb.nw = nwords;
+          __syncwarp();
+          WorkerRegs xw = ws->x;
+          xw.size = wr.size;
+          xw.cntT = wr.cntT;
+          xw.wq = wr.wq;
+          xw.lhead = wr.lhead;
+          xw.ltail = wr.ltail;
+          uint64_t rbuf = ws->x_rbuf[lane];
+          uint32_t ri = ws->x_ri;
 #pragma unroll 1
           for (uint32_t cb = 0; cb < M; cb += 32)
-            rlt_chunk<MemBits, Idx>(mb, S, R, wr, B, min(32u, M - cb), cb, p0, pslot, fallback,
+            rlt_chunk<MemBits, Idx>(mb, S, R, xw, B, min(32u, M - cb), cb, p0, pslot, fallback,
                                     use_list, K, w, rbuf, ri, lane, slots, vbits);
+          __syncwarp();
+          if (lane == 0) {
+            ws->x = xw;
+            ws->x_ri = ri;
+          }
+          ws->x_rbuf[lane] = rbuf;
+          wr.size = xw.size;
+          wr.cntT = xw.cntT;
         }
       } else {
         // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
@@ -1419,7 +1486,11 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 #ifdef KVR_PHASE_PROFILE
           const uint32_t h0 = wr.lhead;
 #endif
-          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane);
+          // (loading the head windows earlier hides their latency but costs the
+          // registers to hold them across the hits and accounting: slower overall)
+          uint64_t lpre[kLogDepth];
+          log_preload(R, wr.lhead, ltail0, lane, lpre);
+          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane, lpre);
           KVR_ACC(11, tt);
           KVR_CNT(12, wr.lhead - h0);
         }
@@ -1436,13 +1507,13 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           slots[qq] = sv;
         }
         wr.size = size0 + nfree;
-        wr.c_evict += nev;
+        if (lane == 0) ws->x.c_evict += nev;
       }
-      wr.c_ins += M;
+      if (lane == 0) ws->x.c_ins += M;
       __syncwarp();
       KVR_ACC(8, tp);
 
-      if (!rlt && defer && nev) {   // LRU overlay bitmap -> registers
+      if (defer) {   // overlay bitmap of this update's victims -> registers
         vbits = vmap[lane];
         vmap[lane] = 0u;
       }
@@ -1455,8 +1526,16 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       if (use_list) wr.ltail = ltail0 + n;
       __syncwarp();
+      if (lane == 0) {
+        ws->x.size = wr.size;
+        ws->x.cntT = wr.cntT;
+        ws->x.wq = wr.wq;
+        ws->x.lhead = wr.lhead;
+        ws->x.ltail = wr.ltail;
+      }
+      __syncwarp();
       if (!defer) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
     }
@@ -1464,7 +1543,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // ---- end of trial ----
     __syncthreads();   // all warps are past their last query before the final applies
     if (ws->active) {
-      apply_update<Idx, kGlobal, kMaxThreads>(p, wr, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+      apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
       vbits = 0;
     }
     __syncthreads();
@@ -1476,11 +1555,11 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     gq += issued;
     if (lane == 0) {
       atomicAdd(&ctrl->cnt[0], ws->c_probes);
-      atomicAdd(&ctrl->cnt[1], (unsigned long long)wr.c_ins);
-      atomicAdd(&ctrl->cnt[2], (unsigned long long)wr.c_evict);
-      atomicAdd(&ctrl->cnt[3], (unsigned long long)wr.c_draws);
-      atomicAdd(&ctrl->cnt[4], (unsigned long long)wr.c_resets);
-      atomicAdd(&ctrl->cnt[5], (unsigned long long)wr.c_fb);
+      atomicAdd(&ctrl->cnt[1], (unsigned long long)ws->x.c_ins);
+      atomicAdd(&ctrl->cnt[2], (unsigned long long)ws->x.c_evict);
+      atomicAdd(&ctrl->cnt[3], (unsigned long long)ws->x.c_draws);
+      atomicAdd(&ctrl->cnt[4], (unsigned long long)ws->x.c_resets);
+      atomicAdd(&ctrl->cnt[5], (unsigned long long)ws->x.c_fb);
       atomicAdd(&ctrl->cnt[6], ws->c_hit);
       atomicAdd(&ctrl->cnt[7], ws->c_in);
       atomicAdd(&ctrl->cnt[8], (unsigned long long)ws->c_q);

@@ -33,7 +33,17 @@ __global__ void k(uint32_t* out, unsigned long long* cyc, uint32_t seed) {
   MEAS(x = (__ffs(~__ballot_sync(0xffffffffu, x & 1u))) + x) // 11 VOTE+BREV/FLO
   MEAS(x = __reduce_min_sync(0xffffffffu, x) + 1u)          // 12 REDUX.MIN + IADD
   MEAS(x = (x >> 3) ^ x)                                    // 13 SHF + LOP3
-  out[lane] = x;
+  double d = 1.0 + lane * 1e-3;
+  MEAS(d = d + 1e-9)                                        // 14 DADD
+  MEAS(d = d * 1.0000001)                                   // 15 DMUL
+  MEAS(d = __fma_rn(d, 1.0000001, 1e-9))                    // 16 DFMA
+  MEAS(d = d / 1.0000001)                                   // 17 DDIV (IEEE)
+  MEAS(d = (double)(uint32_t)(d) + 1.5)                     // 18 F2I + I2F + DADD
+  MEAS(d = d < 2.0 ? d * 1.0000001 : d * 0.9999999)         // 19 DSETP + DMUL
+  MEAS(d = (double)__double_as_longlong(d) * 1e-300)        // 20 I2F.F64 + DMUL
+  float f = 1.0f + lane;
+  MEAS(f = f * 1.0001f + 1e-7f)                             // 21 FFMA
+  out[lane] = x + (uint32_t)d + (uint32_t)f;
 }
 
 int main() {
@@ -46,7 +56,9 @@ int main() {
   cudaDeviceSynchronize();
   const char* names[] = {"POPC+IADD", "IMAD", "IMAD.HI+IADD", "CLZ(FLO)+IADD", "BREV+IADD",
                          "VOTE+IADD", "SHFL.IDX+IADD", "LDS+IADD", "FNS+IADD", "REDUX.SUM+IADD",
-                         "VOTE+POPC+IADD", "VOTE+FFS+IADD", "REDUX.MIN+IADD", "SHF+LOP3"};
-  for (int i = 0; i < 14; ++i) printf("%-16s %6.1f cycles/iter\n", names[i], (double)c[i] / N);
+                         "VOTE+POPC+IADD", "VOTE+FFS+IADD", "REDUX.MIN+IADD", "SHF+LOP3",
+                         "DADD", "DMUL", "DFMA", "DDIV", "F2I+I2F+DADD", "DSETP+DMUL", "I2F64+DMUL",
+                         "FFMA"};
+  for (int i = 0; i < 22; ++i) printf("%-16s %6.1f cycles/iter\n", names[i], (double)c[i] / N);
   return 0;
 }
