@@ -127,13 +127,20 @@ __device__ __forceinline__ Idx tbl_find(const WorkerView<Idx>& S, uint32_t mask,
   }
 }
 
-// tombstone the entry of `slot` (identity h); lanes may run this concurrently
+// remove the entry of `slot` (identity h); lanes may run this concurrently.  The
+// entry becomes EMPTY when the next one is EMPTY (no probe path can run through
+// it: linear-probing clusters are contiguous), else a tombstone.  A lane that reads
+// its neighbour before a concurrent erase of it lands just writes a tombstone.
+// Returns 1 when no tombstone was left.
 template <typename Idx>
-__device__ __forceinline__ void tbl_erase(const WorkerView<Idx>& S, uint32_t mask, uint64_t h, Idx slot) {
+__device__ __forceinline__ uint32_t tbl_erase(const WorkerView<Idx>& S, uint32_t mask, uint64_t h,
+                                              Idx slot) {
   uint32_t pos = (uint32_t)h & mask;
 #pragma unroll 1
   while (S.table[pos] != slot) pos = (pos + 1) & mask;
-  S.table[pos] = Nil<Idx>::tomb;
+  const bool clear = S.table[(pos + 1) & mask] == Nil<Idx>::empty;
+  S.table[pos] = clear ? Nil<Idx>::empty : Nil<Idx>::tomb;
+  return clear ? 1u : 0u;
 }
 
 // claim position pos if it is EMPTY or TOMB (CAS); returns 1 if it was EMPTY
@@ -814,7 +821,8 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   const uint32_t nfree = M - nev;
   const uint64_t vc = ws->vc;
   uint64_t V = 0;
-  uint32_t used_add = 0, prev_last = ws->p0;
+  uint32_t used_add = 0, used_sub = 0, prev_last = ws->p0;
+  KVR_T0(t_ap);
 #pragma unroll 1
   for (uint32_t cb = 0; cb < M; cb += 32) {
     const uint32_t cnt = min(32u, M - cb);
@@ -824,15 +832,17 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     const uint32_t my_slot = sv & 0x7fffffffu;
     const bool my_ev = (sv >> 31) != 0;
     const uint64_t t = act ? H[kf + qq] : 0ull;
+    uint32_t cleared = 0;
     if (act && my_ev) {
       const uint64_t vkey = S.key[my_slot];
-      tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
+      cleared = tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
       V ^= fmix64(vkey ^ ((uint64_t)(qq - nfree + 1) * kPosMul));
       if (vlog) {
         const uint64_t vi = vc + (qq - nfree);
         if (vi < p.victims_per_trial) vlog[vi] = vkey;
       }
     }
+    KVR_ACC(29, t_ap);   // erase (victims) incl. slot/identity loads
     const uint32_t up = __shfl_up_sync(kFull, my_slot, 1);
     const uint32_t par_slot = lane == 0 ? prev_last : up;
     __syncwarp();
@@ -848,16 +858,20 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
       }
     }
     __syncwarp();
+    KVR_ACC(30, t_ap);   // slot arrays, stamps, log entries
     const uint32_t claimed = act ? tbl_insert<Idx>(S, tmask, t, (Idx)my_slot) : 0u;
     used_add += __popc(__ballot_sync(kFull, claimed != 0));
+    used_sub += __popc(__ballot_sync(kFull, cleared != 0));
     prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
     __syncwarp();
+    KVR_ACC(31, t_ap);   // table inserts
   }
-  uint32_t used = ws->x.used + used_add;   // live + tombstone table entries
+  uint32_t used = ws->x.used + used_add - used_sub;   // live + tombstone table entries
   if (used > (p.lay.T >> 1)) {
     tbl_rebuild<Idx>(S, p.lay.T, ws->x.size, lane);
     used = ws->x.size;
   }
+  KVR_ACC(24, t_ap);   // rebuilds
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
   if (lane == 0) {
@@ -885,6 +899,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     ws->x.used = used;
   }
   __syncwarp();
+  KVR_ACC(23, t_ap);   // digest term, record
 }
 
 // occupancy targets (shared memory allows ~4 CTAs/SM at W<=4 and 2 at W<=8):

@@ -67,6 +67,8 @@ for label, ev in (("RLT", 1), ("LRU", 0)):
         print(f"  RLT fast segment: {buf[25] / q:.0f} cycles/query, {int(buf[26]) % (1 << 32)} iterations "
               f"(mod 2^32), {buf[25] / max(1, int(buf[26]) % (1 << 32)):.0f} cycles/iteration")
     print(f"  accounting split: fifo push + Pt {buf[27] / q:.0f}, trial sums (lane 0) {buf[28] / q:.0f} cycles/query")
+    print(f"  apply split (per query): erase {buf[29] / q:.0f}, arrays/log {buf[30] / q:.0f}, "
+          f"inserts {buf[31] / q:.0f}, rebuilds {buf[24] / q:.0f}, digest/record {buf[23] / q:.0f}")
     tc = np.zeros(4096, dtype=np.uint64)
     L.kvr_debug_phase_cycles(tc.ctypes.data, 2)
     tq = tc[:nt].astype(np.float64) / nq
