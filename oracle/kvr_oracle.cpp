@@ -349,9 +349,11 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   if (validate_trace(tr)) return 1;
   const uint32_t W = cfg->W, B = cfg->capacity_blocks;
   if (W < 1 || W > 32 || B < 1 || B > 65536) return 1;
-  if (pol->eviction > KVRO_EVICT_RLT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
+  if (pol->eviction > KVRO_EVICT_OPT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
       pol->router > KVRO_ROUTE_RANDOM)
     return 1;
+  // Belady OPT is defined for one cache: the offline analysis runs it at W = 1
+  if (pol->eviction == KVRO_EVICT_OPT && W != 1) return 1;
   if (!(pol->rho > 0.0 && pol->rho <= 1.0) || !(pol->delta_t_ms > 0.0)) return 1;
   for (uint32_t j = 0; j < tr->n_queries; ++j)       // P:197 with beta = 1
     if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
@@ -359,6 +361,15 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   std::memset(out, 0, sizeof(*out));
   if (hist) std::memset(hist, 0, sizeof(uint32_t) * cfg->latency_hist_bins);
   const std::vector<uint64_t> H = chain_all(tr);
+  // OPT: identity -> ascending query indices containing it, and its path depth
+  std::unordered_map<uint64_t, std::vector<uint64_t>> occ;
+  std::unordered_map<uint64_t, uint32_t> depth_of;
+  if (pol->eviction == KVRO_EVICT_OPT)
+    for (uint32_t j = 0; j < tr->n_queries; ++j)
+      for (uint64_t o = tr->block_offsets[j]; o < tr->block_offsets[j + 1]; ++o) {
+        occ[H[o]].push_back(j);
+        depth_of[H[o]] = (uint32_t)(o - tr->block_offsets[j]) + 1;
+      }
   std::vector<Worker> w(W);
   for (auto& x : w) {
     x.cache.B = B;
@@ -497,6 +508,13 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
       uint64_t r = philox_r64(K, xs.e, best, 1);
       xs.e++;
       return pick(r, nU);
+    };
+    const uint64_t jj = j;
+    ux.next_use = [&](uint64_t id) -> std::pair<uint64_t, uint32_t> {   // OPT only
+      const std::vector<uint64_t>& v = occ[id];
+      auto it = std::upper_bound(v.begin(), v.end(), jj);
+      if (it == v.end()) return {UINT64_MAX, 0};
+      return {*it, depth_of[id]};
     };
     update_cache(xs.cache, Hj, n_in + n_out, ux);
     if (ux.invariant_violation) return 9;

@@ -36,7 +36,7 @@ extern "C" {
 #endif
 
 /* eviction / fallback / router codes (SURVEY §8b enums, duplicated) */
-enum { KVRO_EVICT_LRU = 0, KVRO_EVICT_RLT = 1, KVRO_EVICT_OPT = 2 /* analysis only, W=1 */ };
+enum { KVRO_EVICT_LRU = 0, KVRO_EVICT_RLT = 1, KVRO_EVICT_OPT = 2 /* Belady; W = 1 only */ };
 enum { KVRO_RLT_EARLY_RESET = 0, KVRO_RLT_UNIFORM_LEAF = 1, KVRO_RLT_LRU_MARKED = 2 };
 enum { KVRO_ROUTE_LBGR = 0, KVRO_ROUTE_STATIC_LINEAR = 1, KVRO_ROUTE_THRESHOLD = 2,
        KVRO_ROUTE_ROUND_ROBIN = 3, KVRO_ROUTE_RANDOM = 4 };

@@ -180,6 +180,34 @@ def test_p10_belady_equals_brute_force(oracle_mod):
     assert checked > 100
 
 
+def test_p10b_full_replay_opt_w1(oracle_mod):
+    """The full replay with Belady OPT at W = 1 (the offline analysis the GPU runs,
+    SURVEY §8f #1): misses equal the exhaustive minimum on tiny traces,
+    the single-cache Belady replay on larger ones; W > 1 is refused (P:170 defines
+    OPT for one cache)."""
+    checked = 0
+    for seed in range(120):
+        tr = wl.random_tree(7, seed, max_len=3, alphabet=3, max_out=0)
+        if tr.total_blocks > 22:
+            continue
+        for B in (3, 4, 5):
+            if tr.max_blocks > B:
+                continue
+            cfg = oracle_mod.OracleConfig(W=1, capacity_blocks=B)
+            r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=oracle_mod.EVICT_OPT), 7)
+            assert r.rc == 0
+            assert int(r.result["inserted_blocks"]) == oracle_mod.bruteforce_min_misses(tr, B), (seed, B)
+            checked += 1
+    assert checked > 80
+    tr = wl.adv(32, 4, 4, seed=3)
+    cfg = oracle_mod.OracleConfig(W=1, capacity_blocks=32)
+    r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=oracle_mod.EVICT_OPT), 1)
+    opt, _ = oracle_mod.single_replay(tr, 32, oracle_mod.EVICT_OPT)
+    assert r.rc == 0 and int(r.result["inserted_blocks"]) == opt
+    cfg2 = oracle_mod.OracleConfig(W=2, capacity_blocks=32)
+    assert oracle_mod.run(cfg2, tr, oracle_mod.OraclePolicy(eviction=oracle_mod.EVICT_OPT), 1).rc == 1
+
+
 # -------------------------------------------------------------------------- P11
 @pytest.mark.parametrize("fallback", [0, 1])
 def test_p11_rlt_competitive_gate(oracle_mod, fallback):
