@@ -102,8 +102,28 @@ kvr_status kvr_trace_info(const kvr_trace* tr, uint32_t* n_queries, uint32_t* ma
 kvr_status kvr_trace_chained_hashes(const kvr_trace* tr, const uint64_t** d_hashes);
 kvr_status kvr_trace_destroy(kvr_trace* tr);
 
+/* Next-use index for the offline Belady OPT analysis (KVR_EVICT_OPT; P:170,
+ * SURVEY §8f #1): nu[o] = index of the next query after the one holding block
+ * occurrence o (CSR order) whose path contains the same identity, 0xFFFFFFFF if
+ * none.  Built on the device (stable radix sort of (identity, occurrence) pairs,
+ * then one pass); asynchronous on `stream`.  d_nu: DEVICE [n_blocks_total] u32,
+ * caller-owned; d_scratch: DEVICE, caller-owned, only used during the call.
+ * Returns a NEW handle that borrows tr's packed buffer and d_nu (both must
+ * outlive it); tr itself is unchanged.  INVALID_ARG for null buffers,
+ * WORKSPACE_TOO_SMALL for short ones, UNSUPPORTED for >= 2^31 blocks. */
+kvr_status kvr_trace_next_use_bytes(const kvr_trace* tr, size_t* nu_bytes, size_t* scratch_bytes);
+kvr_status kvr_trace_build_next_use(const kvr_trace* tr, uint32_t* d_nu, size_t nu_bytes,
+                                    void* d_scratch, size_t scratch_bytes, void* stream,
+                                    kvr_trace** out);
+
 /* --------------------------------------------------------------- policies */
-typedef enum { KVR_EVICT_LRU = 0, KVR_EVICT_RLT = 1 } kvr_eviction;
+/* KVR_EVICT_OPT: offline Belady for competitive ratios: evict the leaf
+ * != parent(t) whose next use is furthest; leaves never used again first (lowest
+ * slot among them), equal next use -> the deeper one.  Needs W = 1 and a trace
+ * with a next-use index (kvr_trace_build_next_use); a per-trial OPT policy
+ * without them gets KVR_TRIAL_BAD_POLICY, a default one is refused at
+ * kvr_sim_create (W) / kvr_sim_run (index). */
+typedef enum { KVR_EVICT_LRU = 0, KVR_EVICT_RLT = 1, KVR_EVICT_OPT = 2 } kvr_eviction;
 /* Alg. 1 leaves U = {} undefined (reading A5): */
 typedef enum { KVR_RLT_EARLY_RESET = 0,   /* T <- {t}, then uniform over leaves != parent(t) */
                KVR_RLT_UNIFORM_LEAF = 1,  /* uniform over leaves != parent(t), no reset */

@@ -15,6 +15,7 @@ struct kvr_trace {
   uint64_t total, salt;
   kvr::QueryHdr* hdr;
   uint64_t* hash;
+  const uint32_t* nu = nullptr;   // next-use index (offline OPT), borrowed
 };
 
 struct kvr_sim {
@@ -42,7 +43,7 @@ kvr_status cuda_fail(cudaError_t e, const char* what) {
 bool policy_ok(const kvr_policy& p, std::string* why) {
   char b[256];
   auto bad = [&](const char* s) { snprintf(b, sizeof b, "policy: %s", s); *why = b; return false; };
-  if (p.eviction > KVR_EVICT_RLT) return bad("eviction must be LRU(0) or RLT(1)");
+  if (p.eviction > KVR_EVICT_OPT) return bad("eviction must be LRU(0), RLT(1) or OPT(2)");
   if (p.rlt_fallback > KVR_RLT_LRU_MARKED) return bad("rlt_fallback must be 0..2");
   if (p.router > KVR_ROUTE_RANDOM) return bad("router must be 0..4");
   if (!(p.rho > 0.0 && p.rho <= 1.0)) return bad("rho must be in (0, 1]");
@@ -177,6 +178,36 @@ kvr_status kvr_trace_chained_hashes(const kvr_trace* tr, const uint64_t** d_hash
   return KVR_OK;
 }
 
+kvr_status kvr_trace_next_use_bytes(const kvr_trace* tr, size_t* nu_bytes, size_t* scratch_bytes) {
+  if (!tr || !nu_bytes || !scratch_bytes) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  if (tr->total >= 0x7fffffffull) return fail(KVR_ERR_UNSUPPORTED, "next-use index needs < 2^31 blocks");
+  *nu_bytes = (size_t)tr->total * 4;
+  cudaError_t e = kvr::next_use_scratch_bytes(tr->total, scratch_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "next-use scratch size");
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_build_next_use(const kvr_trace* tr, uint32_t* d_nu, size_t nu_bytes,
+                                    void* d_scratch, size_t scratch_bytes, void* stream,
+                                    kvr_trace** out) {
+  if (!tr || !out) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  size_t need_nu = 0, need_scr = 0;
+  kvr_status st = kvr_trace_next_use_bytes(tr, &need_nu, &need_scr);
+  if (st) return st;
+  if (tr->total && (!d_nu || !d_scratch)) return fail(KVR_ERR_INVALID_ARG, "null next-use/scratch buffer");
+  if (nu_bytes < need_nu || scratch_bytes < need_scr)
+    return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "next-use buffers too small (%zu/%zu < %zu/%zu)",
+                nu_bytes, scratch_bytes, need_nu, need_scr);
+  cudaError_t e = kvr::build_next_use(tr->hdr, tr->N, tr->hash, tr->total, d_nu, d_scratch,
+                                      scratch_bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "next-use index");
+  kvr_trace* t = new kvr_trace(*tr);
+  t->nu = d_nu;
+  *out = t;
+  return KVR_OK;
+}
+
 kvr_status kvr_trace_destroy(kvr_trace* tr) {
   delete tr;
   return KVR_OK;
@@ -198,6 +229,8 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
     return fail(KVR_ERR_INVALID_ARG, "service model must be finite");
   std::string why;
   if (!policy_ok(cfg->default_policy, &why)) return fail(KVR_ERR_INVALID_ARG, "%s", why.c_str());
+  if (cfg->default_policy.eviction == KVR_EVICT_OPT && cfg->W != 1)
+    return fail(KVR_ERR_INVALID_ARG, "policy: OPT (offline Belady) is defined for W = 1");
   kvr_sim* s = new kvr_sim;
   s->cfg = *cfg;
   *out = s;
@@ -265,6 +298,8 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
                   i, t->max_n, c.capacity_blocks);
     max_n = std::max(max_n, t->max_n);
     max_N = std::max(max_N, t->N);
+    if (!d_policies && c.default_policy.eviction == KVR_EVICT_OPT && !t->nu && t->total)
+      return fail(KVR_ERR_INVALID_ARG, "OPT needs a next-use index (kvr_trace_build_next_use) on trace %u", i);
   }
   const uint32_t R = std::min(c.record_trials, n_trials);
   if (R && !d_records) return fail(KVR_ERR_INVALID_ARG, "record_trials > 0 needs d_records");
@@ -279,6 +314,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   for (uint32_t i = 0; i < n_traces; ++i) {
     p.traces[i].hdr = traces[i]->hdr;
     p.traces[i].hash = traces[i]->hash;
+    p.traces[i].nu = traces[i]->nu;
     p.traces[i].N = traces[i]->N;
     p.traces[i].max_n = traces[i]->max_n;
     p.traces[i].block_tokens = traces[i]->block_tokens;

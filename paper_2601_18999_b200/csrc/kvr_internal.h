@@ -28,6 +28,7 @@ static_assert(sizeof(QueryHdr) == 32, "header is 32 B");
 struct TraceDev {
   const QueryHdr* hdr;  // [N]
   const uint64_t* hash; // [total] chained identities, CSR order
+  const uint32_t* nu;   // [total] next-use index (offline OPT) or null
   uint32_t N, max_n, block_tokens, _pad;
 };
 
@@ -168,6 +169,10 @@ cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, 
 cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W);
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
                           cudaStream_t s);
+// next-use index for the offline OPT analysis (kvr_nextuse.cu)
+cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);
+cudaError_t build_next_use(const QueryHdr* hdr, uint32_t N, const uint64_t* hash, uint64_t n,
+                           uint32_t* nu, void* scratch, size_t scratch_bytes, cudaStream_t s);
 // phase profiler (profiling build, -DKVR_PHASE_PROFILE); cudaErrorNotSupported otherwise
 cudaError_t phase_cycles(unsigned long long* out16, int reset);
 

@@ -797,11 +797,103 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
   __syncwarp();
 }
 
+// Offline Belady OPT (the W = 1 analysis of SURVEY §8f #1).  Per miss in
+// path order: evict the leaf != parent(t) with the largest key (next use, depth) --
+// leaves never used again rank highest, the lowest slot first -- found by a warp
+// max over the per-slot keys of the current leaves.  A node's key is set whenever
+// the current query touches it (hit or insert), so it is always its next use after
+// the current query.  Keys live in the worker's aux region (the recency log's
+// space, unused by OPT); LEAF bits and child counts are kept in place as for RLT.
+__device__ __forceinline__ uint64_t opt_key(uint32_t nu, uint32_t depth, uint32_t slot) {
+  return nu == 0xFFFFFFFFu ? (0xFFFFFFFF00000000ull | (0xFFFFu - slot))
+                           : (((uint64_t)nu << 32) | depth);
+}
+
+__device__ __forceinline__ uint64_t* opt_keys(const ReplayParams& p, uint32_t w) {
+  return reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
+                                     p.aux.off_log);
+}
+
+template <typename Idx, bool kGlobal, int kTag>
+__device__ __noinline__ void opt_decide(const ReplayParams& p_, uint32_t M, uint32_t kf, Idx p0,
+                                        const uint32_t* nu_q, uint32_t worker, uint32_t lane) {
+  const Idx NIL = Nil<Idx>::empty;
+  const uint32_t B = p_.B;
+  uint8_t* wb = worker_base<kGlobal>(p_, worker);
+  const WorkerView<Idx> S = make_view<Idx>(wb, p_.lay);
+  uint64_t* okey = opt_keys(p_, worker);
+  WarpSm* ws = warp_sm(p_, worker);
+  uint32_t* slots = ws->slot;
+  MemBits mb;
+  mb.leaf = S.leaf;
+  mb.mark = S.mark;
+  mb.nw = p_.lay.nwords;
+  uint32_t size = ws->x.size;
+  uint32_t vbits = 0, p = (uint32_t)p0;
+#pragma unroll 1
+  for (uint32_t q = 0; q < M; ++q) {
+    uint32_t slot, ev = 0;
+    if (size < B) {
+      slot = size++;
+      mb.leaf_set(slot, lane);
+    } else {
+      uint64_t best = 0;
+      uint32_t bs = 0;
+#pragma unroll 4
+      for (uint32_t base = 0; base < B; base += 32) {
+        const uint32_t sl = base + lane;
+        uint64_t k = 0;
+        if (sl < B && sl != p && ((S.leaf[sl >> 5] >> (sl & 31)) & 1u)) k = okey[sl];
+        if (k > best) {
+          best = k;
+          bs = sl;
+        }
+      }
+      const uint32_t hi = (uint32_t)(best >> 32), lo = (uint32_t)best;
+      const uint32_t mh = __reduce_max_sync(kFull, hi);
+      const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+      const uint32_t wl = __reduce_min_sync(kFull, (hi == mh && lo == ml) ? lane : 31u);
+      const uint32_t v = __shfl_sync(kFull, bs, wl);
+      // Evict(S, v): its parent loses a child and becomes a leaf without children
+      const Idx pv = S.parent[v];
+      if (pv != NIL) {
+        const Idx nc = (Idx)(S.nchild[pv] - 1);
+        __syncwarp();
+        if (lane == 0) S.nchild[pv] = nc;
+        if (nc == 0) mb.leaf_set((uint32_t)pv, lane);
+      }
+      slot = v;
+      ev = 1;
+      if (lane == (v >> 5)) vbits |= 1u << (v & 31);
+    }
+    // Load(S, t): the new leaf's key; its parent gets a child (stops being a leaf)
+    const uint32_t d = kf + q;
+    const uint64_t nk = opt_key(nu_q[d], d + 1, slot);
+    if (lane == 0) okey[slot] = nk;
+    if (q == 0) {
+      if (p0 != NIL) {
+        const Idx nc = S.nchild[p0];
+        __syncwarp();
+        if (lane == 0) S.nchild[p0] = (Idx)(nc + 1);
+        if (nc == 0) mb.leaf_clr((uint32_t)p0, lane);
+      }
+    } else {
+      mb.leaf_clr(p, lane);
+    }
+    if (lane == 0) slots[q] = slot | (ev << 31);
+    p = slot;
+    __syncwarp();
+  }
+  if (lane == 0) ws->x.size = size;
+  (ws->slot + 2 * p_.max_n)[lane] = vbits;   // victims -> overlay bitmap (read back by the caller)
+  __syncwarp();
+}
+
 // Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
 // victim digest term and the query record (trial sums are added in query order
 // by the accounting step).
 template <typename Idx, bool kGlobal, int kTag>
-__device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, uint32_t w, bool rlt,
+__device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, uint32_t w, bool tree,
                                           bool use_list, bool lbgr_or_static, kvr_query_record* rec,
                                           uint64_t* vlog) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(kvr_dsmem);
@@ -848,12 +940,12 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     __syncwarp();
     if (act) {
       S.key[my_slot] = t;
-      if (rlt) {
+      if (tree) {   // RLT and OPT keep the prefix tree (parents, child counts)
         S.parent[my_slot] = (Idx)par_slot;
         S.nchild[my_slot] = (Idx)(qq + 1 < M ? 1 : 0);
       }
       if (use_list) {
-        if (!rlt) R.stamp[my_slot] = wq;
+        if (!tree) R.stamp[my_slot] = wq;
         R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] = ((uint64_t)wq << 32) | my_slot;
       }
     }
@@ -961,7 +1053,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     const uint64_t K = p.keys[trial];
     const uint32_t N = tr.N, bt = tr.block_tokens;
     const bool rlt = pol.eviction == KVR_EVICT_RLT;
-    const bool use_list = !rlt || pol.rlt_fallback == KVR_RLT_LRU_MARKED;
+    const bool opt = pol.eviction == KVR_EVICT_OPT;   // offline Belady analysis (W = 1)
+    const bool tree = rlt || opt;                     // parents / child counts / LEAF bits
+    const bool use_list = pol.eviction == KVR_EVICT_LRU || (rlt && pol.rlt_fallback == KVR_RLT_LRU_MARKED);
     const bool lbgr = pol.router == KVR_ROUTE_LBGR;
     const uint32_t router = pol.router, fallback = pol.rlt_fallback;
     const bool lbgr_or_static = lbgr || router == KVR_ROUTE_STATIC_LINEAR;
@@ -1021,9 +1115,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     for (uint32_t kk = tid; kk <= p.max_n; kk += blockDim.x) divtab[kk] = (double)(bt * kk) / 1000.0;
 
     // a per-trial policy from device memory is validated here (host validated the default)
-    const bool pol_ok = pol.eviction <= KVR_EVICT_RLT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
+    const bool pol_ok = pol.eviction <= KVR_EVICT_OPT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
                         pol.router <= KVR_ROUTE_RANDOM && pol.rho > 0.0 && pol.rho <= 1.0 &&
-                        pol.delta_t_ms > 0.0;
+                        pol.delta_t_ms > 0.0 &&
+                        (!opt || (W == 1 && (tr.nu != nullptr || N == 0)));
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     const uint32_t Nrun = pol_ok ? N : 0;
 
@@ -1287,7 +1382,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
       // deferred apply of this warp's previous update (overlaps others' decisions)
       if (ws->active) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
 #ifdef KVR_PHASE_PROFILE
@@ -1363,6 +1458,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           R.stamp[s] = wr.wq;
           R.log[(ltail0 + (n - 1 - d)) & R.cap_mask] = ((uint64_t)wr.wq << 32) | (uint32_t)s;
         }
+        if (opt && act) opt_keys(p, w)[s] = opt_key(tr.nu[hd.block_off + d], d + 1, (uint32_t)s);
         if (rlt) {
           const bool um = act && !((S.mark[(uint32_t)s >> 5] >> ((uint32_t)s & 31)) & 1u);
           const uint32_t u = __ballot_sync(kFull, um);
@@ -1494,6 +1590,15 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           wr.size = xw.size;
           wr.cntT = xw.cntT;
         }
+      } else if (opt) {
+        if (M) {
+          __syncwarp();
+          if (lane == 0) ws->x.size = wr.size;
+          __syncwarp();
+          opt_decide<Idx, kGlobal, kMaxThreads>(p, M, kf, p0, tr.nu + hd.block_off, w, lane);
+          wr.size = ws->x.size;
+          if (lane == 0) ws->x.c_evict += nev;
+        }
       } else {
         // Leaf-LRU: the nev least recently used nodes, in order (batch == sequential)
         if (nev) {
@@ -1550,7 +1655,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       __syncwarp();
       if (!defer) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
     }
@@ -1558,7 +1663,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // ---- end of trial ----
     __syncthreads();   // all warps are past their last query before the final applies
     if (ws->active) {
-      apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, rlt, use_list, lbgr_or_static, rec, vlog);
+      apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
       vbits = 0;
     }
     __syncthreads();

@@ -1,0 +1,104 @@
+// kvr_nextuse.cu — next-use index of a packed trace for the offline Belady OPT
+// analysis (OPT = evict the leaf whose next use is furthest).
+//
+// nu[o] for block occurrence o (CSR order of the packed identities) is the index
+// of the next query after o's query whose path contains the same identity, or
+// 0xFFFFFFFF.  Identities inside one query are distinct (they encode the
+// position), so that is the query of the next occurrence of the identity in
+// CSR order: a stable radix sort of (identity, occurrence) pairs puts every
+// identity's occurrences next to each other in trace order, and one pass over the
+// sorted pairs writes the answer.  The sort is CUB's (CUDA toolkit) LSD radix
+// sort; this is offline preprocessing, not the replay path.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "kvr_internal.h"
+
+namespace kvr {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// query index of every occurrence: one warp per query
+__global__ void occurrence_query_kernel(const QueryHdr* hdr, uint32_t N, uint32_t* qidx) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= N) return;
+  const uint64_t off = hdr[j].block_off;
+  const uint32_t n = hdr[j].n_in + hdr[j].n_out;
+  for (uint32_t d = lane; d < n; d += 32) qidx[off + d] = j;
+}
+
+__global__ void iota_kernel(uint32_t* v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+
+// sorted[i] = (identity, occurrence) in (identity, occurrence) order
+__global__ void next_use_kernel(const uint64_t* key_sorted, const uint32_t* occ_sorted,
+                                const uint32_t* qidx, uint64_t n, uint32_t* nu) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = occ_sorted[i];
+    uint32_t next = 0xFFFFFFFFu;
+    if (i + 1 < n && key_sorted[i + 1] == key_sorted[i]) next = qidx[occ_sorted[i + 1]];
+    nu[o] = next;
+  }
+}
+
+struct ScratchLayout {
+  size_t keys_out, occ_in, occ_out, qidx, cub, total;
+};
+
+cudaError_t layout(uint64_t n, ScratchLayout* L) {
+  size_t cub_bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint64_t*)nullptr,
+                                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                                  (uint32_t*)nullptr, (int)n);
+  if (e != cudaSuccess) return e;
+  size_t o = 0;
+  L->keys_out = o; o = align_up(o + n * 8);
+  L->occ_in = o;   o = align_up(o + n * 4);
+  L->occ_out = o;  o = align_up(o + n * 4);
+  L->qidx = o;     o = align_up(o + n * 4);
+  L->cub = o;      o = align_up(o + cub_bytes);
+  L->total = o;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes) {
+  ScratchLayout L;
+  cudaError_t e = layout(n_blocks, &L);
+  if (e == cudaSuccess) *bytes = L.total;
+  return e;
+}
+
+cudaError_t build_next_use(const QueryHdr* hdr, uint32_t N, const uint64_t* hash, uint64_t n,
+                           uint32_t* nu, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ScratchLayout L;
+  cudaError_t e = layout(n, &L);
+  if (e != cudaSuccess) return e;
+  if (scratch_bytes < L.total) return cudaErrorInvalidValue;
+  uint8_t* b = static_cast<uint8_t*>(scratch);
+  uint64_t* keys_out = reinterpret_cast<uint64_t*>(b + L.keys_out);
+  uint32_t* occ_in = reinterpret_cast<uint32_t*>(b + L.occ_in);
+  uint32_t* occ_out = reinterpret_cast<uint32_t*>(b + L.occ_out);
+  uint32_t* qidx = reinterpret_cast<uint32_t*>(b + L.qidx);
+  const int threads = 256;
+  const int grid = (int)std::min<uint64_t>((n + threads - 1) / threads, 148ull * 16);
+  occurrence_query_kernel<<<(N + 7) / 8, 256, 0, s>>>(hdr, N, qidx);
+  iota_kernel<<<grid, threads, 0, s>>>(occ_in, n);
+  size_t cub_bytes = scratch_bytes - L.cub;
+  e = cub::DeviceRadixSort::SortPairs(b + L.cub, cub_bytes, hash, keys_out, occ_in, occ_out, (int)n,
+                                      0, 64, s);
+  if (e != cudaSuccess) return e;
+  next_use_kernel<<<grid, threads, 0, s>>>(keys_out, occ_out, qidx, n, nu);
+  return cudaGetLastError();
+}
+
+}  // namespace kvr

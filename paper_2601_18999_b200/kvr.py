@@ -21,14 +21,15 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KVR_LIB", os.path.join(_PKG, "libkvr.so"))
 
-EVICT_LRU, EVICT_RLT = 0, 1
+EVICT_LRU, EVICT_RLT, EVICT_OPT = 0, 1, 2   # OPT: offline Belady, W = 1 (needs with_next_use)
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
 TRIAL_OK, TRIAL_RING_OVERFLOW, TRIAL_VICTIM_LOG_FULL, TRIAL_BAD_POLICY = 0, 1, 2, 3
 
 # C-ABI entry points declared in include/kvr.h (the not-gpu test checks they are exported)
 EXPORTS = ("kvr_last_error", "kvr_abi_version", "kvr_trace_packed_bytes", "kvr_trace_load",
-           "kvr_trace_info", "kvr_trace_chained_hashes", "kvr_trace_destroy", "kvr_sim_create",
+           "kvr_trace_info", "kvr_trace_chained_hashes", "kvr_trace_destroy",
+           "kvr_trace_next_use_bytes", "kvr_trace_build_next_use", "kvr_sim_create",
            "kvr_sim_destroy", "kvr_sim_plan", "kvr_sim_workspace_bytes",
            "kvr_sim_workspace_bytes_multi", "kvr_sim_run", "kvr_sim_run_multi")
 
@@ -105,6 +106,8 @@ def lib():
             "kvr_trace_info": [vp, vp, vp, vp],
             "kvr_trace_chained_hashes": [vp, vp],
             "kvr_trace_destroy": [vp],
+            "kvr_trace_next_use_bytes": [vp, vp, vp],
+            "kvr_trace_build_next_use": [vp, vp, C.c_size_t, vp, C.c_size_t, vp, vp],
             "kvr_sim_create": [vp, vp],
             "kvr_sim_destroy": [vp],
             "kvr_sim_plan": [vp, u32, vp, vp, vp],
@@ -176,6 +179,20 @@ def kvr_trace_chained_hashes(handle: int) -> int:
 
 def kvr_trace_destroy(handle: int):
     _check(lib().kvr_trace_destroy(handle))
+
+
+def kvr_trace_next_use_bytes(handle: int):
+    a, b = C.c_size_t(0), C.c_size_t(0)
+    _check(lib().kvr_trace_next_use_bytes(handle, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def kvr_trace_build_next_use(handle: int, nu, scratch, stream=None) -> int:
+    h = C.c_void_p(0)
+    _check(lib().kvr_trace_build_next_use(handle, _ptr(nu), nu.numel() * nu.element_size(),
+                                          _ptr(scratch), scratch.numel(), _stream_ptr(stream),
+                                          C.byref(h)))
+    return h.value
 
 
 def kvr_sim_create(cfg: kvr_sim_config) -> int:
@@ -331,6 +348,25 @@ class DeviceTrace:
         n = self.n_blocks_total
         off = kvr_trace_chained_hashes(self.handle) - _ptr(self.packed)
         return self.packed[off: off + 8 * n].cpu().numpy().view(np.uint64).copy()
+
+    def with_next_use(self, stream=None) -> "DeviceTrace":
+        """A trace handle that also carries the next-use index (offline OPT,
+        KVR_EVICT_OPT): same packed buffer, plus a u32 [n_blocks_total] index
+        built on the device by kvr_trace_build_next_use."""
+        import copy
+        import torch
+        nb, sb = kvr_trace_next_use_bytes(self.handle)
+        t = copy.copy(self)
+        t.nu = torch.empty(max(1, nb // 4), dtype=torch.int32, device=self.device)
+        scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=self.device)
+        t.handle = kvr_trace_build_next_use(self.handle, t.nu, scratch, stream)
+        torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+        t._parent = self        # keeps the packed buffer alive
+        return t
+
+    def next_use(self) -> np.ndarray:
+        """Copy of the device next-use index (u32 per block occurrence, CSR order)."""
+        return self.nu[: self.n_blocks_total].cpu().numpy().view(np.uint32).copy()
 
     def close(self):
         if getattr(self, "handle", None):

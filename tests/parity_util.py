@@ -34,9 +34,11 @@ def run_oracle(oracle, tr, W, B, pols, keys, truth, ring, record, victims_cap, b
 
 
 def run_gpu(kvr, traces, W, B, pols, keys, truth, ring, record, victims_cap, force_tier=0,
-            trial_trace=None, bins=0):
+            trial_trace=None, bins=0, next_use=False):
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
     dts = [DeviceTrace(t) for t in traces]
+    if next_use:   # offline OPT trials need the next-use index
+        dts = [d.with_next_use() for d in dts]
     sim = Simulator(W, B, alpha_cached_ms=truth[0], alpha_miss_ms=truth[1],
                     out_ms_per_token=truth[2], pending_ring=ring,
                     record_trials=len(keys) if record else 0, force_tier=force_tier,
@@ -71,12 +73,12 @@ def assert_records_equal(grec, orec, n, ctx=""):
 
 
 def compare(oracle, kvr, tr, W, B, pols, keys, truth=(0.0, 1.0, 20.0), ring=256, record=True,
-            victims_cap=None, force_tier=0, bins=0):
+            victims_cap=None, force_tier=0, bins=0, next_use=False):
     n = tr.n_queries
     if victims_cap is None:
         victims_cap = max(1, tr.total_blocks)
     out, _, _ = run_gpu(kvr, [tr], W, B, pols, keys, truth, ring, record, victims_cap,
-                        force_tier=force_tier, bins=bins)
+                        force_tier=force_tier, bins=bins, next_use=next_use)
     orc = run_oracle(oracle, tr, W, B, pols, keys, truth, ring, record, victims_cap, bins=bins)
     for t, o in enumerate(orc):
         ctx = f"trial {t} key {keys[t]} pol {pols[t]}"
