@@ -17,6 +17,7 @@ _HDR = os.path.join(_HERE, "kvr_oracle.h")
 EVICT_LRU, EVICT_RLT, EVICT_OPT = 0, 1, 2
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
+ROUTE_LBGR_RLS = 5   # LBGR with the RLS reading of the 0.992 update (A8b)
 
 
 def build_oracle(force: bool = False) -> str:
@@ -45,7 +46,7 @@ class _Policy(C.Structure):
                 ("est_alpha_cached_ms", C.c_double), ("est_alpha_miss_ms", C.c_double),
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
-                ("w_hit", C.c_double), ("w_load", C.c_double)]
+                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double)]
 
 
 class _Config(C.Structure):
@@ -80,6 +81,8 @@ def lib():
         L.kvro_fmix64.argtypes = [C.c_uint64]
         L.kvro_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.kvro_chain.argtypes = [C.POINTER(_Trace), C.c_void_p]
+        L.kvro_rls_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double]
+        L.kvro_rls_step.restype = None
         L.kvro_run.argtypes = [C.POINTER(_Config), C.POINTER(_Trace), C.POINTER(_Policy),
                                C.c_uint64, C.POINTER(_Result), C.c_void_p, C.c_void_p,
                                C.c_uint64, C.c_void_p, C.c_int]
@@ -111,6 +114,7 @@ class OraclePolicy:
     tau: float = 1.5
     w_hit: float = 1.0
     w_load: float = 1.0
+    rls_p0: float = 1000.0
 
     def _c(self) -> _Policy:
         p = _Policy()
@@ -120,6 +124,7 @@ class OraclePolicy:
         for k in range(4):
             p.theta0[k] = float(self.theta0[k])
         p.tau, p.w_hit, p.w_load = self.tau, self.w_hit, self.w_load
+        p.rls_p0 = self.rls_p0
         return p
 
 
@@ -175,6 +180,12 @@ def philox4x32_10(ctr: Sequence[int], key: Sequence[int]) -> tuple:
     o = np.zeros(4, dtype=np.uint32)
     lib().kvro_philox4x32_10(c.ctypes.data, k.ctypes.data, o.ctypes.data)
     return tuple(int(v) for v in o)
+
+
+def rls_step(P: np.ndarray, theta: np.ndarray, phi, e: float, lam: float):
+    """In-place RLS step (P float64 [4,4] C-contiguous, theta float64 [4])."""
+    ph = np.ascontiguousarray(phi, dtype=np.float64)
+    lib().kvro_rls_step(P.ctypes.data, theta.ctypes.data, ph.ctypes.data, float(e), float(lam))
 
 
 def chain(tr) -> np.ndarray:

@@ -319,10 +319,35 @@ struct Rec {  // one pending completion (A12)
   uint64_t ka;
 };
 
+// One step of exponentially weighted recursive least squares (forgetting factor
+// lam): pi = P phi, gamma = lam + phi' pi, k = pi / gamma, theta += k e,
+// P = (P - k pi') / lam; every sum and loop in ascending index order.
+void rls_step(double Pm[4][4], double th[4], const double phi[4], double e, double lam) {
+  double pi[4];
+  for (int a = 0; a < 4; ++a) {
+    double t = Pm[a][0] * phi[0];
+    t = t + Pm[a][1] * phi[1];
+    t = t + Pm[a][2] * phi[2];
+    t = t + Pm[a][3] * phi[3];
+    pi[a] = t;
+  }
+  double g = phi[0] * pi[0];
+  g = g + phi[1] * pi[1];
+  g = g + phi[2] * pi[2];
+  g = g + phi[3] * pi[3];
+  const double gamma = lam + g;
+  double kv[4];
+  for (int a = 0; a < 4; ++a) kv[a] = pi[a] / gamma;
+  for (int a = 0; a < 4; ++a) th[a] = th[a] + kv[a] * e;
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) Pm[a][b] = (Pm[a][b] - kv[a] * pi[b]) / lam;
+}
+
 struct Worker {
   Cache cache;
   double P = 0.0, F = 0.0, Pt = 0.0;
   double th[4] = {0, 0, 0, 0};
+  double Pm[4][4] = {};          // LBGR_RLS inverse-correlation matrix
   std::deque<Rec> fifo;
   uint64_t k = 0, e = 0;
 };
@@ -332,6 +357,9 @@ struct Worker {
 extern "C" {
 
 uint32_t kvro_version(void) { return 1; }
+void kvro_rls_step(double P[16], double theta[4], const double phi[4], double e, double lam) {
+  rls_step(reinterpret_cast<double(*)[4]>(P), theta, phi, e, lam);
+}
 uint64_t kvro_fmix64(uint64_t x) { return fmix64(x); }
 void kvro_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) { philox(ctr, key, out); }
 
@@ -350,7 +378,10 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   const uint32_t W = cfg->W, B = cfg->capacity_blocks;
   if (W < 1 || W > 32 || B < 1 || B > 65536) return 1;
   if (pol->eviction > KVRO_EVICT_OPT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
-      pol->router > KVRO_ROUTE_RANDOM)
+      pol->router > KVRO_ROUTE_LBGR_RLS)
+    return 1;
+  if (pol->router == KVRO_ROUTE_LBGR_RLS &&
+      (!(pol->mu > 0.0 && pol->mu <= 1.0) || !(pol->rls_p0 > 0.0) || !std::isfinite(pol->rls_p0)))
     return 1;
   // Belady OPT is defined for one cache: the offline analysis runs it at W = 1
   if (pol->eviction == KVRO_EVICT_OPT && W != 1) return 1;
@@ -371,11 +402,15 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
         depth_of[H[o]] = (uint32_t)(o - tr->block_offsets[j]) + 1;
       }
   std::vector<Worker> w(W);
+  const bool rls = pol->router == KVRO_ROUTE_LBGR_RLS;
   for (auto& x : w) {
     x.cache.B = B;
     for (int k = 0; k < 4; ++k) x.th[k] = pol->theta0[k];
+    if (rls)
+      for (int k = 0; k < 4; ++k) x.Pm[k][k] = pol->rls_p0;
   }
-  const bool lbgr = pol->router == KVRO_ROUTE_LBGR;
+  // LBGR_RLS is LBGR (Eq. 4-6, Alg. 2) with the other reading of the update (A8b)
+  const bool lbgr = pol->router == KVRO_ROUTE_LBGR || rls;
   const double rho = pol->rho, dt = pol->delta_t_ms, mu = pol->mu;
   uint64_t D = K;
   uint64_t vcursor = 0;
@@ -406,7 +441,7 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
         if (!x.fifo.empty() && x.fifo.front().c <= t) {
           Rec r = x.fifo.front();
           x.fifo.pop_front();
-          if (lbgr) {
+          if (lbgr && !rls) {
             // OnlineUpdate: NLMS step on the squared residual (A8)
             double E = r.c - r.a;
             double res = E - r.Ehat;
@@ -420,6 +455,12 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
             x.th[1] = x.th[1] + g * r.phi1;
             x.th[2] = x.th[2] + g * r.phi2;
             x.th[3] = x.th[3] + g * phi3;
+          } else if (rls) {
+            // OnlineUpdate, RLS reading (A8b) on the same residual e = E - E^
+            const double phi[4] = {r.phi0, r.phi1, r.phi2, 1.0};
+            rls_step(x.Pm, x.th, phi, (r.c - r.a) - r.Ehat, mu);
+          }
+          if (lbgr) {
             // ReleaseLoad: remove the decayed remainder rho^kappa * Chat (A10)
             uint64_t kap = x.k - r.ka;
             double pw = 1.0, b = rho;
@@ -446,7 +487,7 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     // 3. score + argmin (lowest index on ties, A15)
     uint32_t best = 0;
     double score_best = 0.0;
-    if (pol->router == KVRO_ROUTE_LBGR) {
+    if (lbgr) {
       for (uint32_t i = 0; i < W; ++i) {
         double x = (double)(tr->block_tokens * m[i]);
         double y = (double)(q - tr->block_tokens * m[i]);

@@ -39,7 +39,8 @@ extern "C" {
 enum { KVRO_EVICT_LRU = 0, KVRO_EVICT_RLT = 1, KVRO_EVICT_OPT = 2 /* Belady; W = 1 only */ };
 enum { KVRO_RLT_EARLY_RESET = 0, KVRO_RLT_UNIFORM_LEAF = 1, KVRO_RLT_LRU_MARKED = 2 };
 enum { KVRO_ROUTE_LBGR = 0, KVRO_ROUTE_STATIC_LINEAR = 1, KVRO_ROUTE_THRESHOLD = 2,
-       KVRO_ROUTE_ROUND_ROBIN = 3, KVRO_ROUTE_RANDOM = 4 };
+       KVRO_ROUTE_ROUND_ROBIN = 3, KVRO_ROUTE_RANDOM = 4,
+       KVRO_ROUTE_LBGR_RLS = 5 /* LBGR with the RLS reading of "0.992" (A8b) */ };
 /* per-trial status codes */
 enum { KVRO_TRIAL_OK = 0, KVRO_TRIAL_RING_OVERFLOW = 1, KVRO_TRIAL_VICTIM_LOG_FULL = 2 };
 
@@ -62,6 +63,7 @@ typedef struct {
   double rho, delta_t_ms, mu, theta0[4];
   double tau;
   double w_hit, w_load;
+  double rls_p0;                  /* LBGR_RLS: initial covariance P = rls_p0 * I */
 } kvro_policy;
 
 typedef struct {
@@ -91,6 +93,10 @@ uint64_t kvro_fmix64(uint64_t x);
 void     kvro_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 /* chained block identities of every block of the trace (SURVEY §8c Definitions, A26) */
 int      kvro_chain(const kvro_trace* tr, uint64_t* out_hashes /* [offsets[N]] */);
+
+/* one RLS step of the LBGR_RLS residual model (reading A8b): P row-major 4x4,
+ * e = target - prediction; exposed for the pins */
+void kvro_rls_step(double P[16], double theta[4], const double phi[4], double e, double lam);
 
 /* ---- the replay (one trial) ---- */
 int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* pol,

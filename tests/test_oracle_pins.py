@@ -440,3 +440,26 @@ def test_p22_rlt_draw_slot_order_kat(oracle_mod, key, victim_block):
     r64 = oracle_mod.philox4x32_10([0, 0, 0, 1], [key & 0xFFFFFFFF, key >> 32])
     r64 = r64[0] | (r64[1] << 32)
     assert (r64 * 3) >> 64 == victim_block - 1
+
+
+# -------------------------------------------------------------------------- P23
+@pytest.mark.parametrize("lam", [1.0, 0.992, 0.97])   # (1/lam)^n bounds rounding growth
+def test_p23_rls_step_is_weighted_least_squares(oracle_mod, lam):
+    """The LBGR_RLS residual model (reading A8b of "learning rate 0.992"; the
+    squared-loss objective of P:361): n sequential RLS steps from P0 = p0*I,
+    theta0 = 0 equal the closed-form exponentially weighted least squares
+    argmin sum_t lam^(n-t) (y_t - phi_t' theta)^2 + lam^n/p0 |theta|^2."""
+    rng = np.random.default_rng(23)
+    n, p0 = 200, 1e6
+    X = np.column_stack([rng.normal(size=(n, 3)), np.ones(n)])
+    y = X @ np.array([0.5, -2.0, 1.25, 3.0]) + 0.1 * rng.normal(size=n)
+    P = np.eye(4) * p0
+    th = np.zeros(4)
+    for t in range(n):
+        oracle_mod.rls_step(P, th, X[t], y[t] - X[t] @ th, lam)
+    w = lam ** (n - 1 - np.arange(n))
+    A = (X * w[:, None]).T @ X + (lam ** n / p0) * np.eye(4)
+    ref = np.linalg.solve(A, (X * w[:, None]).T @ y)
+    assert np.allclose(th, ref, rtol=1e-7, atol=1e-9), (th, ref)
+    # P starts at 1e6*I: the first steps cancel ~6 digits, later ones amplify by 1/lam
+    assert np.allclose(P, np.linalg.inv(A), rtol=1e-4, atol=1e-10)
