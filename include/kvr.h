@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 1u
+#define KVR_ABI_VERSION 2u   /* 2: KVR_EVICT_OPT, next-use index, KVR_ROUTE_LBGR_RLS + rls_p0 */
 
 typedef int32_t kvr_status;
 enum {
@@ -133,7 +133,11 @@ typedef enum { KVR_ROUTE_LBGR = 0,           /* Alg. 2 / Eq. 4-6 */
                KVR_ROUTE_STATIC_LINEAR = 1,  /* w_load*pending - w_hit*h/|q| (A17) */
                KVR_ROUTE_THRESHOLD = 2,      /* cache-aware: balance if max>tau*max(1,min) (A16) */
                KVR_ROUTE_ROUND_ROBIN = 3,    /* j mod W */
-               KVR_ROUTE_RANDOM = 4          /* Philox(K,(j,0xFFFFFFFF,2)) */
+               KVR_ROUTE_RANDOM = 4,         /* Philox(K,(j,0xFFFFFFFF,2)) */
+               KVR_ROUTE_LBGR_RLS = 5        /* LBGR with the RLS reading of "learning rate
+                                                0.992" (reading A8b): exponentially
+                                                weighted least squares, forgetting factor mu,
+                                                P(0) = rls_p0 * I */
 } kvr_router;
 
 /* Eq. 1 ground truth: Cost = aC*h + aM*(|q|-h) + o*|a| (A13, A14) */
@@ -147,6 +151,7 @@ typedef struct {
                                                      NLMS step mu (A8), initial theta */
   double tau;                                     /* THRESHOLD */
   double w_hit, w_load;                           /* STATIC_LINEAR */
+  double rls_p0;                                  /* LBGR_RLS: initial covariance scale (> 0) */
 } kvr_policy;
 
 typedef struct {

@@ -45,7 +45,11 @@ bool policy_ok(const kvr_policy& p, std::string* why) {
   auto bad = [&](const char* s) { snprintf(b, sizeof b, "policy: %s", s); *why = b; return false; };
   if (p.eviction > KVR_EVICT_OPT) return bad("eviction must be LRU(0), RLT(1) or OPT(2)");
   if (p.rlt_fallback > KVR_RLT_LRU_MARKED) return bad("rlt_fallback must be 0..2");
-  if (p.router > KVR_ROUTE_RANDOM) return bad("router must be 0..4");
+  if (p.router > KVR_ROUTE_LBGR_RLS) return bad("router must be 0..5");
+  if (p.router == KVR_ROUTE_LBGR_RLS && !(p.mu > 0.0 && p.mu <= 1.0))
+    return bad("LBGR_RLS forgetting factor mu must be in (0, 1]");
+  if (p.router == KVR_ROUTE_LBGR_RLS && !(p.rls_p0 > 0.0 && std::isfinite(p.rls_p0)))
+    return bad("LBGR_RLS rls_p0 must be finite and > 0");
   if (!(p.rho > 0.0 && p.rho <= 1.0)) return bad("rho must be in (0, 1]");
   if (!(p.delta_t_ms > 0.0)) return bad("delta_t_ms must be > 0 (inf allowed)");
   const double fin[] = {p.est_alpha_cached_ms, p.est_alpha_miss_ms, p.mu, p.theta0[0], p.theta0[1],

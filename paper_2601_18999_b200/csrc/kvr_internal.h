@@ -73,7 +73,7 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
 // compacted when full; validated by the per-slot stamps of the worker state).
 struct AuxLayout {
   uint32_t ring, log_cap;
-  size_t off_fifo, off_log, bytes;
+  size_t off_fifo, off_log, off_rls, bytes;   // rls: LBGR_RLS P (4x4, fp64)
 };
 
 inline AuxLayout make_aux(uint32_t B, uint32_t ring, uint32_t max_n) {
@@ -85,6 +85,7 @@ inline AuxLayout make_aux(uint32_t B, uint32_t ring, uint32_t max_n) {
   size_t o = 0;
   A.off_fifo = o;  o = align16(o + (size_t)ring * kFifoRecBytes);
   A.off_log = o;   o = align16(o + (size_t)C * 8);
+  A.off_rls = o;   o = align16(o + 16 * 8);
   A.bytes = (o + 127) & ~(size_t)127;
   return A;
 }

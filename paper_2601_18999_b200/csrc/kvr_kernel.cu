@@ -797,6 +797,13 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
   __syncwarp();
 }
 
+// LBGR_RLS residual model (reading A8b of "learning rate 0.992"; squared
+// loss): P (4x4, fp64) lives in the worker's aux region (global, L2).
+__device__ __forceinline__ double* rls_region(const ReplayParams& p, uint32_t w) {
+  return reinterpret_cast<double*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
+                                   p.aux.off_rls);
+}
+
 // Offline Belady OPT (the W = 1 analysis of SURVEY §8f #1).  Per miss in
 // path order: evict the leaf != parent(t) with the largest key (next use, depth) --
 // leaves never used again rank highest, the lowest slot first -- found by a warp
@@ -1056,7 +1063,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     const bool opt = pol.eviction == KVR_EVICT_OPT;   // offline Belady analysis (W = 1)
     const bool tree = rlt || opt;                     // parents / child counts / LEAF bits
     const bool use_list = pol.eviction == KVR_EVICT_LRU || (rlt && pol.rlt_fallback == KVR_RLT_LRU_MARKED);
-    const bool lbgr = pol.router == KVR_ROUTE_LBGR;
+    const bool rls = pol.router == KVR_ROUTE_LBGR_RLS;   // LBGR, RLS reading A8b
+    const bool lbgr = pol.router == KVR_ROUTE_LBGR || rls;
     const uint32_t router = pol.router, fallback = pol.rlt_fallback;
     const bool lbgr_or_static = lbgr || router == KVR_ROUTE_STATIC_LINEAR;
     const bool recorded = trial < p.record_trials;
@@ -1093,6 +1101,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // front record of the pending FIFO: lane f < 8 holds field f; fr_c is uniform
     double fr = 0.0, fr_c = 0.0;
     uint32_t vbits = 0;     // victims of this warp's pending update (lane l: word l)
+    if (rls && lane < 16) rls_region(p, w)[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;   // P = p0 I
     if (lane == 0) {
       ws->active = 0;
       ws->c_probes = 0; ws->c_hit = 0; ws->c_in = 0; ws->c_q = 0; ws->c_maxp = 0;
@@ -1116,7 +1125,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
     // a per-trial policy from device memory is validated here (host validated the default)
     const bool pol_ok = pol.eviction <= KVR_EVICT_OPT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
-                        pol.router <= KVR_ROUTE_RANDOM && pol.rho > 0.0 && pol.rho <= 1.0 &&
+                        pol.router <= KVR_ROUTE_LBGR_RLS && pol.rho > 0.0 && pol.rho <= 1.0 &&
+                        (!rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
+                                  pol.rls_p0 < INFINITY)) &&
                         pol.delta_t_ms > 0.0 &&
                         (!opt || (W == 1 && (tr.nu != nullptr || N == 0)));
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
@@ -1196,19 +1207,47 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
               const double g0 = __shfl_sync(kFull, fr, 3), g1 = __shfl_sync(kFull, fr, 4);
               const double g2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
               const uint64_t ka = (uint64_t)__double_as_longlong(__shfl_sync(kFull, fr, 7));
-              // OnlineUpdate (A8): NLMS on the squared residual
               const double E = fr_c - fa;
               const double res = E - fE;
-              const double g3 = 1.0;
-              double s = g0 * g0;
-              s = s + g1 * g1;
-              s = s + g2 * g2;
-              s = s + g3 * g3;
-              const double gstep = (pol.mu * res) / (1.0 + s);
-              th0 = th0 + gstep * g0;
-              th1 = th1 + gstep * g1;
-              th2 = th2 + gstep * g2;
-              th3 = th3 + gstep * g3;
+              if (rls) {
+                // OnlineUpdate, RLS reading (A8b), one weighted least-squares step in
+                // the oracle's order (rls_step): lane 4a+b holds P[a][b]; every sum is
+                // gathered by shuffles left to right.  pi = P phi, gamma = lam + phi'pi,
+                // k = pi / gamma, theta += k e, P = (P - k pi') / lam.
+                const double lam = pol.mu;
+                double* Rg = rls_region(p, w);
+                const uint32_t ra = (lane >> 2) & 3u, rb = lane & 3u;
+                const double Pab = lane < 16 ? Rg[lane] : 0.0;
+                const double phb = rb == 0 ? g0 : (rb == 1 ? g1 : (rb == 2 ? g2 : 1.0));
+                const double prod = Pab * phb;
+                double pi = __shfl_sync(kFull, prod, 4 * ra);
+                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 1);
+                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 2);
+                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 3);   // pi[a] in lanes 4a..4a+3
+                double gsum = g0 * __shfl_sync(kFull, pi, 0);
+                gsum = gsum + g1 * __shfl_sync(kFull, pi, 4);
+                gsum = gsum + g2 * __shfl_sync(kFull, pi, 8);
+                gsum = gsum + 1.0 * __shfl_sync(kFull, pi, 12);
+                const double gamma = lam + gsum;
+                const double kk = pi / gamma;                       // k[a]
+                const double pib = __shfl_sync(kFull, pi, 4 * rb);  // pi[b]
+                if (lane < 16) Rg[lane] = (Pab - kk * pib) / lam;
+                th0 = th0 + __shfl_sync(kFull, kk, 0) * res;
+                th1 = th1 + __shfl_sync(kFull, kk, 4) * res;
+                th2 = th2 + __shfl_sync(kFull, kk, 8) * res;
+                th3 = th3 + __shfl_sync(kFull, kk, 12) * res;
+              } else {     // OnlineUpdate (A8): NLMS on the squared residual
+                const double g3 = 1.0;
+                double s = g0 * g0;
+                s = s + g1 * g1;
+                s = s + g2 * g2;
+                s = s + g3 * g3;
+                const double gstep = (pol.mu * res) / (1.0 + s);
+                th0 = th0 + gstep * g0;
+                th1 = th1 + gstep * g1;
+                th2 = th2 + gstep * g2;
+                th3 = th3 + gstep * g3;
+              }
               // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
               uint64_t kap = k - ka;
               double pw = 1.0, bb = rho;
@@ -1350,7 +1389,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
       // ---- 4. argmin over workers (every warp computes the same i*) ----
       uint32_t best = 0;
-      if (router == KVR_ROUTE_LBGR || router == KVR_ROUTE_STATIC_LINEAR) {
+      if (lbgr || router == KVR_ROUTE_STATIC_LINEAR) {
         // first minimum = lowest lane holding the smallest order-preserving key of
         // the fp64 score (-0 folded into +0, which the fp compare treats as equal);
         // three uniform-datapath reductions instead of a 5-round shuffle tournament

@@ -24,6 +24,7 @@ LIB_PATH = os.environ.get("KVR_LIB", os.path.join(_PKG, "libkvr.so"))
 EVICT_LRU, EVICT_RLT, EVICT_OPT = 0, 1, 2   # OPT: offline Belady, W = 1 (needs with_next_use)
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
+ROUTE_LBGR_RLS = 5   # LBGR, RLS reading of the 0.992 update (A8b)
 TRIAL_OK, TRIAL_RING_OVERFLOW, TRIAL_VICTIM_LOG_FULL, TRIAL_BAD_POLICY = 0, 1, 2, 3
 
 # C-ABI entry points declared in include/kvr.h (the not-gpu test checks they are exported)
@@ -59,7 +60,7 @@ class kvr_policy(C.Structure):
                 ("est_alpha_cached_ms", C.c_double), ("est_alpha_miss_ms", C.c_double),
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
-                ("w_hit", C.c_double), ("w_load", C.c_double)]
+                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double)]
 
 
 class kvr_sim_config(C.Structure):
@@ -73,7 +74,7 @@ POLICY_DTYPE = np.dtype([("eviction", "<u4"), ("rlt_fallback", "<u4"), ("router"
                          ("_pad", "<u4"), ("est_alpha_cached_ms", "<f8"),
                          ("est_alpha_miss_ms", "<f8"), ("rho", "<f8"), ("delta_t_ms", "<f8"),
                          ("mu", "<f8"), ("theta0", "<f8", (4,)), ("tau", "<f8"),
-                         ("w_hit", "<f8"), ("w_load", "<f8")])
+                         ("w_hit", "<f8"), ("w_load", "<f8"), ("rls_p0", "<f8")])
 RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
     "queries", "hit_tokens", "input_tokens", "probes", "inserted_blocks", "evictions",
     "rlt_draws", "rlt_resets", "rlt_fallbacks", "max_pending", "decision_digest")] +
@@ -83,7 +84,7 @@ RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
 RECORD_DTYPE = np.dtype([("worker", "<u4"), ("hit_tokens", "<u4"), ("n_victims", "<u4"),
                          ("_pad", "<u4"), ("ttft_ms", "<f8"), ("latency_ms", "<f8"),
                          ("score", "<f8"), ("victim_offset", "<u8")])
-assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 112
+assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 120
 assert RESULT_DTYPE.itemsize == 144 and RECORD_DTYPE.itemsize == 48
 
 _lib = None
@@ -260,6 +261,7 @@ class Policy:
     tau: float = 1.5
     w_hit: float = 1.0
     w_load: float = 1.0
+    rls_p0: float = 1000.0     # LBGR_RLS initial covariance P = rls_p0 * I
 
     def c(self) -> kvr_policy:
         p = kvr_policy()

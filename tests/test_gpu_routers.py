@@ -1,0 +1,48 @@
+"""Router variants on the GPU: LBGR with the RLS reading of the
+0.992 update (router 5, reading A8b) against the oracle's full replay, field by
+field and per query (decisions bit-exact; the RLS algebra runs in the oracle's
+order).  The oracle's RLS step is pinned to closed-form weighted least squares
+(test_p23)."""
+import numpy as np
+import pytest
+
+from paper_2601_18999_b200 import workloads as wl
+from parity_util import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def kvr():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    from paper_2601_18999_b200 import build
+    build.build()
+    from paper_2601_18999_b200 import kvr as k
+    return k
+
+
+@pytest.mark.parametrize("W", [1, 4, 8])
+def test_lbgr_rls_parity(kvr, oracle_mod, W):
+    tr = wl.gsp(30, 16, 0.5, seed=0x81 + W, W=W)
+    pols = [kvr.Policy(router=kvr.ROUTE_LBGR_RLS, eviction=e, mu=mu, rls_p0=p0)
+            for e, mu, p0 in ((1, 0.992, 1000.0), (0, 0.992, 10.0), (1, 0.9, 1e4), (1, 1.0, 1.0))]
+    compare(oracle_mod, kvr, tr, W, 512, pols, [11, 12, 13, 14], record=True)
+
+
+def test_lbgr_rls_drift_and_tiers(kvr, oracle_mod):
+    tr = wl.drift(2048, 200_000, seed=0xC5, W=16).prefix(3000)
+    for tier in (1, 2):
+        pols = [kvr.Policy(router=kvr.ROUTE_LBGR_RLS), kvr.Policy(router=kvr.ROUTE_LBGR)]
+        compare(oracle_mod, kvr, tr, 16, 512, pols, [21, 22], record=True, force_tier=tier)
+
+
+def test_lbgr_rls_validation(kvr):
+    with pytest.raises(kvr.KvrError):
+        kvr.Simulator(4, 64, policy=kvr.Policy(router=kvr.ROUTE_LBGR_RLS, rls_p0=0.0))
+    tr = wl.gsp(4, 4, 0.5, seed=1, W=2)
+    sim = kvr.Simulator(2, 512)
+    out = sim.run(kvr.DeviceTrace(tr), np.array([1, 2], np.uint64),
+                  kvr.policies_array([kvr.Policy(router=kvr.ROUTE_LBGR_RLS, mu=1.5),
+                                      kvr.Policy(router=kvr.ROUTE_LBGR_RLS)]))
+    assert int(out.results[0]["status"]) == 3 and int(out.results[1]["status"]) == 0
