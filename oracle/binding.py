@@ -46,7 +46,8 @@ class _Policy(C.Structure):
                 ("est_alpha_cached_ms", C.c_double), ("est_alpha_miss_ms", C.c_double),
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
-                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double)]
+                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double),
+                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32)]
 
 
 class _Config(C.Structure):
@@ -115,6 +116,8 @@ class OraclePolicy:
     w_hit: float = 1.0
     w_load: float = 1.0
     rls_p0: float = 1000.0
+    tracker_lag: int = 0       # A29: router lags the previous query's update
+    tracker_grain: int = 1     # A29: router sees whole grains of matched blocks
 
     def _c(self) -> _Policy:
         p = _Policy()
@@ -125,6 +128,7 @@ class OraclePolicy:
             p.theta0[k] = float(self.theta0[k])
         p.tau, p.w_hit, p.w_load = self.tau, self.w_hit, self.w_load
         p.rls_p0 = self.rls_p0
+        p.tracker_lag, p.tracker_grain = self.tracker_lag, self.tracker_grain
         return p
 
 

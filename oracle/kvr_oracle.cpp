@@ -380,6 +380,7 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   if (pol->eviction > KVRO_EVICT_OPT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
       pol->router > KVRO_ROUTE_LBGR_RLS)
     return 1;
+  if (pol->tracker_lag > 1 || pol->tracker_grain < 1) return 1;
   if (pol->router == KVRO_ROUTE_LBGR_RLS &&
       (!(pol->mu > 0.0 && pol->mu <= 1.0) || !(pol->rls_p0 > 0.0) || !std::isfinite(pol->rls_p0)))
     return 1;
@@ -415,7 +416,9 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   uint64_t D = K;
   uint64_t vcursor = 0;
   bool vlog_full = false;
-  std::vector<uint32_t> m(W);
+  std::vector<uint32_t> m(W), mt(W);   // true match, and the tracker's view of it (A29)
+  Cache prev_cache;                      // the previous chooser's cache before its update
+  int64_t prev_worker = -1;
   std::vector<double> Ehat(W), Chat(W), phi0(W), phi1(W), phi2(W);
 
   for (uint32_t j = 0; j < tr->n_queries; ++j) {
@@ -482,6 +485,11 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     for (uint32_t i = 0; i < W; ++i) {
       m[i] = match_prefix(w[i].cache, Hj, n_in);
       out->probes += std::min<uint64_t>(m[i] + 1, n_in);
+      // global tracker (App. E; reading A29): the router's estimate h~
+      // lags the previous query's update and is coarsened to whole grains
+      uint32_t v = (pol->tracker_lag && (int64_t)i == prev_worker)
+                       ? match_prefix(prev_cache, Hj, n_in) : m[i];
+      mt[i] = pol->tracker_grain * (v / pol->tracker_grain);
     }
 
     // 3. score + argmin (lowest index on ties, A15)
@@ -489,8 +497,8 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     double score_best = 0.0;
     if (lbgr) {
       for (uint32_t i = 0; i < W; ++i) {
-        double x = (double)(tr->block_tokens * m[i]);
-        double y = (double)(q - tr->block_tokens * m[i]);
+        double x = (double)(tr->block_tokens * mt[i]);          // h~ (A29; = h by default)
+        double y = (double)(q - tr->block_tokens * mt[i]);
         double C = (pol->est_alpha_cached_ms * x) + (pol->est_alpha_miss_ms * y);   // Eq. 5
         double f0 = x / 1000.0, f1 = y / 1000.0, f2 = w[i].Pt / 1000.0, f3 = 1.0;  // A9
         double d = w[i].th[0] * f0;
@@ -506,7 +514,7 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
     } else if (pol->router == KVRO_ROUTE_STATIC_LINEAR) {   // A17
       double bs = 0.0;
       for (uint32_t i = 0; i < W; ++i) {
-        double x = (double)(tr->block_tokens * m[i]);
+        double x = (double)(tr->block_tokens * mt[i]);
         double s = (pol->w_load * (double)w[i].fifo.size()) - (pol->w_hit * (x / (double)q));
         if (i == 0 || s < bs) { bs = s; best = i; }
       }
@@ -522,7 +530,7 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
           if (w[i].fifo.size() < w[best].fifo.size()) best = i;
       } else {
         for (uint32_t i = 1; i < W; ++i)
-          if (m[i] > m[best]) best = i;
+          if (mt[i] > mt[best]) best = i;
       }
     } else if (pol->router == KVRO_ROUTE_ROUND_ROBIN) {
       best = j % W;
@@ -557,6 +565,10 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
       if (it == v.end()) return {UINT64_MAX, 0};
       return {*it, depth_of[id]};
     };
+    if (pol->tracker_lag) {   // the tracker will still see this cache at the next query
+      prev_cache = xs.cache;
+      prev_worker = best;
+    }
     update_cache(xs.cache, Hj, n_in + n_out, ux);
     if (ux.invariant_violation) return 9;
     out->inserted_blocks += ux.inserted;

@@ -64,6 +64,8 @@ typedef struct {
   double tau;
   double w_hit, w_load;
   double rls_p0;                  /* LBGR_RLS: initial covariance P = rls_p0 * I */
+  uint32_t tracker_lag;           /* A29: 1 = the router does not yet see the previous query's update */
+  uint32_t tracker_grain;         /* A29: the router sees grain * floor(m / grain) matched blocks (>= 1) */
 } kvro_policy;
 
 typedef struct {

@@ -463,3 +463,43 @@ def test_p23_rls_step_is_weighted_least_squares(oracle_mod, lam):
     assert np.allclose(th, ref, rtol=1e-7, atol=1e-9), (th, ref)
     # P starts at 1e6*I: the first steps cancel ~6 digits, later ones amplify by 1/lam
     assert np.allclose(P, np.linalg.inv(A), rtol=1e-4, atol=1e-10)
+
+
+# -------------------------------------------------------------------------- P24
+def _record_run(oracle_mod, tr, W, B, pol, key=5):
+    cfg = oracle_mod.OracleConfig(W=W, capacity_blocks=B)
+    r = oracle_mod.run(cfg, tr, pol, key, record=True)
+    assert r.rc == 0
+    return r
+
+
+def test_p24_tracker_lag_hand_example(oracle_mod):
+    """App. E: the global tracker can be stale.  Reading A29 with
+    tracker_lag = 1: the router has not yet seen the previous query's update.
+    Two workers, STATIC router (w_load = w_hit = 1), the same 3-block path twice
+    (both arrive at t = 0, so query 0 is still pending at query 1):
+      live view:  worker 0 scores 1*1 - 1*1 = 0, worker 1 scores 0 -> tie -> worker 0, full hit;
+      lagged:     worker 0 scores 1*1 - 0   = 1, worker 1 scores 0 -> worker 1, no hit."""
+    tr = wl.from_paths([[11, 12, 13], [11, 12, 13]])
+    base = dict(router=oracle_mod.ROUTE_STATIC_LINEAR, w_hit=1.0, w_load=1.0, eviction=0)
+    live = _record_run(oracle_mod, tr, 2, 8, oracle_mod.OraclePolicy(**base))
+    lag = _record_run(oracle_mod, tr, 2, 8, oracle_mod.OraclePolicy(tracker_lag=1, **base))
+    assert list(live.records["worker"]) == [0, 0] and list(lag.records["worker"]) == [0, 1]
+    assert list(live.records["hit_tokens"]) == [0, 3 * 16] and list(lag.records["hit_tokens"]) == [0, 0]
+
+
+def test_p24_tracker_grain_reduces_to_no_hit_term(oracle_mod):
+    """A29 grain larger than every path: the tracker sees no hits, so STATIC with
+    w_hit = 1 routes exactly like STATIC with w_hit = 0 and an exact tracker;
+    grain = 1, lag = 0 is the default replay bit for bit."""
+    tr = wl.gsp(12, 8, 0.5, seed=0x24, W=4)
+    big = max(int(tr.n_in_blocks.max()) + 1, 2)
+    a = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy(
+        router=oracle_mod.ROUTE_STATIC_LINEAR, w_hit=1.0, tracker_grain=big))
+    b = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy(
+        router=oracle_mod.ROUTE_STATIC_LINEAR, w_hit=0.0))
+    assert np.array_equal(a.records["worker"], b.records["worker"])
+    assert a.result["decision_digest"] == b.result["decision_digest"]
+    c = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy(tracker_grain=1, tracker_lag=0))
+    d = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy())
+    assert c.result["decision_digest"] == d.result["decision_digest"]
