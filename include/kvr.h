@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 2u   /* 2: KVR_EVICT_OPT, next-use index, KVR_ROUTE_LBGR_RLS + rls_p0 */
+#define KVR_ABI_VERSION 3u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain */
 
 typedef int32_t kvr_status;
 enum {
@@ -152,6 +152,10 @@ typedef struct {
   double tau;                                     /* THRESHOLD */
   double w_hit, w_load;                           /* STATIC_LINEAR */
   double rls_p0;                                  /* LBGR_RLS: initial covariance scale (> 0) */
+  uint32_t tracker_lag;    /* App. E / reading A29: 1 = the router's hit estimate h~ does not
+                              yet include the previous query's cache update (needs B <= 1024) */
+  uint32_t tracker_grain;  /* A29: the router sees grain*floor(m/grain) matched blocks (>= 1);
+                              service times (Eq. 1) always use the true h */
 } kvr_policy;
 
 typedef struct {

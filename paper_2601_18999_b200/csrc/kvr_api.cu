@@ -46,6 +46,8 @@ bool policy_ok(const kvr_policy& p, std::string* why) {
   if (p.eviction > KVR_EVICT_OPT) return bad("eviction must be LRU(0), RLT(1) or OPT(2)");
   if (p.rlt_fallback > KVR_RLT_LRU_MARKED) return bad("rlt_fallback must be 0..2");
   if (p.router > KVR_ROUTE_LBGR_RLS) return bad("router must be 0..5");
+  if (p.tracker_lag > 1) return bad("tracker_lag must be 0 or 1");
+  if (p.tracker_grain < 1) return bad("tracker_grain must be >= 1");
   if (p.router == KVR_ROUTE_LBGR_RLS && !(p.mu > 0.0 && p.mu <= 1.0))
     return bad("LBGR_RLS forgetting factor mu must be in (0, 1]");
   if (p.router == KVR_ROUTE_LBGR_RLS && !(p.rls_p0 > 0.0 && std::isfinite(p.rls_p0)))
@@ -233,6 +235,8 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
     return fail(KVR_ERR_INVALID_ARG, "service model must be finite");
   std::string why;
   if (!policy_ok(cfg->default_policy, &why)) return fail(KVR_ERR_INVALID_ARG, "%s", why.c_str());
+  if (cfg->default_policy.tracker_lag && cfg->capacity_blocks > 1024)
+    return fail(KVR_ERR_UNSUPPORTED, "policy: tracker_lag needs capacity_blocks <= 1024");
   if (cfg->default_policy.eviction == KVR_EVICT_OPT && cfg->W != 1)
     return fail(KVR_ERR_INVALID_ARG, "policy: OPT (offline Belady) is defined for W = 1");
   kvr_sim* s = new kvr_sim;

@@ -1129,7 +1129,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
                         (!rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
                                   pol.rls_p0 < INFINITY)) &&
                         pol.delta_t_ms > 0.0 &&
-                        (!opt || (W == 1 && (tr.nu != nullptr || N == 0)));
+                        (!opt || (W == 1 && (tr.nu != nullptr || N == 0))) &&
+                        pol.tracker_lag <= 1 && pol.tracker_grain >= 1 && (!pol.tracker_lag || defer);
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     const uint32_t Nrun = pol_ok ? N : 0;
 
@@ -1166,6 +1167,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // minus the pending update's victims (register bitmap vbits) if minus_victims.
     auto score_query = [&](const uint64_t* Hq, double aq, uint32_t nq_in, uint32_t qtok,
                            const uint64_t* Hp, uint32_t np, bool minus_victims, uint32_t& m_o,
+                           uint32_t& mview_o,
                            double& score_o, double& Chat_o, double& f0_o, double& f1_o,
                            double& f2_o) {
       KVR_T0(tl);
@@ -1271,46 +1273,62 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       KVR_ACC(1, tl);
 
-      // 2. longest cached prefix over the input (ballot of 32 probes)
-      uint32_t mm = 0;
+      // 2. longest cached prefix over the input (ballot of 32 probes).  With the
+      // tracker lag (App. E, reading A29) a second pass over the old table alone
+      // (before this worker's pending update) gives the router's view.
+      uint32_t mm = 0, mv = 0;
 #pragma unroll 1
-      for (uint32_t base = 0; base < nq_in; base += 32) {
-        const uint32_t d = base + lane;
-        bool hit = false, check = false;
-        uint32_t sidx = 0;
-        if (d < nq_in) {
-          const uint64_t hh = Hq[d];
-          if (d < np && Hp[d] == hh) {
-            hit = true;
-          } else {
-            const Idx s = tbl_find<Idx>(S, tmask, hh);
-            hit = s != NIL;
-            check = minus_victims && hit;
-            sidx = (uint32_t)s;
+      for (uint32_t pass = 0; pass < 2; ++pass) {
+        const bool ovl = pass == 0 && minus_victims;
+        const uint32_t npp = pass == 0 ? np : 0u;
+        uint32_t mx = 0;
+#pragma unroll 1
+        for (uint32_t base = 0; base < nq_in; base += 32) {
+          const uint32_t d = base + lane;
+          bool hit = false, check = false;
+          uint32_t sidx = 0;
+          if (d < nq_in) {
+            const uint64_t hh = Hq[d];
+            if (d < npp && Hp[d] == hh) {
+              hit = true;
+            } else {
+              const Idx s = tbl_find<Idx>(S, tmask, hh);
+              hit = s != NIL;
+              check = ovl && hit;
+              sidx = (uint32_t)s;
+            }
           }
+          if (ovl) {   // found in the old table but evicted by the pending update?
+            const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
+            if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
+          }
+          const uint32_t bal = __ballot_sync(kFull, hit);
+          if (bal == kFull) {
+            mx = base + 32;
+            continue;
+          }
+          mx = base + (__ffs(~bal) - 1);
+          break;
         }
-        if (minus_victims) {   // found in the old table but evicted by the pending update?
-          const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
-          if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
+        if (mx > nq_in) mx = nq_in;
+        if (pass == 1) {
+          mv = mx;
+          break;
         }
-        const uint32_t bal = __ballot_sync(kFull, hit);
-        if (bal == kFull) {
-          mm = base + 32;
-          continue;
-        }
-        mm = base + (__ffs(~bal) - 1);
-        break;
+        mm = mx;
+        mv = mx;
+        if (!(pol.tracker_lag && minus_victims)) break;
       }
-      if (mm > nq_in) mm = nq_in;
+      if (pol.tracker_grain > 1) mv = pol.tracker_grain * (mv / pol.tracker_grain);
       KVR_ACC(2, tl);
 
-      // 3. score (Eq. 4-5, A9)
-      const double x = (double)(bt * mm), y = (double)(qtok - bt * mm);
+      // 3. score (Eq. 4-5, A9) on the tracker's view h~ = bt*mv (= h by default)
+      const double x = (double)(bt * mv), y = (double)(qtok - bt * mv);
       double sc = 0.0, Ch = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0;
       if (lbgr) {
         Ch = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
-        h0 = divtab[mm];            // == x / 1000.0 (x = bt*m)
-        h1 = divtab[nq_in - mm];    // == y / 1000.0 (y = bt*(n_in-m))
+        h0 = divtab[mv];            // == x / 1000.0 (x = bt*m~)
+        h1 = divtab[nq_in - mv];    // == y / 1000.0 (y = bt*(n_in-m~))
         h2 = Pt / 1000.0;
         const double h3 = 1.0;
         double dd = th0 * h0;
@@ -1323,6 +1341,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       KVR_ACC(3, tl);
       m_o = mm;
+      mview_o = mv;
       score_o = sc;
       Chat_o = Ch;
       f0_o = h0;
@@ -1356,12 +1375,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
              (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
         np = ws->n;
       }
-      uint32_t m;
+      uint32_t m, mview;
       double score, Chat, f0, f1, f2;
-      score_query(H, a, n_in, q, Hp, np, overlay, m, score, Chat, f0, f1, f2);
+      score_query(H, a, n_in, q, Hp, np, overlay, m, mview, score, Chat, f0, f1, f2);
       if (lane == 0) {
         ctrl->score[par][w] = score;
-        ctrl->mhit[par][w] = m;
+        ctrl->mhit[par][w] = mview;   // the router's view (THRESHOLD)
         ctrl->npend[par][w] = fn;
         ws->c_probes += min(m + 1, n_in);
       }

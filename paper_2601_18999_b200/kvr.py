@@ -60,7 +60,8 @@ class kvr_policy(C.Structure):
                 ("est_alpha_cached_ms", C.c_double), ("est_alpha_miss_ms", C.c_double),
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
-                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double)]
+                ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double),
+                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32)]
 
 
 class kvr_sim_config(C.Structure):
@@ -74,7 +75,8 @@ POLICY_DTYPE = np.dtype([("eviction", "<u4"), ("rlt_fallback", "<u4"), ("router"
                          ("_pad", "<u4"), ("est_alpha_cached_ms", "<f8"),
                          ("est_alpha_miss_ms", "<f8"), ("rho", "<f8"), ("delta_t_ms", "<f8"),
                          ("mu", "<f8"), ("theta0", "<f8", (4,)), ("tau", "<f8"),
-                         ("w_hit", "<f8"), ("w_load", "<f8"), ("rls_p0", "<f8")])
+                         ("w_hit", "<f8"), ("w_load", "<f8"), ("rls_p0", "<f8"),
+                         ("tracker_lag", "<u4"), ("tracker_grain", "<u4")])
 RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
     "queries", "hit_tokens", "input_tokens", "probes", "inserted_blocks", "evictions",
     "rlt_draws", "rlt_resets", "rlt_fallbacks", "max_pending", "decision_digest")] +
@@ -84,7 +86,7 @@ RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
 RECORD_DTYPE = np.dtype([("worker", "<u4"), ("hit_tokens", "<u4"), ("n_victims", "<u4"),
                          ("_pad", "<u4"), ("ttft_ms", "<f8"), ("latency_ms", "<f8"),
                          ("score", "<f8"), ("victim_offset", "<u8")])
-assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 120
+assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 128
 assert RESULT_DTYPE.itemsize == 144 and RECORD_DTYPE.itemsize == 48
 
 _lib = None
@@ -262,6 +264,8 @@ class Policy:
     w_hit: float = 1.0
     w_load: float = 1.0
     rls_p0: float = 1000.0     # LBGR_RLS initial covariance P = rls_p0 * I
+    tracker_lag: int = 0       # A29: router's h~ lags the previous query's update
+    tracker_grain: int = 1     # A29: router sees whole grains of matched blocks
 
     def c(self) -> kvr_policy:
         p = kvr_policy()

@@ -46,3 +46,36 @@ def test_lbgr_rls_validation(kvr):
                   kvr.policies_array([kvr.Policy(router=kvr.ROUTE_LBGR_RLS, mu=1.5),
                                       kvr.Policy(router=kvr.ROUTE_LBGR_RLS)]))
     assert int(out.results[0]["status"]) == 3 and int(out.results[1]["status"]) == 0
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_tracker_parity(kvr, oracle_mod, W):
+    """Approximate / stale global tracker (App. E, reading A29): the
+    router scores with h~ (1-event lag and/or whole grains) while Eq. 1 uses h."""
+    tr = wl.gsp(24, 12, 0.5, seed=0x90 + W, W=W)
+    pols = []
+    for router in (kvr.ROUTE_LBGR, kvr.ROUTE_STATIC_LINEAR, kvr.ROUTE_THRESHOLD):
+        for lag, grain in ((1, 1), (0, 4), (1, 8)):
+            pols.append(kvr.Policy(router=router, tracker_lag=lag, tracker_grain=grain,
+                                   eviction=1 if grain != 4 else 0))
+    compare(oracle_mod, kvr, tr, W, 512, pols, list(range(31, 31 + len(pols))), record=True)
+
+
+def test_tracker_lag_hand_example(kvr, oracle_mod):
+    tr = wl.from_paths([[11, 12, 13], [11, 12, 13]])
+    pol = dict(router=kvr.ROUTE_STATIC_LINEAR, w_hit=1.0, w_load=1.0, eviction=0)
+    out, _ = compare(oracle_mod, kvr, tr, 2, 8, [kvr.Policy(**pol), kvr.Policy(tracker_lag=1, **pol)],
+                     [5, 5], record=True)
+    assert list(out.records[0]["worker"][:2]) == [0, 0] and list(out.records[1]["worker"][:2]) == [0, 1]
+
+
+def test_tracker_validation(kvr):
+    with pytest.raises(kvr.KvrError):   # the lag reads the deferred-apply overlay (B <= 1024)
+        kvr.Simulator(1, 2048, policy=kvr.Policy(tracker_lag=1))
+    with pytest.raises(kvr.KvrError):
+        kvr.Simulator(2, 64, policy=kvr.Policy(tracker_grain=0))
+    tr = wl.adv(2048, 4, 1, seed=2)
+    sim = kvr.Simulator(1, 2048)
+    out = sim.run(kvr.DeviceTrace(tr), np.array([1, 2], np.uint64),
+                  kvr.policies_array([kvr.Policy(tracker_lag=1), kvr.Policy()]))
+    assert int(out.results[0]["status"]) == 3 and int(out.results[1]["status"]) == 0
