@@ -1,6 +1,7 @@
 """Router variants on the GPU: the two readings of LBGR's "learning
 rate 0.992" (A8 NLMS step vs A8b RLS forgetting factor), the decay-interval
-ablation of P:791-795 (Delta t = 10..80 ms and no decay), and the baselines, on
+ablation of P:791-795 (Delta t = 10..80 ms and no decay), the approximate / stale
+global tracker (§8f #3, App. E, reading A29), and the baselines, on
 config 2's GSP shape (W = 8) and config 3's drifting trace (W = 16).  RLT eviction;
 `trials` seeded trials per cell, all cells in one multi-trial launch.
 
@@ -35,7 +36,14 @@ CELLS = [("LBGR NLMS (A8), dt=10", dict(router=ROUTE_LBGR, delta_t_ms=10.0)),
          ("LBGR RLS (A8b), dt=40", dict(router=ROUTE_LBGR_RLS, delta_t_ms=40.0)),
          ("LBGR RLS (A8b), dt=80", dict(router=ROUTE_LBGR_RLS, delta_t_ms=80.0)),
          ("LBGR RLS (A8b), no decay", dict(router=ROUTE_LBGR_RLS, delta_t_ms=math.inf)),
+         ("LBGR RLS dt=20, tracker lag 1", dict(router=ROUTE_LBGR_RLS, tracker_lag=1)),
+         ("LBGR RLS dt=20, tracker grain 8", dict(router=ROUTE_LBGR_RLS, tracker_grain=8)),
+         ("LBGR RLS dt=20, tracker grain 32", dict(router=ROUTE_LBGR_RLS, tracker_grain=32)),
+         ("LBGR RLS dt=20, lag 1 + grain 32", dict(router=ROUTE_LBGR_RLS, tracker_lag=1, tracker_grain=32)),
+         ("LBGR NLMS dt=40, tracker lag 1", dict(router=ROUTE_LBGR, delta_t_ms=40.0, tracker_lag=1)),
+         ("LBGR NLMS dt=40, tracker grain 32", dict(router=ROUTE_LBGR, delta_t_ms=40.0, tracker_grain=32)),
          ("Static linear (A17)", dict(router=ROUTE_STATIC_LINEAR)),
+         ("Static linear, tracker grain 32", dict(router=ROUTE_STATIC_LINEAR, tracker_grain=32)),
          ("Threshold / cache-aware (A16)", dict(router=ROUTE_THRESHOLD)),
          ("Round robin", dict(router=ROUTE_ROUND_ROBIN)),
          ("Random", dict(router=ROUTE_RANDOM))]
