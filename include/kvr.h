@@ -37,7 +37,8 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 3u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain */
+#define KVR_ABI_VERSION 4u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
+                                4: kvr_sim_config.extended_policies */
 
 typedef int32_t kvr_status;
 enum {
@@ -167,6 +168,11 @@ typedef struct {
   uint32_t record_trials;          /* the first R trials emit per-query records + victim logs */
   uint32_t latency_hist_bins;      /* 0, or 1..256 log-bucket bins (4 per octave, bin 0 = <1 ms) */
   uint32_t force_tier;             /* 0 auto, 1 shared-memory tables, 2 global-memory tables */
+  uint32_t extended_policies;      /* 1: per-trial policies may use OPT / LBGR_RLS / tracker bias
+                                      (runs the kernel instantiation that carries them; implied
+                                      when default_policy uses one).  0: such a per-trial policy
+                                      gets KVR_TRIAL_BAD_POLICY; the lean instantiation runs. */
+  uint32_t _pad;
 } kvr_sim_config;
 
 typedef struct kvr_sim kvr_sim;

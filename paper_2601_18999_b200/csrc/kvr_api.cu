@@ -40,6 +40,16 @@ kvr_status cuda_fail(cudaError_t e, const char* what) {
   return fail(KVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// policies that need the extended kernel instantiation
+bool policy_extended(const kvr_policy& p) {
+  return p.eviction == KVR_EVICT_OPT || p.router == KVR_ROUTE_LBGR_RLS || p.tracker_lag != 0 ||
+         p.tracker_grain != 1;
+}
+
+bool sim_extended(const kvr_sim_config& c) {
+  return c.extended_policies != 0 || policy_extended(c.default_policy);
+}
+
 bool policy_ok(const kvr_policy& p, std::string* why) {
   char b[256];
   auto bad = [&](const char* s) { snprintf(b, sizeof b, "policy: %s", s); *why = b; return false; };
@@ -103,7 +113,7 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan
   pl->tier = tier;
   pl->lay = tier == 1 ? l16 : l32;
   pl->smem = tier == 1 ? smem1 : base;
-  cudaError_t e = kvr::replay_attrs(tier, pl->smem, &pl->ctas_per_sm, c.W);
+  cudaError_t e = kvr::replay_attrs(tier, pl->smem, &pl->ctas_per_sm, c.W, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
@@ -229,6 +239,7 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
   if (cfg->latency_hist_bins > kvr::kMaxHistBins)
     return fail(KVR_ERR_INVALID_ARG, "latency_hist_bins must be <= 256");
   if (cfg->force_tier > 2) return fail(KVR_ERR_INVALID_ARG, "force_tier must be 0, 1 or 2");
+  if (cfg->extended_policies > 1) return fail(KVR_ERR_INVALID_ARG, "extended_policies must be 0 or 1");
   const kvr_service_model& t = cfg->truth;
   if (!std::isfinite(t.alpha_cached_ms) || !std::isfinite(t.alpha_miss_ms) ||
       !std::isfinite(t.out_ms_per_token))
@@ -358,7 +369,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);
   if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
-  e = kvr::launch_replay(pl.tier, p, pl.grid, pl.smem, s);
+  e = kvr::launch_replay(pl.tier, p, pl.grid, pl.smem, s, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   return KVR_OK;
 }

@@ -167,9 +167,10 @@ inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
 cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, uint32_t* scratch,
                         cudaStream_t s);
 // tier 1 = tables in shared memory (u16 slot ids), 2 = tables in global memory (u32 slot ids)
-cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W);
+// ext: the instantiation with the extended policies (OPT, LBGR_RLS, tracker bias)
+cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W, bool ext);
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
-                          cudaStream_t s);
+                          cudaStream_t s, bool ext);
 // next-use index for the offline OPT analysis (kvr_nextuse.cu)
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);
 cudaError_t build_next_use(const QueryHdr* hdr, uint32_t N, const uint64_t* hash, uint64_t n,

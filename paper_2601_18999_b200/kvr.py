@@ -68,7 +68,8 @@ class kvr_sim_config(C.Structure):
     _fields_ = [("W", C.c_uint32), ("capacity_blocks", C.c_uint32),
                 ("truth", kvr_service_model), ("default_policy", kvr_policy),
                 ("pending_ring", C.c_uint32), ("record_trials", C.c_uint32),
-                ("latency_hist_bins", C.c_uint32), ("force_tier", C.c_uint32)]
+                ("latency_hist_bins", C.c_uint32), ("force_tier", C.c_uint32),
+                ("extended_policies", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 POLICY_DTYPE = np.dtype([("eviction", "<u4"), ("rlt_fallback", "<u4"), ("router", "<u4"),
@@ -287,6 +288,13 @@ class Policy:
         return r
 
 
+def policies_extended(arr: np.ndarray) -> bool:
+    """True if any policy needs the extended kernel (OPT, LBGR_RLS, tracker bias)."""
+    a = np.asarray(arr).view(POLICY_DTYPE)
+    return bool(np.any((a["eviction"] == EVICT_OPT) | (a["router"] == ROUTE_LBGR_RLS) |
+                       (a["tracker_lag"] != 0) | (a["tracker_grain"] != 1)))
+
+
 def policies_array(pols: Sequence[Policy]) -> np.ndarray:
     a = np.zeros(len(pols), dtype=POLICY_DTYPE)
     for i, p in enumerate(pols):
@@ -400,7 +408,8 @@ class Simulator:
     def __init__(self, W: int, capacity_blocks: int, policy: Optional[Policy] = None,
                  alpha_cached_ms: float = 0.0, alpha_miss_ms: float = 1.0,
                  out_ms_per_token: float = 20.0, pending_ring: int = 256,
-                 record_trials: int = 0, latency_hist_bins: int = 0, force_tier: int = 0):
+                 record_trials: int = 0, latency_hist_bins: int = 0, force_tier: int = 0,
+                 extended_policies: bool = False):
         cfg = kvr_sim_config()
         cfg.W, cfg.capacity_blocks = W, capacity_blocks
         cfg.truth.alpha_cached_ms = alpha_cached_ms
@@ -409,9 +418,20 @@ class Simulator:
         cfg.default_policy = (policy or Policy()).c()
         cfg.pending_ring, cfg.record_trials = pending_ring, record_trials
         cfg.latency_hist_bins, cfg.force_tier = latency_hist_bins, force_tier
+        cfg.extended_policies = 1 if extended_policies else 0
         self.cfg = cfg
         self.handle = kvr_sim_create(cfg)
         self._ws = None
+
+    def _need_extended(self, policies: Optional[np.ndarray]):
+        """Switch to the kernel instantiation with the extended policies when a
+        per-trial policy array uses one (OPT, LBGR_RLS, tracker bias)."""
+        if policies is None or self.cfg.extended_policies or not policies_extended(policies):
+            return
+        self.cfg.extended_policies = 1
+        old = self.handle
+        self.handle = kvr_sim_create(self.cfg)
+        kvr_sim_destroy(old)
 
     def plan(self, max_path_blocks: int):
         return kvr_sim_plan(self.handle, max_path_blocks)
@@ -432,6 +452,7 @@ class Simulator:
             traces = [traces]
         dev = traces[0].device
         n = len(keys)
+        self._need_extended(policies)
         b = buffers if buffers is not None else self.alloc(traces, n, victims_cap, dev)
         if policies is not None:
             b["policies"].copy_(torch.from_numpy(np.ascontiguousarray(policies).view(np.uint8)))

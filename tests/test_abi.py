@@ -35,14 +35,14 @@ def test_header_declares_the_north_star_entry_points():
 def test_library_exports_every_declared_symbol(libkvr):
     for name in _declared():
         assert hasattr(libkvr, name), name
-    assert libkvr.kvr_abi_version() == 3
+    assert libkvr.kvr_abi_version() == 4
 
 
 def test_struct_sizes_match_header(libkvr):
     from paper_2601_18999_b200 import kvr
     assert C.sizeof(kvr.kvr_policy) == 128
     assert C.sizeof(kvr.kvr_trace_desc) == 72
-    assert C.sizeof(kvr.kvr_sim_config) == 4 + 4 + 24 + 128 + 16
+    assert C.sizeof(kvr.kvr_sim_config) == 4 + 4 + 24 + 128 + 16 + 8
     assert kvr.RESULT_DTYPE.itemsize == 144 and kvr.RECORD_DTYPE.itemsize == 48
 
 

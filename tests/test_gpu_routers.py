@@ -79,3 +79,21 @@ def test_tracker_validation(kvr):
     out = sim.run(kvr.DeviceTrace(tr), np.array([1, 2], np.uint64),
                   kvr.policies_array([kvr.Policy(tracker_lag=1), kvr.Policy()]))
     assert int(out.results[0]["status"]) == 3 and int(out.results[1]["status"]) == 0
+
+
+def test_lean_kernel_refuses_extended_policies(kvr):
+    """Without kvr_sim_config.extended_policies the lean kernel instantiation runs and an
+    extended per-trial policy is refused (status 3) instead of silently misbehaving."""
+    import torch
+    tr = wl.gsp(4, 4, 0.5, seed=3, W=2)
+    dt = kvr.DeviceTrace(tr)
+    sim = kvr.Simulator(2, 512)
+    pols = kvr.policies_array([kvr.Policy(router=kvr.ROUTE_LBGR_RLS), kvr.Policy(tracker_grain=4),
+                               kvr.Policy()])
+    b = sim.alloc([dt], 3, 0, dt.device)
+    b["keys"].copy_(torch.arange(1, 4, dtype=torch.int64))
+    b["policies"].copy_(torch.from_numpy(pols.view(np.uint8)))
+    sim.launch([dt], 3, b, with_policies=True)
+    out = sim.collect(b, 3)
+    assert list(out.results["status"]) == [3, 3, 0]
+    assert not sim.cfg.extended_policies
