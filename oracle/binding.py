@@ -54,7 +54,8 @@ class _Config(C.Structure):
     _fields_ = [("W", C.c_uint32), ("capacity_blocks", C.c_uint32),
                 ("alpha_cached_ms", C.c_double), ("alpha_miss_ms", C.c_double),
                 ("out_ms_per_token", C.c_double),
-                ("pending_ring", C.c_uint32), ("latency_hist_bins", C.c_uint32)]
+                ("pending_ring", C.c_uint32), ("latency_hist_bins", C.c_uint32),
+                ("batch_slots", C.c_uint32), ("_pad", C.c_uint32)]
 
 
 class _Result(C.Structure):
@@ -141,6 +142,7 @@ class OracleConfig:
     out_ms_per_token: float = 20.0
     pending_ring: int = 256
     latency_hist_bins: int = 0
+    batch_slots: int = 0       # 0: beta = 1 model (A3/A12); >= 1: continuous batching (A30-A35)
 
     def _c(self) -> _Config:
         c = _Config()
@@ -148,6 +150,7 @@ class OracleConfig:
         c.alpha_cached_ms, c.alpha_miss_ms = self.alpha_cached_ms, self.alpha_miss_ms
         c.out_ms_per_token = self.out_ms_per_token
         c.pending_ring, c.latency_hist_bins = self.pending_ring, self.latency_hist_bins
+        c.batch_slots = self.batch_slots
         return c
 
 

@@ -115,6 +115,7 @@ struct Node {
   uint32_t slot;       // physical slot (A6 slot rule)
   uint64_t stamp;      // index j of the last query that touched it (A7)
   uint32_t depth;      // position along the path, 1-based
+  uint32_t pin = 0;    // in-flight paths holding it (continuous batching, A30)
 };
 
 struct Cache {
@@ -133,6 +134,10 @@ struct UpdateCtx {
   std::vector<uint64_t> victims;
   std::vector<uint8_t>* miss_flags = nullptr;
   bool invariant_violation = false;
+  // continuous batching (A30): the path is pinned block by block as it is
+  // accessed, and only unpinned leaves are eviction candidates
+  bool pinning = false;
+  bool admission_fail = false;  // full cache and no unpinned leaf
 };
 
 // (stamp, -depth) order of Leaf-LRU (A7): true if a is less recently used.
@@ -164,6 +169,7 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
     auto it = C.S.find(t);
     if (it != C.S.end()) {
       it->second.stamp = x.j;
+      if (x.pinning) it->second.pin++;
       x.hits++;
       if (x.miss_flags) x.miss_flags->push_back(0);
       continue;
@@ -179,7 +185,12 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
         // always a leaf and never on Gamma_j (A7).
         const Node* best = nullptr;
         for (auto& kv : C.S) {
-          if (kv.second.stamp >= x.j) continue;
+          if (x.pinning) {
+            // A30/A33: least recently used UNPINNED leaf (the current path is pinned)
+            if (kv.second.pin != 0 || kv.second.nchild != 0) continue;
+          } else if (kv.second.stamp >= x.j) {
+            continue;
+          }
           if (!best || lru_less(kv.second, *best)) { best = &kv.second; v = kv.first; found = true; }
         }
         if (found && C.S[v].nchild != 0) x.invariant_violation = true;
@@ -189,6 +200,7 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
         for (auto& kv : C.S) {
           if (kv.second.nchild != 0) continue;
           if (has_p && kv.first == p) continue;
+          if (kv.second.pin != 0) continue;          // A30: in-flight blocks stay
           if (C.T.count(kv.first)) continue;
           U.push_back({kv.second.slot, kv.first});
         }
@@ -206,6 +218,7 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
             for (auto& kv : C.S) {
               if (kv.second.nchild != 0) continue;
               if (has_p && kv.first == p) continue;
+              if (kv.second.pin != 0) continue;
               if (!best || lru_less(kv.second, *best)) { best = &kv.second; v = kv.first; found = true; }
             }
             no_draw = true;
@@ -213,6 +226,7 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
             for (auto& kv : C.S) {
               if (kv.second.nchild != 0) continue;
               if (has_p && kv.first == p) continue;
+              if (kv.second.pin != 0) continue;
               U.push_back({kv.second.slot, kv.first});
             }
           }
@@ -243,7 +257,11 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
           if (better) { best = &kv.second; bnu = nu; v = kv.first; found = true; }
         }
       }
-      if (!found) { x.invariant_violation = true; return; }
+      if (!found) {
+        if (x.pinning) x.admission_fail = true;   // every leaf is in flight
+        else x.invariant_violation = true;
+        return;
+      }
       // Evict(S, v)
       Node nv = C.S[v];
       if (nv.nchild != 0) x.invariant_violation = true;
@@ -260,6 +278,7 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
     Node nn;
     nn.parent = p; nn.has_parent = has_p; nn.nchild = 0; nn.slot = slot;
     nn.stamp = x.j; nn.depth = d + 1;
+    nn.pin = x.pinning ? 1 : 0;
     C.S[t] = nn;
     if (has_p) C.S[p].nchild++;
     x.inserted++;
@@ -352,6 +371,324 @@ struct Worker {
   uint64_t k = 0, e = 0;
 };
 
+
+// ---------------------------------------------------------------------------
+// Continuous batching, beta >= 1 ("the system handles beta distinct
+// queries concurrently"; SPEC simulator S:499-549; readings A30-A35 in DESIGN.md).
+// Per worker: beta batch slots; assigned queries wait FIFO until a slot frees;
+// UpdateCache (Eq. 3) runs at DEQUEUE and gives the true h; in-flight paths are
+// pinned (SPEC access_path S:133-141) until their completion.
+// ---------------------------------------------------------------------------
+struct BRec {            // one assigned query (waiting, then in flight)
+  uint32_t j;
+  double a, Ehat, phi0, phi1, phi2, Chat;
+  uint64_t ka;
+  double c;              // completion time, set at dequeue
+};
+
+struct BWorker {
+  Cache cache;
+  double P = 0.0, F = 0.0, Pt = 0.0;
+  double th[4] = {0, 0, 0, 0};
+  double Pm[4][4] = {};
+  std::deque<BRec> waiting;     // FIFO (A30)
+  std::vector<BRec> inflight;   // <= beta
+  uint64_t k = 0, e = 0;
+  double sum_lat = 0.0, sum_ttft = 0.0;   // per-worker partial sums (A34)
+  uint64_t vcur = 0;                       // per-worker victim-log cursor (A34)
+};
+
+int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* pol,
+                uint64_t K, const std::vector<uint64_t>& H, kvro_result* out,
+                kvro_query_record* records, uint64_t* victims, uint64_t victims_cap,
+                uint32_t* hist, int check_invariants) {
+  const uint32_t W = cfg->W, B = cfg->capacity_blocks, beta = cfg->batch_slots;
+  std::vector<BWorker> w(W);
+  const bool rls = pol->router == KVRO_ROUTE_LBGR_RLS;
+  const bool lbgr = pol->router == KVRO_ROUTE_LBGR || rls;
+  for (auto& x : w) {
+    x.cache.B = B;
+    for (int k = 0; k < 4; ++k) x.th[k] = pol->theta0[k];
+    if (rls)
+      for (int k = 0; k < 4; ++k) x.Pm[k][k] = pol->rls_p0;
+  }
+  const double rho = pol->rho, dt = pol->delta_t_ms, mu = pol->mu;
+  const uint64_t vshare = (victims && W) ? victims_cap / W : 0;   // A34: per-worker sub-share
+  uint64_t D = K;
+  bool vlog_full = false, admission = false, violation = false;
+
+  // Dequeue r on worker i at time s: UpdateCache with pinning, true h, Eq. 1 truth.
+  auto dequeue = [&](uint32_t i, BRec r, double s) {
+    BWorker& x = w[i];
+    const uint32_t j = r.j;
+    const uint32_t n_in = tr->n_in_blocks[j], n_out = tr->n_out_blocks[j];
+    const uint32_t q = tr->block_tokens * n_in;
+    const uint64_t* Hj = H.data() + tr->block_offsets[j];
+    const uint32_t m = match_prefix(x.cache, Hj, n_in);      // true h at dequeue (A30)
+    UpdateCtx ux;
+    ux.eviction = pol->eviction;
+    ux.fallback = pol->rlt_fallback;
+    ux.j = j;                                                // A33: per-worker dequeue order
+    ux.pinning = true;
+    ux.choose = [&](uint64_t nU) -> uint64_t {
+      uint64_t rr = philox_r64(K, x.e, i, 1);
+      x.e++;
+      return pick(rr, nU);
+    };
+    update_cache(x.cache, Hj, n_in + n_out, ux);
+    if (ux.invariant_violation) { violation = true; return; }
+    if (ux.admission_fail) { admission = true; return; }
+    out->inserted_blocks += ux.inserted;
+    out->evictions += ux.evictions;
+    out->rlt_draws += ux.draws;
+    out->rlt_resets += ux.resets;
+    out->rlt_fallbacks += ux.fallbacks;
+    const uint32_t h = tr->block_tokens * m;
+    const double xh = (double)h, yh = (double)(q - h);
+    const double pre = (cfg->alpha_cached_ms * xh) + (cfg->alpha_miss_ms * yh);   // Eq. 1
+    const double O = cfg->out_ms_per_token * (double)tr->out_tokens[j];
+    const double cost = pre + O;
+    const double ttft = (s + pre) - r.a;                    // A20 (prefill done - arrival)
+    const double comp = s + cost;
+    const double lat = comp - r.a;
+    r.c = comp;
+    x.inflight.push_back(r);
+    if (comp > x.F) x.F = comp;
+    x.P = x.P + cost;                                        // Eq. 2
+    out->hit_tokens += h;
+    out->input_tokens += q;
+    x.sum_lat = x.sum_lat + lat;
+    x.sum_ttft = x.sum_ttft + ttft;
+    if (lat > out->max_latency_ms) out->max_latency_ms = lat;
+    out->queries++;
+    uint64_t V = 0;
+    for (size_t k = 0; k < ux.victims.size(); ++k)
+      V ^= fmix64(ux.victims[k] ^ ((uint64_t)(k + 1) * K_POS));
+    uint64_t T = fmix64(K ^ (uint64_t)j);
+    T = fmix64(T ^ (uint64_t)i);
+    T = fmix64(T ^ (uint64_t)m);
+    T = fmix64(T ^ (uint64_t)ux.victims.size());
+    T = fmix64(T ^ V);
+    D += T;
+    if (records) {
+      kvro_query_record& R = records[j];
+      R.worker = i; R.hit_tokens = h; R.n_victims = (uint32_t)ux.victims.size(); R._pad = 0;
+      R.ttft_ms = ttft; R.latency_ms = lat;
+      R.victim_offset = (uint64_t)i * vshare + x.vcur;
+      for (uint64_t v : ux.victims) {
+        if (victims && x.vcur < vshare) victims[(uint64_t)i * vshare + x.vcur] = v;
+        else if (victims) vlog_full = true;
+        x.vcur++;
+      }
+    }
+    if (hist && cfg->latency_hist_bins) hist[hist_bin(lat, cfg->latency_hist_bins)]++;
+  };
+
+  // Completion of the earliest in-flight query (ties: lower j, A31): LBGR
+  // OnlineUpdate + ReleaseLoad exactly as in the beta = 1 model, unpin Gamma_j,
+  // free the slot and start the head of the waiting FIFO at the same instant.
+  auto complete_next = [&](uint32_t i) {
+    BWorker& x = w[i];
+    size_t b = 0;
+    for (size_t u = 1; u < x.inflight.size(); ++u)
+      if (x.inflight[u].c < x.inflight[b].c ||
+          (x.inflight[u].c == x.inflight[b].c && x.inflight[u].j < x.inflight[b].j))
+        b = u;
+    BRec r = x.inflight[b];
+    x.inflight.erase(x.inflight.begin() + (long)b);
+    if (lbgr && !rls) {
+      double E = r.c - r.a;
+      double res = E - r.Ehat;
+      double phi3 = 1.0;
+      double s2 = r.phi0 * r.phi0;
+      s2 = s2 + r.phi1 * r.phi1;
+      s2 = s2 + r.phi2 * r.phi2;
+      s2 = s2 + phi3 * phi3;
+      double g = (mu * res) / (1.0 + s2);
+      x.th[0] = x.th[0] + g * r.phi0;
+      x.th[1] = x.th[1] + g * r.phi1;
+      x.th[2] = x.th[2] + g * r.phi2;
+      x.th[3] = x.th[3] + g * phi3;
+    } else if (rls) {
+      const double phi[4] = {r.phi0, r.phi1, r.phi2, 1.0};
+      rls_step(x.Pm, x.th, phi, (r.c - r.a) - r.Ehat, mu);
+    }
+    if (lbgr) {
+      uint64_t kap = x.k - r.ka;
+      double pw = 1.0, bb = rho;
+      while (kap) {
+        if (kap & 1) pw = pw * bb;
+        bb = bb * bb;
+        kap >>= 1;
+      }
+      x.Pt = x.Pt - r.Chat * pw;
+      if (x.Pt < 0.0) x.Pt = 0.0;
+    }
+    const uint64_t* Hj = H.data() + tr->block_offsets[r.j];
+    const uint32_t n = tr->n_in_blocks[r.j] + tr->n_out_blocks[r.j];
+    for (uint32_t d = 0; d < n; ++d) {                       // release_path
+      auto it = x.cache.S.find(Hj[d]);
+      if (it == x.cache.S.end() || it->second.pin == 0) { violation = true; return; }
+      it->second.pin--;
+    }
+    while (x.inflight.size() < beta && !x.waiting.empty() && !admission && !violation) {
+      BRec h = x.waiting.front();
+      x.waiting.pop_front();
+      dequeue(i, h, r.c);
+    }
+  };
+
+  auto next_completion = [&](const BWorker& x) -> double {
+    double c = INFINITY;
+    for (const BRec& r : x.inflight) if (r.c < c) c = r.c;
+    return c;
+  };
+
+  std::vector<uint32_t> m(W);
+  std::vector<double> Ehat(W), Chat(W), phi0(W), phi1(W), phi2(W);
+  for (uint32_t j = 0; j < tr->n_queries && !admission && !violation; ++j) {
+    const double t = tr->arrival_ms[j];
+    const uint32_t n_in = tr->n_in_blocks[j];
+    const uint32_t q = tr->block_tokens * n_in;
+    const uint64_t* Hj = H.data() + tr->block_offsets[j];
+
+    // 1. catch-up per worker: ticks, completions (and the dequeues they
+    //    trigger) in time order; tick < completion at equal times (A31)
+    for (uint32_t i = 0; i < W && !admission && !violation; ++i) {
+      BWorker& x = w[i];
+      for (;;) {
+        const double c = next_completion(x);
+        if (lbgr) {
+          double tau = (double)(x.k + 1) * dt;
+          if (tau <= t && tau <= c) {
+            x.Pt = rho * x.Pt;
+            x.k++;
+            continue;
+          }
+        }
+        if (c <= t) {
+          complete_next(i);
+          if (admission || violation) break;
+          continue;
+        }
+        break;
+      }
+    }
+    if (admission || violation) break;
+
+    // 2. match on the cache as it stands at a_j (A32)
+    for (uint32_t i = 0; i < W; ++i) {
+      m[i] = match_prefix(w[i].cache, Hj, n_in);
+      out->probes += std::min<uint64_t>(m[i] + 1, n_in);
+    }
+    auto pending = [&](uint32_t i) -> size_t { return w[i].waiting.size() + w[i].inflight.size(); };
+
+    // 3. score + argmin (lowest index on ties, A15); pending = waiting + in flight (A32)
+    uint32_t best = 0;
+    double score_best = 0.0;
+    if (lbgr) {
+      for (uint32_t i = 0; i < W; ++i) {
+        double x = (double)(tr->block_tokens * m[i]);
+        double y = (double)(q - tr->block_tokens * m[i]);
+        double C = (pol->est_alpha_cached_ms * x) + (pol->est_alpha_miss_ms * y);   // Eq. 5
+        double f0 = x / 1000.0, f1 = y / 1000.0, f2 = w[i].Pt / 1000.0, f3 = 1.0;  // A9
+        double d = w[i].th[0] * f0;
+        d = d + w[i].th[1] * f1;
+        d = d + w[i].th[2] * f2;
+        d = d + w[i].th[3] * f3;
+        Ehat[i] = (C + w[i].Pt) + d;                                               // Eq. 4
+        Chat[i] = C; phi0[i] = f0; phi1[i] = f1; phi2[i] = f2;
+      }
+      for (uint32_t i = 1; i < W; ++i)
+        if (Ehat[i] < Ehat[best]) best = i;
+      score_best = Ehat[best];
+    } else if (pol->router == KVRO_ROUTE_STATIC_LINEAR) {
+      double bs = 0.0;
+      for (uint32_t i = 0; i < W; ++i) {
+        double x = (double)(tr->block_tokens * m[i]);
+        double s = (pol->w_load * (double)pending(i)) - (pol->w_hit * (x / (double)q));
+        if (i == 0 || s < bs) { bs = s; best = i; }
+      }
+      score_best = bs;
+    } else if (pol->router == KVRO_ROUTE_THRESHOLD) {
+      size_t mx = pending(0), mn = pending(0);
+      for (uint32_t i = 1; i < W; ++i) {
+        mx = std::max(mx, pending(i));
+        mn = std::min(mn, pending(i));
+      }
+      if ((double)mx > pol->tau * (double)std::max<size_t>(1, mn)) {
+        for (uint32_t i = 1; i < W; ++i)
+          if (pending(i) < pending(best)) best = i;
+      } else {
+        for (uint32_t i = 1; i < W; ++i)
+          if (m[i] > m[best]) best = i;
+      }
+    } else if (pol->router == KVRO_ROUTE_ROUND_ROBIN) {
+      best = j % W;
+    } else {
+      best = (uint32_t)pick(philox_r64(K, j, 0xFFFFFFFFu, 2), W);
+    }
+    BWorker& xs = w[best];
+    if (cfg->pending_ring && xs.waiting.size() >= cfg->pending_ring) {
+      out->status = KVRO_TRIAL_RING_OVERFLOW;
+      break;
+    }
+
+    // 4. assignment: Eq. 6 at assignment, enqueue, start now if a slot is free
+    BRec r;
+    r.j = j; r.a = t; r.c = 0.0;
+    r.Ehat = lbgr ? Ehat[best] : 0.0;
+    r.phi0 = lbgr ? phi0[best] : 0.0;
+    r.phi1 = lbgr ? phi1[best] : 0.0;
+    r.phi2 = lbgr ? phi2[best] : 0.0;
+    r.Chat = lbgr ? Chat[best] : 0.0;
+    r.ka = xs.k;
+    if (lbgr) xs.Pt = xs.Pt + Chat[best];
+    if (records) records[j].score = score_best;
+    if (xs.inflight.size() < beta) dequeue(best, r, t);   // the FIFO is empty here (A30)
+    else xs.waiting.push_back(r);
+    if (pending(best) > out->max_pending) out->max_pending = pending(best);
+
+    if (check_invariants && !admission && !violation) {
+      for (uint32_t i = 0; i < W; ++i) {
+        const BWorker& x = w[i];
+        if (!check_cache(x.cache) || x.inflight.size() > beta) return 9;
+        if (!x.waiting.empty() && x.inflight.size() < beta) return 9;
+        // pin count of every block = number of in-flight paths through it
+        std::unordered_map<uint64_t, uint32_t> pins;
+        for (const BRec& f : x.inflight) {
+          const uint64_t* Hf = H.data() + tr->block_offsets[f.j];
+          const uint32_t n = tr->n_in_blocks[f.j] + tr->n_out_blocks[f.j];
+          for (uint32_t d = 0; d < n; ++d) pins[Hf[d]]++;
+        }
+        for (auto& kv : x.cache.S) {
+          auto it = pins.find(kv.first);
+          if (kv.second.pin != (it == pins.end() ? 0u : it->second)) return 9;
+        }
+        if (x.Pt < 0.0) return 9;
+      }
+    }
+  }
+  // 5. drain (A35): every remaining completion and dequeue, in time order per
+  //    worker; decay ticks can no longer change any output and are not run
+  if (out->status == 0)
+    for (uint32_t i = 0; i < W && !admission && !violation; ++i)
+      while (!w[i].inflight.empty() && !admission && !violation) complete_next(i);
+  if (violation) return 9;
+  if (admission && out->status == 0) out->status = KVRO_TRIAL_ADMISSION;
+
+  for (uint32_t i = 0; i < W; ++i) {                 // A34: worker-index order
+    out->sum_latency_ms = out->sum_latency_ms + w[i].sum_lat;
+    out->sum_ttft_ms = out->sum_ttft_ms + w[i].sum_ttft;
+    if (w[i].P > out->makespan_ms) out->makespan_ms = w[i].P;
+    if (w[i].F > out->last_completion_ms) out->last_completion_ms = w[i].F;
+    out->sum_load_ms = out->sum_load_ms + w[i].P;
+  }
+  out->decision_digest = D;
+  if (out->status == 0 && vlog_full) out->status = KVRO_TRIAL_VICTIM_LOG_FULL;
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -387,12 +724,21 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   // Belady OPT is defined for one cache: the offline analysis runs it at W = 1
   if (pol->eviction == KVRO_EVICT_OPT && W != 1) return 1;
   if (!(pol->rho > 0.0 && pol->rho <= 1.0) || !(pol->delta_t_ms > 0.0)) return 1;
-  for (uint32_t j = 0; j < tr->n_queries; ++j)       // P:197 with beta = 1
-    if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
+  // beta * L_max <= B (beta = 1 in the default model)
+  const uint64_t beta = cfg->batch_slots > 0 ? cfg->batch_slots : 1;
+  if (cfg->batch_slots > 64) return 1;
+  if (cfg->batch_slots > 0 &&
+      (pol->eviction == KVRO_EVICT_OPT || pol->tracker_lag != 0 || pol->tracker_grain != 1))
+    return 1;   // the batched engine (A30) carries neither OPT nor tracker bias
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    if (beta * ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j]) > B) return 2;
 
   std::memset(out, 0, sizeof(*out));
   if (hist) std::memset(hist, 0, sizeof(uint32_t) * cfg->latency_hist_bins);
   const std::vector<uint64_t> H = chain_all(tr);
+  if (cfg->batch_slots > 0)
+    return run_batched(cfg, tr, pol, K, H, out, records, victims, victims_cap, hist,
+                       check_invariants);
   // OPT: identity -> ascending query indices containing it, and its path depth
   std::unordered_map<uint64_t, std::vector<uint64_t>> occ;
   std::unordered_map<uint64_t, uint32_t> depth_of;

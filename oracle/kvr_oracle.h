@@ -24,6 +24,10 @@
  *     5. accounting: Eq. 1, Eq. 2, Eq. 6,
  *        single-server FIFO latency / TTFT (A12, A20)
  *     6. decision digest
+ *   With kvro_config.batch_slots = beta >= 1 the same steps run in the
+ *   continuous-batching engine (readings A30-A36):
+ *   beta slots per worker, FIFO wait, UpdateCache at dequeue with the
+ *   in-flight paths pinned, completions in time order (run_batched).
  *
  * Every function returns 0 on success, nonzero on a contract error; none throws.
  */
@@ -42,7 +46,8 @@ enum { KVRO_ROUTE_LBGR = 0, KVRO_ROUTE_STATIC_LINEAR = 1, KVRO_ROUTE_THRESHOLD =
        KVRO_ROUTE_ROUND_ROBIN = 3, KVRO_ROUTE_RANDOM = 4,
        KVRO_ROUTE_LBGR_RLS = 5 /* LBGR with the RLS reading of "0.992" (A8b) */ };
 /* per-trial status codes */
-enum { KVRO_TRIAL_OK = 0, KVRO_TRIAL_RING_OVERFLOW = 1, KVRO_TRIAL_VICTIM_LOG_FULL = 2 };
+enum { KVRO_TRIAL_OK = 0, KVRO_TRIAL_RING_OVERFLOW = 1, KVRO_TRIAL_VICTIM_LOG_FULL = 2,
+       KVRO_TRIAL_ADMISSION = 4 /* batched: full cache, every leaf in flight */ };
 
 /* raw (un-chained) trace: host arrays.  Gamma_j = n_in input blocks then
  * n_out output blocks (A2); |q_j| = block_tokens*n_in (A1). */
@@ -73,6 +78,10 @@ typedef struct {
   double alpha_cached_ms, alpha_miss_ms, out_ms_per_token;   /* Eq. 1 truth */
   uint32_t pending_ring;        /* FIFO capacity per worker (0 = unbounded) */
   uint32_t latency_hist_bins;   /* 0 = no histogram */
+  uint32_t batch_slots;         /* 0: beta = 1 model of A3/A12 (update at assignment);
+                                   beta >= 1: continuous batching (A30-A35):
+                                   update at dequeue, in-flight paths pinned */
+  uint32_t _pad;
 } kvro_config;
 
 typedef struct {
