@@ -37,8 +37,9 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 4u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
-                                4: kvr_sim_config.extended_policies */
+#define KVR_ABI_VERSION 5u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
+                                4: kvr_sim_config.extended_policies;
+                                5: kvr_sim_config.batch_slots (continuous batching) */
 
 typedef int32_t kvr_status;
 enum {
@@ -56,7 +57,11 @@ enum {
   KVR_TRIAL_RING_OVERFLOW = 1,    /* a worker's pending-completion FIFO exceeded pending_ring:
                                      the trial stops before the overflowing query's cache update */
   KVR_TRIAL_VICTIM_LOG_FULL = 2,  /* recorded trial produced more victims than its log share */
-  KVR_TRIAL_BAD_POLICY = 3        /* per-trial policy out of range (trial not run) */
+  KVR_TRIAL_BAD_POLICY = 3,       /* per-trial policy out of range (trial not run) */
+  KVR_TRIAL_ADMISSION = 4         /* batching engine: full cache and every leaf in flight
+                                     (SPEC S:137); impossible when beta*L_max <= B, which
+                                     kvr_sim_run enforces.  Counters of a trial with a nonzero
+                                     status are unspecified in the batching engine. */
 };
 
 const char* kvr_last_error(void);
@@ -172,7 +177,16 @@ typedef struct {
                                       (runs the kernel instantiation that carries them; implied
                                       when default_policy uses one).  0: such a per-trial policy
                                       gets KVR_TRIAL_BAD_POLICY; the lean instantiation runs. */
-  uint32_t _pad;
+  uint32_t batch_slots;            /* 0: the beta = 1 model (update at assignment, single-server
+                                      FIFO; readings A3, A12).  1..64: continuous batching with
+                                      beta = batch_slots concurrent queries per worker (P:195-208,
+                                      Thm 2; readings A30-A36): FIFO wait for a slot, UpdateCache
+                                      at dequeue, in-flight paths pinned.  Runs kvr_batch.cu;
+                                      policies: LRU/RLT with every router (OPT and tracker bias
+                                      -> INVALID_ARG / KVR_TRIAL_BAD_POLICY); premise
+                                      beta * L_max <= B checked by kvr_sim_run (KVR_ERR_CAPACITY).
+                                      A recorded trial's victim share is split evenly over the
+                                      W workers, each logging its victims in dequeue order. */
 } kvr_sim_config;
 
 typedef struct kvr_sim kvr_sim;

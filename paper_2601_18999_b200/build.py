@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libkvr.so")
-SOURCES = ["kvr_api.cu", "kvr_pack.cu", "kvr_kernel.cu", "kvr_nextuse.cu"]
+SOURCES = ["kvr_api.cu", "kvr_pack.cu", "kvr_kernel.cu", "kvr_nextuse.cu", "kvr_batch.cu"]
 DEPS = SOURCES + ["kvr_internal.h", "kvr_device.cuh"]
 
 NVCC_FLAGS = [

@@ -92,13 +92,40 @@ struct Plan {
   uint32_t grid;
   kvr::WorkerLayout lay;
   kvr::AuxLayout aux;
+  kvr::BatchLayout blay;
   size_t ws_aux, ws_state, ws_total;
 };
+
+// continuous batching (kvr_batch.cu): per-worker state in shared memory when W
+// of them fit next to the control block (tier 1), else in the workspace (tier 2)
+kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, int optin,
+                           Plan* pl) {
+  const kvr_sim_config& c = sim->cfg;
+  pl->blay = kvr::make_batch_layout(c.capacity_blocks, c.batch_slots, std::max<uint32_t>(max_n, 1));
+  const size_t ctrl = kvr::batch_ctrl_bytes();
+  const size_t smem1 = ctrl + (size_t)c.W * pl->blay.bytes;
+  const bool fit1 = smem1 <= (size_t)optin;
+  const uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
+  if (tier == 1 && !fit1)
+    return fail(KVR_ERR_UNSUPPORTED, "batching: shared-memory tier needs %zu B > %d B", smem1, optin);
+  pl->tier = tier;
+  pl->smem = tier == 1 ? smem1 : ctrl;
+  cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy query (batching kernel)");
+  if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "batching kernel cannot be resident");
+  const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
+  pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
+  pl->ws_aux = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * sizeof(kvr::BFlight));
+  pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->blay.bytes : 0;
+  pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
+  return KVR_OK;
+}
 
 kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan* pl) {
   const kvr_sim_config& c = sim->cfg;
   const int optin = smem_optin();
   if (optin <= 0) return fail(KVR_ERR_CUDA, "no CUDA device available");
+  if (c.batch_slots > 0) return make_batch_plan(sim, max_n, n_trials, optin, pl);
   const size_t base = kvr::smem_base_bytes(c.W, max_n);
   const kvr::WorkerLayout l16 = kvr::make_layout(c.capacity_blocks, 2);
   const kvr::WorkerLayout l32 = kvr::make_layout(c.capacity_blocks, 4);
@@ -250,6 +277,12 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
     return fail(KVR_ERR_UNSUPPORTED, "policy: tracker_lag needs capacity_blocks <= 1024");
   if (cfg->default_policy.eviction == KVR_EVICT_OPT && cfg->W != 1)
     return fail(KVR_ERR_INVALID_ARG, "policy: OPT (offline Belady) is defined for W = 1");
+  if (cfg->batch_slots > 64) return fail(KVR_ERR_INVALID_ARG, "batch_slots must be in 0..64");
+  if (cfg->batch_slots > 0 &&
+      (cfg->default_policy.eviction == KVR_EVICT_OPT || cfg->default_policy.tracker_lag != 0 ||
+       cfg->default_policy.tracker_grain != 1))
+    return fail(KVR_ERR_INVALID_ARG,
+                "policy: the batching engine (batch_slots > 0) carries neither OPT nor tracker bias (A36)");
   kvr_sim* s = new kvr_sim;
   s->cfg = *cfg;
   *out = s;
@@ -311,10 +344,11 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   for (uint32_t i = 0; i < n_traces; ++i) {
     const kvr_trace* t = traces[i];
     if (!t) return fail(KVR_ERR_INVALID_ARG, "null trace %u", i);
-    if (t->max_n > c.capacity_blocks)
+    const uint64_t beta = c.batch_slots > 0 ? c.batch_slots : 1;
+    if (beta * t->max_n > c.capacity_blocks)
       return fail(KVR_ERR_CAPACITY,
-                  "trace %u has a complete path of %u blocks > capacity B=%u (premise beta*L_max<=B)",
-                  i, t->max_n, c.capacity_blocks);
+                  "trace %u: beta*L_max = %u*%u blocks > capacity B=%u (premise beta*L_max<=B, P:197)",
+                  i, (uint32_t)beta, t->max_n, c.capacity_blocks);
     max_n = std::max(max_n, t->max_n);
     max_N = std::max(max_N, t->N);
     if (!d_policies && c.default_policy.eviction == KVR_EVICT_OPT && !t->nu && t->total)
@@ -369,6 +403,15 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);
   if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
+  if (c.batch_slots > 0) {
+    p.beta = c.batch_slots;
+    p.blay = pl.blay;
+    p.bglobal = pl.tier == 2 ? 1u : 0u;
+    p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux : nullptr;
+    e = kvr::launch_batch(p, pl.grid, pl.smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "batching replay launch");
+    return KVR_OK;
+  }
   e = kvr::launch_replay(pl.tier, p, pl.grid, pl.smem, s, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   return KVR_OK;

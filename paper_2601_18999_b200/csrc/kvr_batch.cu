@@ -1,0 +1,794 @@
+// kvr_batch.cu — the continuous-batching replay kernel (beta >= 1 concurrent
+// queries per worker, readings A30-A36).
+//
+// Model ("the system handles beta distinct queries concurrently",
+// Thm 2; the SPEC's event engine S:499-549): every worker has beta batch slots;
+// an assigned query waits FIFO until a slot frees; UpdateCache (Eq. 3, Alg. 1 /
+// Leaf-LRU) runs when it is DEQUEUED and yields the true h; its blocks stay
+// pinned until its completion, so evictions pick unpinned leaves only.
+//
+// Execution: one CTA per trial (persistent over a work counter), one warp per
+// worker.  Per query j: every warp catches its worker up to a_j (decay ticks,
+// completions in time order, the dequeues they trigger — each warp mutates only
+// its own cache, so the W catch-ups run in parallel), matches the query's
+// prefix (lane-parallel probes + ballot) and scores; one __syncthreads; every
+// warp takes the same argmin; the chosen warp enqueues the query (or starts it
+// at once if a slot is free).  Scores, matches and the abort flag are
+// double-buffered by query parity so one barrier per query suffices.
+//
+// Per-worker state (tree slots, open-addressed identity -> slot table with
+// backward-shift deletion, pin counts, RLT marks, in-flight records, staged
+// path) lives in shared memory when W of them fit, else in the workspace
+// (L2-resident); the waiting FIFO is a ring in the workspace.  Victim
+// selection is a warp-parallel scan over the B slots (Leaf-LRU: warp min of
+// (stamp, -depth); RLT: ballot count + Philox draw + ballot select), i.e.
+// O(B/32) per eviction: this kernel is correct-first, the tuned β = 1 kernel
+// is kvr_kernel.cu.
+#include <math.h>
+
+#include "kvr_device.cuh"
+#include "kvr_internal.h"
+
+namespace kvr {
+
+extern __shared__ __align__(16) uint8_t kvr_bsmem[];
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;
+
+struct BView {
+  uint64_t* key;
+  uint32_t *stamp, *parent, *nchild, *depth, *table;
+  uint8_t *pin, *mark;
+  BFlight* fl;
+  double* rlsP;
+  uint64_t* gam;
+  uint32_t tmask;
+};
+
+__device__ __forceinline__ BView bview(uint8_t* base, const BatchLayout& L) {
+  BView v;
+  v.key = reinterpret_cast<uint64_t*>(base + L.off_key);
+  v.stamp = reinterpret_cast<uint32_t*>(base + L.off_stamp);
+  v.parent = reinterpret_cast<uint32_t*>(base + L.off_parent);
+  v.nchild = reinterpret_cast<uint32_t*>(base + L.off_nchild);
+  v.depth = reinterpret_cast<uint32_t*>(base + L.off_depth);
+  v.table = reinterpret_cast<uint32_t*>(base + L.off_table);
+  v.pin = base + L.off_pin;
+  v.mark = base + L.off_mark;
+  v.fl = reinterpret_cast<BFlight*>(base + L.off_fl);
+  v.rlsP = reinterpret_cast<double*>(base + L.off_rls);
+  v.gam = reinterpret_cast<uint64_t*>(base + L.off_gam);
+  v.tmask = L.T - 1;
+  return v;
+}
+
+// ---- identity -> slot table: linear probing, backward-shift deletion ----
+__device__ __forceinline__ uint32_t t_find(const BView& S, uint64_t t) {
+  uint32_t i = (uint32_t)t & S.tmask;
+  for (;;) {
+    const uint32_t s = S.table[i];
+    if (s == kNone) return kNone;
+    if (S.key[s] == t) return s;
+    i = (i + 1) & S.tmask;
+  }
+}
+__device__ __forceinline__ void t_insert(const BView& S, uint64_t t, uint32_t slot) {
+  uint32_t i = (uint32_t)t & S.tmask;
+  while (S.table[i] != kNone) i = (i + 1) & S.tmask;
+  S.table[i] = slot;
+}
+__device__ __forceinline__ void t_erase(const BView& S, uint64_t t) {
+  uint32_t i = (uint32_t)t & S.tmask;
+  while (S.key[S.table[i]] != t) i = (i + 1) & S.tmask;   // present (caller's contract)
+  uint32_t j = i;
+  for (;;) {
+    j = (j + 1) & S.tmask;
+    const uint32_t s = S.table[j];
+    if (s == kNone) break;
+    const uint32_t home = (uint32_t)S.key[s] & S.tmask;
+    // keep s where it is iff its home lies cyclically in (i, j]
+    const bool keep = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
+    if (!keep) {
+      S.table[i] = s;
+      i = j;
+    }
+  }
+  S.table[i] = kNone;
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t u = __shfl_xor_sync(kFull, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t hist_bin_b(double lat, uint32_t bins) {
+  if (!(lat >= 1.0)) return 0;
+  int e;
+  const double f = frexp(lat, &e);
+  const uint32_t q = (uint32_t)((f * 2.0 - 1.0) * 4.0);
+  const uint64_t b = 1 + 4 * (uint64_t)(e - 1) + q;
+  return b >= bins ? bins - 1 : (uint32_t)b;
+}
+
+// Control block of one CTA (one trial).
+struct __align__(16) BCtrl {
+  double score[2][kMaxW];
+  uint32_t mhit[2][kMaxW];
+  uint32_t pend[2][kMaxW];
+  uint32_t abortf[2];
+  uint32_t trial, status;
+  kvr_policy pol;
+  // per-worker partials, combined in worker order at the end of the trial (A34)
+  double P[kMaxW], F[kMaxW], slat[kMaxW], sttft[kMaxW], mlat[kMaxW];
+  unsigned long long cnt[kMaxW][12];
+  uint32_t hist[kMaxHistBins];
+};
+
+// Per-warp (worker) scalar state: warp-uniform registers.
+struct BW {
+  uint32_t size, cntT, nfl, wh, wn;
+  uint64_t e, k, vcur;
+  double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
+  // counters: probes, inserted, evictions, draws, resets, fallbacks, hit tokens,
+  // input tokens, queries, max pending, digest sum, victim-log overflow
+  unsigned long long c[12];
+  bool dead;   // admission failure / violation: stop this worker
+};
+
+struct BTrial {
+  const ReplayParams* p;
+  TraceDev tr;
+  const kvr_policy* pol;
+  uint64_t K;
+  uint32_t W, B, beta, i, lane, bt;
+  bool rlt, lbgr, rls;
+  kvr_query_record* rec;
+  uint64_t* vlog;
+  uint64_t vshare;
+  BFlight* ring;
+  uint32_t ringcap;
+  BCtrl* ctrl;
+};
+
+// UpdateCache(S_i, Gamma_j) at dequeue (Eq. 3 with Alg. 1 / Leaf-LRU, P:115-122,
+// P:225-245), pinning every block as it is accessed (A30, A33).
+// Returns the number of leading input hits m, or kNone on an admission failure.
+__device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j, uint32_t n,
+                             uint32_t n_in, uint32_t* nvict, uint64_t* Vout) {
+  const uint32_t lane = T.lane, B = T.B;
+  const kvr_policy& pol = *T.pol;
+  uint32_t prev = kNone;
+  uint32_t m = 0;
+  bool hitrun = true;   // hits are a prefix of Gamma (prefix closure)
+  uint32_t nv = 0;
+  uint64_t V = 0;
+  for (uint32_t d = 0; d < n; ++d) {
+    const uint64_t t = S.gam[d];
+    uint32_t s = hitrun ? t_find(S, t) : kNone;
+    if (s == kNone) hitrun = false;
+    // Alg. 1 l.6-9: mark t; the (B+1)-th distinct mark resets T to {t}
+    if (T.rlt) {
+      const bool marked = s != kNone && S.mark[s];
+      if (!marked) {
+        if (x.cntT + 1 == B + 1) {
+          for (uint32_t w = lane; w < (B + 3) / 4; w += 32) reinterpret_cast<uint32_t*>(S.mark)[w] = 0;
+          __syncwarp();
+          x.cntT = 1;
+          x.c[4]++;
+        } else {
+          x.cntT++;
+        }
+        if (s != kNone && lane == 0) S.mark[s] = 1;
+        __syncwarp();
+      }
+    }
+    if (s != kNone) {   // hit (Alg. 1 l.10-11): refresh, pin
+      if (lane == 0) {
+        S.stamp[s] = j;
+        S.pin[s] = (uint8_t)(S.pin[s] + 1);
+      }
+      __syncwarp();
+      if (d < n_in) m = d + 1;
+      prev = s;
+      continue;
+    }
+    uint32_t slot;
+    if (x.size == B) {
+      // choose the victim among unpinned leaves (A30, A33)
+      uint32_t v = kNone;
+      bool use_lru = !T.rlt;
+      bool mark_ok = T.rlt;    // RLT: U excludes T
+      if (T.rlt) {
+        uint32_t nU = 0;
+        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+          const uint32_t q = b0 + lane;
+          const bool c = q < B && S.pin[q] == 0 && S.nchild[q] == 0 && S.mark[q] == 0;
+          nU += __popc(__ballot_sync(kFull, c));
+        }
+        if (nU == 0) {   // A5: U empty
+          x.c[5]++;
+          mark_ok = false;
+          if (pol.rlt_fallback == KVR_RLT_EARLY_RESET) {
+            for (uint32_t w = lane; w < (B + 3) / 4; w += 32) reinterpret_cast<uint32_t*>(S.mark)[w] = 0;
+            __syncwarp();
+            x.cntT = 1;    // T <- {t}; t is loaded marked below
+            x.c[4]++;
+          } else if (pol.rlt_fallback == KVR_RLT_LRU_MARKED) {
+            use_lru = true;
+          }
+        }
+        if (!use_lru) {
+          if (!mark_ok) {
+            nU = 0;
+            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+              const uint32_t q = b0 + lane;
+              nU += __popc(__ballot_sync(kFull, q < B && S.pin[q] == 0 && S.nchild[q] == 0));
+            }
+          }
+          if (nU > 0) {
+            // Alg. 1 l.15: uniform over U in physical-slot order (A6)
+            const uint64_t r = philox_r64(T.K, x.e, T.i, 1);
+            x.e++;
+            x.c[3]++;
+            uint32_t idx = (uint32_t)pick_index(r, nU);
+            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
+              const uint32_t q = b0 + lane;
+              const bool c = q < B && S.pin[q] == 0 && S.nchild[q] == 0 && (!mark_ok || S.mark[q] == 0);
+              const uint32_t bal = __ballot_sync(kFull, c);
+              const uint32_t cnt = __popc(bal);
+              if (idx < cnt) {
+                v = b0 + select_bit(bal, idx);
+                break;
+              }
+              idx -= cnt;
+            }
+          }
+        }
+      }
+      if (use_lru) {   // least (stamp, -depth) among unpinned leaves
+        uint64_t best = ~0ull;
+        for (uint32_t q = lane; q < B; q += 32)
+          if (S.pin[q] == 0 && S.nchild[q] == 0) {
+            const uint64_t key = ((uint64_t)S.stamp[q] << 32) |
+                                 ((uint64_t)((0x10000u - S.depth[q]) & 0xffffu) << 16) | (uint64_t)q;
+            best = key < best ? key : best;
+          }
+        best = warp_min_u64(best);
+        if (best != ~0ull) v = (uint32_t)(best & 0xffffu);   // B <= 65536: slot fits 16 bits
+      }
+      if (v == kNone) return kNone;   // every leaf is in flight
+      // Evict(S, v): table delete, parent child count, T \ {v}
+      const uint64_t hv = S.key[v];
+      if (S.mark[v]) x.cntT--;
+      __syncwarp();
+      if (lane == 0) {
+        t_erase(S, hv);
+        if (S.parent[v] != kNone) S.nchild[S.parent[v]]--;
+        S.mark[v] = 0;
+      }
+      __syncwarp();
+      x.c[2]++;
+      V ^= fmix64(hv ^ ((uint64_t)(nv + 1) * kPosMul));
+      if (T.vlog) {
+        if (x.vcur < T.vshare) {
+          if (lane == 0) T.vlog[(uint64_t)T.i * T.vshare + x.vcur] = hv;
+        } else {
+          x.c[11] = 1;
+        }
+      }
+      x.vcur++;
+      nv++;
+      slot = v;
+    } else {
+      slot = x.size++;
+    }
+    // Load(S, t): pinned, stamped, marked under RLT (t in T after l.6-9)
+    if (lane == 0) {
+      S.key[slot] = t;
+      S.parent[slot] = prev;
+      S.nchild[slot] = 0;
+      S.stamp[slot] = j;
+      S.depth[slot] = d + 1;
+      S.pin[slot] = 1;
+      S.mark[slot] = T.rlt ? 1 : 0;
+      t_insert(S, t, slot);
+      if (prev != kNone) S.nchild[prev]++;
+    }
+    __syncwarp();
+    x.c[1]++;
+    prev = slot;
+  }
+  *nvict = nv;
+  *Vout = V;
+  return m;
+}
+
+// Dequeue r on worker T.i at time s (A30): stage Gamma_j, UpdateCache with
+// pinning, true h, Eq. 1 truth, record/digest/histogram, into a batch slot.
+__device__ bool b_dequeue(const BTrial& T, const BView& S, BW& x, const BFlight& r, double s) {
+  const uint32_t j = r.j, lane = T.lane;
+  const QueryHdr& h = T.tr.hdr[j];
+  const uint32_t n_in = h.n_in, n = h.n_in + h.n_out;
+  const uint64_t* Hj = T.tr.hash + h.block_off;
+  for (uint32_t d = lane; d < n; d += 32) S.gam[d] = Hj[d];
+  __syncwarp();
+  uint32_t nv = 0;
+  uint64_t V = 0;
+  const uint32_t m = b_update(T, S, x, j, n, n_in, &nv, &V);
+  if (m == kNone) return false;
+  const kvr_service_model& tm = T.p->truth;
+  const uint32_t q = T.bt * n_in;
+  const uint32_t hh = T.bt * m;
+  const double xh = (double)hh, yh = (double)(q - hh);
+  const double pre = (tm.alpha_cached_ms * xh) + (tm.alpha_miss_ms * yh);   // Eq. 1
+  const double O = tm.out_ms_per_token * (double)h.out_tokens;
+  const double cost = pre + O;
+  const double ttft = (s + pre) - r.a;                                        // A20
+  const double comp = s + cost;
+  const double lat = comp - r.a;
+  if (lane == 0) {
+    BFlight f = r;
+    f.c = comp;
+    S.fl[x.nfl] = f;
+  }
+  __syncwarp();
+  x.nfl++;
+  if (comp > x.F) x.F = comp;
+  x.P = x.P + cost;                                                           // Eq. 2
+  x.c[6] += hh;
+  x.c[7] += q;
+  x.slat = x.slat + lat;
+  x.sttft = x.sttft + ttft;
+  if (lat > x.mlat) x.mlat = lat;
+  x.c[8]++;
+  uint64_t Tj = fmix64(T.K ^ (uint64_t)j);
+  Tj = fmix64(Tj ^ (uint64_t)T.i);
+  Tj = fmix64(Tj ^ (uint64_t)m);
+  Tj = fmix64(Tj ^ (uint64_t)nv);
+  Tj = fmix64(Tj ^ V);
+  x.c[10] += Tj;
+  if (lane == 0) {
+    if (T.rec) {
+      kvr_query_record& R = T.rec[j];
+      R.worker = T.i;
+      R.hit_tokens = hh;
+      R.n_victims = nv;
+      R._pad = 0;
+      R.ttft_ms = ttft;
+      R.latency_ms = lat;
+      R.victim_offset = (uint64_t)T.i * T.vshare + (x.vcur - nv);
+    }
+    if (T.p->bins) atomicAdd(&T.ctrl->hist[hist_bin_b(lat, T.p->bins)], 1u);
+  }
+  return true;
+}
+
+// Completion of the earliest in-flight query (ties: lower j, A31): LBGR
+// OnlineUpdate (NLMS A8 / RLS A8b) and ReleaseLoad (A10) as in the beta = 1
+// model, unpin Gamma_j, then start the head of the waiting FIFO at c.
+__device__ bool b_complete(const BTrial& T, const BView& S, BW& x, uint32_t b) {
+  const uint32_t lane = T.lane;
+  const BFlight r = S.fl[b];
+  __syncwarp();
+  if (lane == 0) S.fl[b] = S.fl[x.nfl - 1];
+  __syncwarp();
+  x.nfl--;
+  const kvr_policy& pol = *T.pol;
+  if (T.lbgr) {
+    const double res = (r.c - r.a) - r.Ehat;
+    if (T.rls) {
+      // one exponentially weighted RLS step in the oracle's literal order (rls_step)
+      const double lam = pol.mu;
+      const double phi[4] = {r.phi0, r.phi1, r.phi2, 1.0};
+      double* Pm = S.rlsP;
+      double pi[4];
+      for (int a = 0; a < 4; ++a) {
+        double t = Pm[4 * a] * phi[0];
+        t = t + Pm[4 * a + 1] * phi[1];
+        t = t + Pm[4 * a + 2] * phi[2];
+        t = t + Pm[4 * a + 3] * phi[3];
+        pi[a] = t;
+      }
+      double g = phi[0] * pi[0];
+      g = g + phi[1] * pi[1];
+      g = g + phi[2] * pi[2];
+      g = g + phi[3] * pi[3];
+      const double gamma = lam + g;
+      double kv[4];
+      for (int a = 0; a < 4; ++a) kv[a] = pi[a] / gamma;
+      x.th0 = x.th0 + kv[0] * res;
+      x.th1 = x.th1 + kv[1] * res;
+      x.th2 = x.th2 + kv[2] * res;
+      x.th3 = x.th3 + kv[3] * res;
+      double nP = 0.0;
+      if (lane < 16) nP = (Pm[lane] - kv[lane >> 2] * pi[lane & 3]) / lam;
+      __syncwarp();
+      if (lane < 16) Pm[lane] = nP;
+      __syncwarp();
+    } else {
+      const double phi3 = 1.0;
+      double s2 = r.phi0 * r.phi0;
+      s2 = s2 + r.phi1 * r.phi1;
+      s2 = s2 + r.phi2 * r.phi2;
+      s2 = s2 + phi3 * phi3;
+      const double gs = (pol.mu * res) / (1.0 + s2);
+      x.th0 = x.th0 + gs * r.phi0;
+      x.th1 = x.th1 + gs * r.phi1;
+      x.th2 = x.th2 + gs * r.phi2;
+      x.th3 = x.th3 + gs * phi3;
+    }
+    uint64_t kap = x.k - r.ka;
+    double pw = 1.0, bb = pol.rho;
+    while (kap) {
+      if (kap & 1) pw = pw * bb;
+      bb = bb * bb;
+      kap >>= 1;
+    }
+    x.Pt = x.Pt - r.Chat * pw;
+    if (x.Pt < 0.0) x.Pt = 0.0;
+  }
+  // release_path: lane-parallel lookups, distinct slots
+  const QueryHdr& h = T.tr.hdr[r.j];
+  const uint32_t n = h.n_in + h.n_out;
+  const uint64_t* Hj = T.tr.hash + h.block_off;
+  bool bad = false;
+  for (uint32_t d = lane; d < n; d += 32) {
+    const uint32_t s = t_find(S, Hj[d]);
+    if (s == kNone || S.pin[s] == 0) bad = true;
+    else S.pin[s] = (uint8_t)(S.pin[s] - 1);
+  }
+  if (__any_sync(kFull, bad)) return false;
+  __syncwarp();
+  if (x.wn > 0) {
+    const BFlight hq = T.ring[(size_t)T.i * T.ringcap + x.wh];
+    x.wh = x.wh + 1 == T.ringcap ? 0 : x.wh + 1;
+    x.wn--;
+    return b_dequeue(T, S, x, hq, r.c);
+  }
+  return true;
+}
+
+__device__ __forceinline__ uint32_t b_next(const BView& S, const BW& x, double* c) {
+  uint32_t b = kNone;
+  double bc = INFINITY;
+  uint32_t bj = 0;
+  for (uint32_t u = 0; u < x.nfl; ++u) {
+    const double cu = S.fl[u].c;
+    const uint32_t ju = S.fl[u].j;
+    if (b == kNone || cu < bc || (cu == bc && ju < bj)) {
+      b = u;
+      bc = cu;
+      bj = ju;
+    }
+  }
+  *c = bc;
+  return b;
+}
+
+template <int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_constant__ ReplayParams p) {
+  uint8_t* smem = kvr_bsmem;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t W = p.W, B = p.B;
+  const BatchLayout& L = p.blay;
+  BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem);
+  uint8_t* sbase = smem + align16(sizeof(BCtrl));
+  uint8_t* wbase = p.bglobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
+                             : sbase + (size_t)w * L.bytes;
+  const BView S = bview(wbase, L);
+
+#pragma unroll 1
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t tt = atomicAdd(p.work_counter, 1u);
+      ctrl->trial = tt;
+      if (tt < p.n_trials) ctrl->pol = p.policies ? p.policies[tt] : p.defpol;
+      ctrl->abortf[0] = 0;
+      ctrl->abortf[1] = 0;
+      ctrl->status = 0;
+    }
+    for (uint32_t b = tid; b < p.bins; b += blockDim.x) ctrl->hist[b] = 0;
+    __syncthreads();
+    const uint32_t trial = ctrl->trial;
+    if (trial >= p.n_trials) break;
+    const kvr_policy& pol = ctrl->pol;
+    BTrial T;
+    T.p = &p;
+    T.tr = p.traces[p.trial_trace ? p.trial_trace[trial] : 0];
+    T.pol = &pol;
+    T.K = p.keys[trial];
+    T.W = W;
+    T.B = B;
+    T.beta = p.beta;
+    T.i = w;
+    T.lane = lane;
+    T.bt = T.tr.block_tokens;
+    T.rlt = pol.eviction == KVR_EVICT_RLT;
+    T.rls = pol.router == KVR_ROUTE_LBGR_RLS;
+    T.lbgr = pol.router == KVR_ROUTE_LBGR || T.rls;
+    const bool recorded = trial < p.record_trials;
+    T.rec = recorded ? p.records + (size_t)trial * p.rec_stride : nullptr;
+    T.vlog = (recorded && p.victims) ? p.victims + (size_t)trial * p.victims_per_trial : nullptr;
+    T.vshare = T.vlog ? p.victims_per_trial / W : 0;
+    T.ringcap = p.ring;
+    T.ring = reinterpret_cast<BFlight*>(p.aux_base) + (size_t)blockIdx.x * W * p.ring;
+    T.ctrl = ctrl;
+    const uint32_t N = T.tr.N;
+
+    // a per-trial policy from device memory is validated here (A36)
+    const bool pol_ok = pol.eviction <= KVR_EVICT_RLT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
+                        pol.router <= KVR_ROUTE_LBGR_RLS && pol.rho > 0.0 && pol.rho <= 1.0 &&
+                        pol.delta_t_ms > 0.0 && pol.tracker_lag == 0 && pol.tracker_grain == 1 &&
+                        (!T.rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
+                                    pol.rls_p0 < INFINITY));
+    // ---- per-trial init: empty caches, P = 0 ----
+    for (uint32_t q = lane; q < L.T; q += 32) S.table[q] = kNone;
+    for (uint32_t q = lane; q < B; q += 32) {
+      S.pin[q] = 0;
+      S.mark[q] = 0;
+    }
+    if (T.rls && lane < 16) S.rlsP[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;
+    __syncwarp();
+    BW x;
+    x.size = 0; x.cntT = 0; x.nfl = 0; x.wh = 0; x.wn = 0;
+    x.e = 0; x.k = 0; x.vcur = 0;
+    x.Pt = 0.0; x.P = 0.0; x.F = 0.0; x.slat = 0.0; x.sttft = 0.0; x.mlat = 0.0;
+    x.th0 = pol.theta0[0]; x.th1 = pol.theta0[1]; x.th2 = pol.theta0[2]; x.th3 = pol.theta0[3];
+    for (int c = 0; c < 12; ++c) x.c[c] = 0;
+    x.dead = false;
+    if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
+    const uint32_t Nrun = pol_ok ? N : 0;
+    const double rho = pol.rho, dt = pol.delta_t_ms;
+    bool aborted = false;
+    // Ehat / C^ / phi of this worker for the current query (used if it is chosen)
+    double myE = 0.0, myC = 0.0, f0 = 0.0, f1 = 0.0, f2 = 0.0;
+
+#pragma unroll 1
+    for (uint32_t j = 0; j < Nrun; ++j) {
+      const uint32_t par = j & 1;
+      const QueryHdr& hq = T.tr.hdr[j];
+      const double t = hq.arrival_ms;
+      const uint32_t n_in = hq.n_in;
+      const uint32_t q = T.bt * n_in;
+      // 1. catch-up: ticks, completions and the dequeues they start, in time order (A31)
+      if (!x.dead) {
+        for (;;) {
+          double c;
+          const uint32_t b = b_next(S, x, &c);
+          if (T.lbgr) {
+            const double tau = (double)(x.k + 1) * dt;
+            if (tau <= t && tau <= c) {
+              x.Pt = rho * x.Pt;
+              x.k++;
+              continue;
+            }
+          }
+          if (b != kNone && c <= t) {
+            if (!b_complete(T, S, x, b)) {
+              x.dead = true;
+              break;
+            }
+            continue;
+          }
+          break;
+        }
+        if (x.dead && lane == 0) {
+          atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_ADMISSION);
+          ctrl->abortf[par] = 1;
+        }
+      }
+      // 2. longest cached prefix at a_j (A32): lane-parallel probes, first miss by ballot
+      const uint64_t* Hj = T.tr.hash + hq.block_off;
+      uint32_t m = 0;
+      for (uint32_t b0 = 0; b0 < n_in; b0 += 32) {
+        const uint32_t d = b0 + lane;
+        const bool hit = d < n_in && t_find(S, Hj[d]) != kNone;
+        const uint32_t bal = __ballot_sync(kFull, hit);
+        if (bal != kFull) {
+          m = b0 + __ffs(~bal) - 1;
+          break;
+        }
+        m = b0 + 32;
+      }
+      if (m > n_in) m = n_in;
+      x.c[0] += (m + 1 < n_in) ? m + 1 : n_in;
+      const uint32_t pend = x.nfl + x.wn;
+      double sc = 0.0;
+      if (T.lbgr) {
+        const double xx = (double)(T.bt * m), yy = (double)(q - T.bt * m);
+        const double C = (pol.est_alpha_cached_ms * xx) + (pol.est_alpha_miss_ms * yy);   // Eq. 5
+        f0 = xx / 1000.0;
+        f1 = yy / 1000.0;
+        f2 = x.Pt / 1000.0;
+        double d = x.th0 * f0;
+        d = d + x.th1 * f1;
+        d = d + x.th2 * f2;
+        d = d + x.th3 * 1.0;
+        myE = (C + x.Pt) + d;                                                            // Eq. 4
+        myC = C;
+        sc = myE;
+      } else if (pol.router == KVR_ROUTE_STATIC_LINEAR) {
+        const double xx = (double)(T.bt * m);
+        sc = (pol.w_load * (double)pend) - (pol.w_hit * (xx / (double)q));                // A17
+      }
+      if (lane == 0) {
+        ctrl->score[par][w] = sc;
+        ctrl->mhit[par][w] = m;
+        ctrl->pend[par][w] = pend;
+      }
+      __syncthreads();
+      if (ctrl->abortf[par]) {
+        aborted = true;
+        break;
+      }
+      // 3. argmin (lowest index on ties, A15), identical in every warp
+      uint32_t best = 0;
+      const uint32_t router = pol.router;
+      if (T.lbgr || router == KVR_ROUTE_STATIC_LINEAR) {
+        for (uint32_t i = 1; i < W; ++i)
+          if (ctrl->score[par][i] < ctrl->score[par][best]) best = i;
+      } else if (router == KVR_ROUTE_THRESHOLD) {   // A16 on pending = waiting + in flight
+        uint32_t mx = ctrl->pend[par][0], mn = mx;
+        for (uint32_t i = 1; i < W; ++i) {
+          mx = max(mx, ctrl->pend[par][i]);
+          mn = min(mn, ctrl->pend[par][i]);
+        }
+        if ((double)mx > pol.tau * (double)max(1u, mn)) {
+          for (uint32_t i = 1; i < W; ++i)
+            if (ctrl->pend[par][i] < ctrl->pend[par][best]) best = i;
+        } else {
+          for (uint32_t i = 1; i < W; ++i)
+            if (ctrl->mhit[par][i] > ctrl->mhit[par][best]) best = i;
+        }
+      } else if (router == KVR_ROUTE_ROUND_ROBIN) {
+        best = j % W;
+      } else {
+        best = (uint32_t)pick_index(philox_r64(T.K, j, 0xFFFFFFFFu, 2), W);
+      }
+      // 4. assignment on the chosen worker (Eq. 6 at assignment, A32)
+      if (w == best) {
+        const uint32_t np = par ^ 1;   // flags written now are read after the next barrier
+        if (x.wn >= p.ring) {
+          if (lane == 0) {
+            atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_RING_OVERFLOW);
+            ctrl->abortf[np] = 1;
+          }
+          x.dead = true;
+        } else if (!x.dead) {
+          BFlight r;
+          r.j = j;
+          r._p = 0;
+          r.a = t;
+          r.c = 0.0;
+          r.Ehat = T.lbgr ? myE : 0.0;
+          r.phi0 = T.lbgr ? f0 : 0.0;
+          r.phi1 = T.lbgr ? f1 : 0.0;
+          r.phi2 = T.lbgr ? f2 : 0.0;
+          r.Chat = T.lbgr ? myC : 0.0;
+          r.ka = x.k;
+          if (T.lbgr) x.Pt = x.Pt + myC;
+          if (T.rec && lane == 0) T.rec[j].score = ctrl->score[par][best];
+          if (x.nfl < T.beta) {
+            if (!b_dequeue(T, S, x, r, t)) {
+              x.dead = true;
+              if (lane == 0) {
+                atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_ADMISSION);
+                ctrl->abortf[np] = 1;
+              }
+            }
+          } else {
+            if (lane == 0) {
+              uint32_t slot = x.wh + x.wn;
+              if (slot >= T.ringcap) slot -= T.ringcap;
+              T.ring[(size_t)T.i * T.ringcap + slot] = r;
+            }
+            __syncwarp();
+            x.wn++;
+          }
+          const uint32_t pe = x.nfl + x.wn;
+          if (pe > x.c[9]) x.c[9] = pe;
+        }
+      }
+    }
+    if (!aborted) {
+      __syncthreads();   // flags of the last query's assignment
+      if (ctrl->abortf[Nrun & 1]) aborted = true;
+    }
+    // 5. drain (A35): remaining completions and dequeues, per worker, no ticks
+    if (!aborted && !x.dead) {
+      for (;;) {
+        double c;
+        const uint32_t b = b_next(S, x, &c);
+        if (b == kNone) break;
+        if (!b_complete(T, S, x, b)) {
+          x.dead = true;
+          if (lane == 0) atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_ADMISSION);
+          break;
+        }
+      }
+    }
+    if (lane == 0) {
+      ctrl->P[w] = x.P;
+      ctrl->F[w] = x.F;
+      ctrl->slat[w] = x.slat;
+      ctrl->sttft[w] = x.sttft;
+      ctrl->mlat[w] = x.mlat;
+      for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = x.c[c];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      kvr_trial_result Rr;
+      unsigned long long s[12] = {0};
+      unsigned long long mp = 0, vfull = 0;
+      double mk = 0.0, lc = 0.0, sl = 0.0, slat = 0.0, sttft = 0.0, ml = 0.0;
+      for (uint32_t i = 0; i < W; ++i) {   // worker-index order (A34)
+        for (int c = 0; c < 12; ++c) s[c] += ctrl->cnt[i][c];
+        if (ctrl->cnt[i][9] > mp) mp = ctrl->cnt[i][9];
+        vfull |= ctrl->cnt[i][11];
+        if (ctrl->P[i] > mk) mk = ctrl->P[i];
+        if (ctrl->F[i] > lc) lc = ctrl->F[i];
+        sl = sl + ctrl->P[i];
+        slat = slat + ctrl->slat[i];
+        sttft = sttft + ctrl->sttft[i];
+        if (ctrl->mlat[i] > ml) ml = ctrl->mlat[i];
+      }
+      Rr.probes = s[0];
+      Rr.inserted_blocks = s[1];
+      Rr.evictions = s[2];
+      Rr.rlt_draws = s[3];
+      Rr.rlt_resets = s[4];
+      Rr.rlt_fallbacks = s[5];
+      Rr.hit_tokens = s[6];
+      Rr.input_tokens = s[7];
+      Rr.queries = s[8];
+      Rr.max_pending = mp;
+      Rr.decision_digest = T.K + s[10];
+      Rr.sum_latency_ms = slat;
+      Rr.sum_ttft_ms = sttft;
+      Rr.max_latency_ms = ml;
+      Rr.makespan_ms = mk;
+      Rr.last_completion_ms = lc;
+      Rr.sum_load_ms = sl;
+      uint32_t st = ctrl->status;
+      if (st == 0 && vfull) st = KVR_TRIAL_VICTIM_LOG_FULL;
+      Rr.status = (int32_t)st;
+      Rr._pad = 0;
+      p.results[trial] = Rr;
+    }
+    if (p.hist)
+      for (uint32_t b = tid; b < p.bins; b += blockDim.x)
+        p.hist[(size_t)trial * p.bins + b] = ctrl->hist[b];
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t batch_ctrl_bytes() { return align16(sizeof(BCtrl)); }
+
+static const void* batch_kernel_for(uint32_t W) {
+  if (W <= 4) return (const void*)batch_kernel<128>;
+  if (W <= 8) return (const void*)batch_kernel<256>;
+  if (W <= 16) return (const void*)batch_kernel<512>;
+  return (const void*)batch_kernel<1024>;
+}
+
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W) {
+  const void* k = batch_kernel_for(W);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, 32 * W, smem);
+}
+
+cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s) {
+  void* args[] = {const_cast<ReplayParams*>(&p)};
+  return cudaLaunchKernel(batch_kernel_for(p.W), dim3(grid), dim3(32 * p.W), args, smem, s);
+}
+
+}  // namespace kvr

@@ -132,6 +132,49 @@ inline size_t scratch_bytes(uint32_t max_n) {
   return align16(sizeof(WarpSm) + 4 * (2 * (size_t)max_n + 32));
 }
 
+// ---- continuous batching (kvr_batch.cu; readings A30-A36) ----
+// one assigned query: waiting in the FIFO ring, then in a batch slot (c set at dequeue)
+struct __align__(16) BFlight {
+  double c, a, Ehat, phi0, phi1, phi2, Chat;
+  uint64_t ka;
+  uint32_t j, _p;
+};
+static_assert(sizeof(BFlight) == 80, "flight record is 80 B");
+
+// Per-worker state of the batching kernel: u32 slot ids (NONE = 0xFFFFFFFF),
+// pin counts (u8, beta <= 64) and RLT marks (u8) per slot, the table
+// (T >= 2B, linear probing, backward-shift deletion), beta in-flight records,
+// the LBGR_RLS matrix and the staged path of the query being dequeued.
+struct BatchLayout {
+  uint32_t B, T, beta, max_n;
+  size_t off_key, off_stamp, off_parent, off_nchild, off_depth, off_table, off_pin, off_mark,
+      off_fl, off_rls, off_gam, bytes;
+};
+
+inline BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n) {
+  BatchLayout L{};
+  L.B = B;
+  L.beta = beta;
+  L.max_n = max_n;
+  uint32_t T = 64;
+  while (T < 2 * B) T <<= 1;
+  L.T = T;
+  size_t o = 0;
+  L.off_key = o;    o = align16(o + (size_t)B * 8);
+  L.off_stamp = o;  o = align16(o + (size_t)B * 4);
+  L.off_parent = o; o = align16(o + (size_t)B * 4);
+  L.off_nchild = o; o = align16(o + (size_t)B * 4);
+  L.off_depth = o;  o = align16(o + (size_t)B * 4);
+  L.off_table = o;  o = align16(o + (size_t)T * 4);
+  L.off_pin = o;    o = align16(o + (size_t)B + 4);
+  L.off_mark = o;   o = align16(o + (size_t)B + 4);
+  L.off_fl = o;     o = align16(o + (size_t)beta * sizeof(BFlight));
+  L.off_rls = o;    o = align16(o + 16 * 8);
+  L.off_gam = o;    o = align16(o + (size_t)max_n * 8);
+  L.bytes = o;
+  return L;
+}
+
 struct ReplayParams {
   TraceDev traces[kMaxTraces];
   const uint32_t* trial_trace;   // [n_trials] or null
@@ -153,6 +196,9 @@ struct ReplayParams {
   uint8_t* aux_base;             // [grid][W][aux.bytes]
   uint8_t* gstate;               // [grid][W][lay.bytes] (global tier) or null
   unsigned int* work_counter;
+  // batching kernel only (kvr_batch.cu)
+  uint32_t beta, bglobal;        // batch slots; per-worker state in gstate (1) or smem (0)
+  BatchLayout blay;              // aux_base = [grid][W][ring] BFlight waiting FIFOs
 };
 
 // exact table (bt * k) / 1000.0 for k = 0..max_n (the A9 feature scaling of integer token counts)
@@ -171,6 +217,10 @@ cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, 
 cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W, bool ext);
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
                           cudaStream_t s, bool ext);
+// continuous-batching kernel (kvr_batch.cu)
+size_t batch_ctrl_bytes();
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W);
+cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s);
 // next-use index for the offline OPT analysis (kvr_nextuse.cu)
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);
 cudaError_t build_next_use(const QueryHdr* hdr, uint32_t N, const uint64_t* hash, uint64_t n,

@@ -69,7 +69,7 @@ class kvr_sim_config(C.Structure):
                 ("truth", kvr_service_model), ("default_policy", kvr_policy),
                 ("pending_ring", C.c_uint32), ("record_trials", C.c_uint32),
                 ("latency_hist_bins", C.c_uint32), ("force_tier", C.c_uint32),
-                ("extended_policies", C.c_uint32), ("_pad", C.c_uint32)]
+                ("extended_policies", C.c_uint32), ("batch_slots", C.c_uint32)]
 
 
 POLICY_DTYPE = np.dtype([("eviction", "<u4"), ("rlt_fallback", "<u4"), ("router", "<u4"),
@@ -409,7 +409,7 @@ class Simulator:
                  alpha_cached_ms: float = 0.0, alpha_miss_ms: float = 1.0,
                  out_ms_per_token: float = 20.0, pending_ring: int = 256,
                  record_trials: int = 0, latency_hist_bins: int = 0, force_tier: int = 0,
-                 extended_policies: bool = False):
+                 extended_policies: bool = False, batch_slots: int = 0):
         cfg = kvr_sim_config()
         cfg.W, cfg.capacity_blocks = W, capacity_blocks
         cfg.truth.alpha_cached_ms = alpha_cached_ms
@@ -419,6 +419,7 @@ class Simulator:
         cfg.pending_ring, cfg.record_trials = pending_ring, record_trials
         cfg.latency_hist_bins, cfg.force_tier = latency_hist_bins, force_tier
         cfg.extended_policies = 1 if extended_policies else 0
+        cfg.batch_slots = batch_slots   # 0: beta = 1 model; >= 1: continuous batching (A30-A36)
         self.cfg = cfg
         self.handle = kvr_sim_create(cfg)
         self._ws = None
@@ -426,7 +427,8 @@ class Simulator:
     def _need_extended(self, policies: Optional[np.ndarray]):
         """Switch to the kernel instantiation with the extended policies when a
         per-trial policy array uses one (OPT, LBGR_RLS, tracker bias)."""
-        if policies is None or self.cfg.extended_policies or not policies_extended(policies):
+        if (policies is None or self.cfg.extended_policies or self.cfg.batch_slots
+                or not policies_extended(policies)):
             return
         self.cfg.extended_policies = 1
         old = self.handle

@@ -95,3 +95,46 @@ def compare(oracle, kvr, tr, W, B, pols, keys, truth=(0.0, 1.0, 20.0), ring=256,
         if bins:
             assert np.array_equal(out.hist[t], o.hist), ctx + " hist"
     return out, orc
+
+
+# ------------------------------------------------------------ continuous batching
+def compare_batched(oracle, kvr, tr, W, B, beta, pols, keys, truth=(0.0, 1.0, 20.0), ring=256,
+                    record=True, victims_cap=None, force_tier=0, bins=0):
+    """GPU batching kernel (kvr_batch.cu) vs the oracle's batching engine (A30-A36).
+    Trials with a nonzero status compare the status only (counters unspecified)."""
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
+    n = tr.n_queries
+    if victims_cap is None:
+        victims_cap = W * max(1, tr.total_blocks)
+    sim = Simulator(W, B, alpha_cached_ms=truth[0], alpha_miss_ms=truth[1],
+                    out_ms_per_token=truth[2], pending_ring=ring,
+                    record_trials=len(keys) if record else 0, force_tier=force_tier,
+                    latency_hist_bins=bins, batch_slots=beta)
+    out = sim.run(DeviceTrace(tr), np.asarray(keys, np.uint64), policies_array(pols),
+                  victims_cap=victims_cap * len(keys) if record else 0)
+    cfg = oracle.OracleConfig(W=W, capacity_blocks=B, alpha_cached_ms=truth[0],
+                              alpha_miss_ms=truth[1], out_ms_per_token=truth[2],
+                              pending_ring=ring, latency_hist_bins=bins, batch_slots=beta)
+    orc = []
+    for t, (k, pol) in enumerate(zip(keys, pols)):
+        o = oracle.run(cfg, tr, to_oracle_policy(oracle, pol), int(k), record=record,
+                       victims_cap=victims_cap)
+        assert o.rc == 0, o.rc
+        orc.append(o)
+        ctx = f"batched beta={beta} trial {t} key {k} pol {pol}"
+        g = out.results[t]
+        if o.result["status"] not in (0, 2) or int(g["status"]) not in (0, 2):
+            assert int(g["status"]) == o.result["status"], ctx
+            continue
+        assert_result_equal(g, o.result, ctx)
+        if record:
+            assert_records_equal(out.records[t], o.records, n, ctx)
+            gv = out.victims[t * victims_cap:(t + 1) * victims_cap]
+            for j in range(n):
+                off, nv = int(o.records[j]["victim_offset"]), int(o.records[j]["n_victims"])
+                hi = min(off + nv, (int(o.records[j]["worker"]) + 1) * (victims_cap // W))
+                if hi > off:
+                    assert np.array_equal(gv[off:hi], o.victims[off:hi]), f"{ctx} victims q{j}"
+        if bins:
+            assert np.array_equal(out.hist[t], o.hist), ctx + " hist"
+    return out, orc
