@@ -101,16 +101,19 @@ struct Plan {
 kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, int optin,
                            Plan* pl) {
   const kvr_sim_config& c = sim->cfg;
-  pl->blay = kvr::make_batch_layout(c.capacity_blocks, c.batch_slots, std::max<uint32_t>(max_n, 1));
+  const uint32_t mx = std::max<uint32_t>(max_n, 1);
+  const kvr::BatchLayout l16 = kvr::make_batch_layout(c.capacity_blocks, c.batch_slots, mx, 2);
+  const kvr::BatchLayout l32 = kvr::make_batch_layout(c.capacity_blocks, c.batch_slots, mx, 4);
   const size_t ctrl = kvr::batch_ctrl_bytes();
-  const size_t smem1 = ctrl + (size_t)c.W * pl->blay.bytes;
-  const bool fit1 = smem1 <= (size_t)optin;
+  const size_t smem1 = ctrl + (size_t)c.W * l16.bytes;
+  const bool fit1 = c.capacity_blocks <= 65535 && smem1 <= (size_t)optin;   // 0xFFFF = NONE
   const uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
   if (tier == 1 && !fit1)
     return fail(KVR_ERR_UNSUPPORTED, "batching: shared-memory tier needs %zu B > %d B", smem1, optin);
   pl->tier = tier;
+  pl->blay = tier == 1 ? l16 : l32;
   pl->smem = tier == 1 ? smem1 : ctrl;
-  cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W);
+  cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W, tier == 2);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query (batching kernel)");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "batching kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();

@@ -21,9 +21,10 @@
 // path) lives in shared memory when W of them fit, else in the workspace
 // (L2-resident); the waiting FIFO is a ring in the workspace.  Victim
 // selection is a warp-parallel scan over the B slots (Leaf-LRU: warp min of
-// (stamp, -depth); RLT: ballot count + Philox draw + ballot select), i.e.
-// O(B/32) per eviction: this kernel is correct-first, the tuned β = 1 kernel
-// is kvr_kernel.cu.
+// (stamp, -depth) over the set bits of the unpinned-leaf bitmap LEAFU; RLT:
+// popc of LEAFU & ~MARK per word, a Philox draw, a warp scan + bit select).
+// LEAFU is maintained incrementally: hits/loads pin (clear), unpins of a
+// childless node and evictions that empty an unpinned parent set it.
 #include <math.h>
 
 #include "kvr_device.cuh"
@@ -37,26 +38,33 @@ namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
 
+// Idx = u16 (shared-memory tier) or u32 (global tier) slot ids; all-ones = NONE
+template <typename Idx>
 struct BView {
+  static constexpr uint32_t NIL = (uint32_t)(Idx)~(Idx)0;
   uint64_t* key;
-  uint32_t *stamp, *parent, *nchild, *depth, *table;
-  uint8_t *pin, *mark;
+  uint32_t* stamp;
+  Idx *parent, *nchild, *depth, *table;
+  uint8_t* pin;
+  uint32_t *leafu, *markb;   // bitmaps: unpinned leaves (eviction candidates), RLT marks T
   BFlight* fl;
   double* rlsP;
   uint64_t* gam;
   uint32_t tmask;
 };
 
-__device__ __forceinline__ BView bview(uint8_t* base, const BatchLayout& L) {
-  BView v;
+template <typename Idx>
+__device__ __forceinline__ BView<Idx> bview(uint8_t* base, const BatchLayout& L) {
+  BView<Idx> v;
   v.key = reinterpret_cast<uint64_t*>(base + L.off_key);
   v.stamp = reinterpret_cast<uint32_t*>(base + L.off_stamp);
-  v.parent = reinterpret_cast<uint32_t*>(base + L.off_parent);
-  v.nchild = reinterpret_cast<uint32_t*>(base + L.off_nchild);
-  v.depth = reinterpret_cast<uint32_t*>(base + L.off_depth);
-  v.table = reinterpret_cast<uint32_t*>(base + L.off_table);
+  v.parent = reinterpret_cast<Idx*>(base + L.off_parent);
+  v.nchild = reinterpret_cast<Idx*>(base + L.off_nchild);
+  v.depth = reinterpret_cast<Idx*>(base + L.off_depth);
+  v.table = reinterpret_cast<Idx*>(base + L.off_table);
   v.pin = base + L.off_pin;
-  v.mark = base + L.off_mark;
+  v.leafu = reinterpret_cast<uint32_t*>(base + L.off_leafu);
+  v.markb = reinterpret_cast<uint32_t*>(base + L.off_mark);
   v.fl = reinterpret_cast<BFlight*>(base + L.off_fl);
   v.rlsP = reinterpret_cast<double*>(base + L.off_rls);
   v.gam = reinterpret_cast<uint64_t*>(base + L.off_gam);
@@ -65,37 +73,40 @@ __device__ __forceinline__ BView bview(uint8_t* base, const BatchLayout& L) {
 }
 
 // ---- identity -> slot table: linear probing, backward-shift deletion ----
-__device__ __forceinline__ uint32_t t_find(const BView& S, uint64_t t) {
+template <typename Idx>
+__device__ __forceinline__ uint32_t t_find(const BView<Idx>& S, uint64_t t) {
   uint32_t i = (uint32_t)t & S.tmask;
   for (;;) {
     const uint32_t s = S.table[i];
-    if (s == kNone) return kNone;
+    if (s == BView<Idx>::NIL) return kNone;
     if (S.key[s] == t) return s;
     i = (i + 1) & S.tmask;
   }
 }
-__device__ __forceinline__ void t_insert(const BView& S, uint64_t t, uint32_t slot) {
+template <typename Idx>
+__device__ __forceinline__ void t_insert(const BView<Idx>& S, uint64_t t, uint32_t slot) {
   uint32_t i = (uint32_t)t & S.tmask;
-  while (S.table[i] != kNone) i = (i + 1) & S.tmask;
-  S.table[i] = slot;
+  while (S.table[i] != BView<Idx>::NIL) i = (i + 1) & S.tmask;
+  S.table[i] = (Idx)slot;
 }
-__device__ __forceinline__ void t_erase(const BView& S, uint64_t t) {
+template <typename Idx>
+__device__ __forceinline__ void t_erase(const BView<Idx>& S, uint64_t t) {
   uint32_t i = (uint32_t)t & S.tmask;
   while (S.key[S.table[i]] != t) i = (i + 1) & S.tmask;   // present (caller's contract)
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & S.tmask;
     const uint32_t s = S.table[j];
-    if (s == kNone) break;
+    if (s == BView<Idx>::NIL) break;
     const uint32_t home = (uint32_t)S.key[s] & S.tmask;
     // keep s where it is iff its home lies cyclically in (i, j]
     const bool keep = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
     if (!keep) {
-      S.table[i] = s;
+      S.table[i] = (Idx)s;
       i = j;
     }
   }
-  S.table[i] = kNone;
+  S.table[i] = (Idx)BView<Idx>::NIL;
 }
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
@@ -146,7 +157,7 @@ struct BTrial {
   TraceDev tr;
   const kvr_policy* pol;
   uint64_t K;
-  uint32_t W, B, beta, i, lane, bt;
+  uint32_t W, B, beta, i, lane, bt, nwords;
   bool rlt, lbgr, rls;
   kvr_query_record* rec;
   uint64_t* vlog;
@@ -156,10 +167,52 @@ struct BTrial {
   BCtrl* ctrl;
 };
 
+__device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t s) {
+  return (bm[s >> 5] >> (s & 31)) & 1u;
+}
+
+// |candidates|: unpinned leaves (LEAFU), without RLT marks if `unmarked`
+template <typename Idx>
+__device__ __forceinline__ uint32_t cand_count(const BView<Idx>& S, const BTrial& T, bool unmarked) {
+  uint32_t c = 0;
+  for (uint32_t w = T.lane; w < T.nwords; w += 32)
+    c += __popc(S.leafu[w] & (unmarked ? ~S.markb[w] : ~0u));
+  return __reduce_add_sync(kFull, c);
+}
+
+// slot of the idx-th candidate in physical-slot order (idx < count): one warp
+// scan of the per-word counts per round of 32 words, then a bit select
+template <typename Idx>
+__device__ __forceinline__ uint32_t cand_select(const BView<Idx>& S, const BTrial& T, bool unmarked,
+                                                uint32_t idx) {
+  for (uint32_t w0 = 0; w0 < T.nwords; w0 += 32) {
+    const uint32_t w = w0 + T.lane;
+    const uint32_t word = w < T.nwords ? (S.leafu[w] & (unmarked ? ~S.markb[w] : ~0u)) : 0u;
+    const uint32_t c = __popc(word);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(kFull, inc, o);
+      if (T.lane >= (uint32_t)o) inc += u;
+    }
+    const uint32_t tot = __shfl_sync(kFull, inc, 31);
+    if (idx < tot) {
+      const uint32_t exc = inc - c;
+      const bool mine = idx >= exc && idx < inc;
+      const uint32_t owner = __ffs(__ballot_sync(kFull, mine)) - 1;
+      const uint32_t pos = mine ? (w << 5) + select_bit(word, idx - exc) : 0u;
+      return __shfl_sync(kFull, pos, owner);
+    }
+    idx -= tot;
+  }
+  return kNone;
+}
+
 // UpdateCache(S_i, Gamma_j) at dequeue (Eq. 3 with Alg. 1 / Leaf-LRU, P:115-122,
 // P:225-245), pinning every block as it is accessed (A30, A33).
 // Returns the number of leading input hits m, or kNone on an admission failure.
-__device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j, uint32_t n,
+template <typename Idx>
+__device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t j, uint32_t n,
                              uint32_t n_in, uint32_t* nvict, uint64_t* Vout) {
   const uint32_t lane = T.lane, B = T.B;
   const kvr_policy& pol = *T.pol;
@@ -174,24 +227,26 @@ __device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j,
     if (s == kNone) hitrun = false;
     // Alg. 1 l.6-9: mark t; the (B+1)-th distinct mark resets T to {t}
     if (T.rlt) {
-      const bool marked = s != kNone && S.mark[s];
+      const bool marked = s != kNone && bit_test(S.markb, s);
       if (!marked) {
         if (x.cntT + 1 == B + 1) {
-          for (uint32_t w = lane; w < (B + 3) / 4; w += 32) reinterpret_cast<uint32_t*>(S.mark)[w] = 0;
+          for (uint32_t w = lane; w < T.nwords; w += 32) S.markb[w] = 0;
           __syncwarp();
           x.cntT = 1;
           x.c[4]++;
         } else {
           x.cntT++;
         }
-        if (s != kNone && lane == 0) S.mark[s] = 1;
+        if (s != kNone && lane == 0) S.markb[s >> 5] |= 1u << (s & 31);
         __syncwarp();
       }
     }
-    if (s != kNone) {   // hit (Alg. 1 l.10-11): refresh, pin
+    if (s != kNone) {   // hit (Alg. 1 l.10-11): refresh, pin (an unpinned leaf stops being a candidate)
       if (lane == 0) {
         S.stamp[s] = j;
-        S.pin[s] = (uint8_t)(S.pin[s] + 1);
+        const uint32_t pv = S.pin[s];
+        S.pin[s] = (uint8_t)(pv + 1);
+        if (pv == 0) S.leafu[s >> 5] &= ~(1u << (s & 31));
       }
       __syncwarp();
       if (d < n_in) m = d + 1;
@@ -200,77 +255,63 @@ __device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j,
     }
     uint32_t slot;
     if (x.size == B) {
-      // choose the victim among unpinned leaves (A30, A33)
+      // choose the victim among unpinned leaves (A30, A33): LEAFU bitmap
       uint32_t v = kNone;
       bool use_lru = !T.rlt;
-      bool mark_ok = T.rlt;    // RLT: U excludes T
       if (T.rlt) {
-        uint32_t nU = 0;
-        for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-          const uint32_t q = b0 + lane;
-          const bool c = q < B && S.pin[q] == 0 && S.nchild[q] == 0 && S.mark[q] == 0;
-          nU += __popc(__ballot_sync(kFull, c));
-        }
+        bool mark_ok = true;    // RLT: U = LEAFU \ T
+        uint32_t nU = cand_count(S, T, true);
         if (nU == 0) {   // A5: U empty
           x.c[5]++;
           mark_ok = false;
           if (pol.rlt_fallback == KVR_RLT_EARLY_RESET) {
-            for (uint32_t w = lane; w < (B + 3) / 4; w += 32) reinterpret_cast<uint32_t*>(S.mark)[w] = 0;
+            for (uint32_t w = lane; w < T.nwords; w += 32) S.markb[w] = 0;
             __syncwarp();
             x.cntT = 1;    // T <- {t}; t is loaded marked below
             x.c[4]++;
           } else if (pol.rlt_fallback == KVR_RLT_LRU_MARKED) {
             use_lru = true;
           }
+          if (!use_lru) nU = cand_count(S, T, false);
         }
-        if (!use_lru) {
-          if (!mark_ok) {
-            nU = 0;
-            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-              const uint32_t q = b0 + lane;
-              nU += __popc(__ballot_sync(kFull, q < B && S.pin[q] == 0 && S.nchild[q] == 0));
-            }
-          }
-          if (nU > 0) {
-            // Alg. 1 l.15: uniform over U in physical-slot order (A6)
-            const uint64_t r = philox_r64(T.K, x.e, T.i, 1);
-            x.e++;
-            x.c[3]++;
-            uint32_t idx = (uint32_t)pick_index(r, nU);
-            for (uint32_t b0 = 0; b0 < B; b0 += 32) {
-              const uint32_t q = b0 + lane;
-              const bool c = q < B && S.pin[q] == 0 && S.nchild[q] == 0 && (!mark_ok || S.mark[q] == 0);
-              const uint32_t bal = __ballot_sync(kFull, c);
-              const uint32_t cnt = __popc(bal);
-              if (idx < cnt) {
-                v = b0 + select_bit(bal, idx);
-                break;
-              }
-              idx -= cnt;
-            }
-          }
+        if (!use_lru && nU > 0) {
+          // Alg. 1 l.15: uniform over U in physical-slot order (A6)
+          const uint64_t r = philox_r64(T.K, x.e, T.i, 1);
+          x.e++;
+          x.c[3]++;
+          v = cand_select(S, T, mark_ok, (uint32_t)pick_index(r, nU));
         }
       }
       if (use_lru) {   // least (stamp, -depth) among unpinned leaves
         uint64_t best = ~0ull;
-        for (uint32_t q = lane; q < B; q += 32)
-          if (S.pin[q] == 0 && S.nchild[q] == 0) {
+        for (uint32_t w = lane; w < T.nwords; w += 32) {
+          uint32_t bits = S.leafu[w];
+          while (bits) {
+            const uint32_t q = (w << 5) + (__ffs(bits) - 1);
+            bits &= bits - 1;
             const uint64_t key = ((uint64_t)S.stamp[q] << 32) |
                                  ((uint64_t)((0x10000u - S.depth[q]) & 0xffffu) << 16) | (uint64_t)q;
             best = key < best ? key : best;
           }
+        }
         best = warp_min_u64(best);
         if (best != ~0ull) v = (uint32_t)(best & 0xffffu);   // B <= 65536: slot fits 16 bits
       }
       if (v == kNone) return kNone;   // every leaf is in flight
-      // Evict(S, v): table delete, parent child count, T \ {v}
+      // Evict(S, v): table delete, parent child count (+ LEAFU), T \ {v}
       const uint64_t hv = S.key[v];
-      if (S.mark[v]) x.cntT--;
+      if (bit_test(S.markb, v)) x.cntT--;
       __syncwarp();
       if (lane == 0) {
         t_erase(S, hv);
-        if (S.parent[v] != kNone) S.nchild[S.parent[v]]--;
-        S.mark[v] = 0;
+        const uint32_t pa = S.parent[v];
+        if (pa != BView<Idx>::NIL) {
+          const uint32_t nc = S.nchild[pa] - 1u;
+          S.nchild[pa] = (Idx)nc;
+          if (nc == 0 && S.pin[pa] == 0) S.leafu[pa >> 5] |= 1u << (pa & 31);
+        }
+        S.markb[v >> 5] &= ~(1u << (v & 31));
+        S.leafu[v >> 5] &= ~(1u << (v & 31));
       }
       __syncwarp();
       x.c[2]++;
@@ -288,17 +329,17 @@ __device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j,
     } else {
       slot = x.size++;
     }
-    // Load(S, t): pinned, stamped, marked under RLT (t in T after l.6-9)
+    // Load(S, t): pinned (not in LEAFU), stamped, marked under RLT (t in T after l.6-9)
     if (lane == 0) {
       S.key[slot] = t;
-      S.parent[slot] = prev;
+      S.parent[slot] = (Idx)prev;           // kNone -> NIL (root child)
       S.nchild[slot] = 0;
       S.stamp[slot] = j;
-      S.depth[slot] = d + 1;
+      S.depth[slot] = (Idx)(d + 1);
       S.pin[slot] = 1;
-      S.mark[slot] = T.rlt ? 1 : 0;
+      if (T.rlt) S.markb[slot >> 5] |= 1u << (slot & 31);
       t_insert(S, t, slot);
-      if (prev != kNone) S.nchild[prev]++;
+      if (prev != kNone) S.nchild[prev] = (Idx)(S.nchild[prev] + 1);   // prev is pinned: never in LEAFU
     }
     __syncwarp();
     x.c[1]++;
@@ -311,7 +352,8 @@ __device__ uint32_t b_update(const BTrial& T, const BView& S, BW& x, uint32_t j,
 
 // Dequeue r on worker T.i at time s (A30): stage Gamma_j, UpdateCache with
 // pinning, true h, Eq. 1 truth, record/digest/histogram, into a batch slot.
-__device__ bool b_dequeue(const BTrial& T, const BView& S, BW& x, const BFlight& r, double s) {
+template <typename Idx>
+__device__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFlight& r, double s) {
   const uint32_t j = r.j, lane = T.lane;
   const QueryHdr& h = T.tr.hdr[j];
   const uint32_t n_in = h.n_in, n = h.n_in + h.n_out;
@@ -372,7 +414,8 @@ __device__ bool b_dequeue(const BTrial& T, const BView& S, BW& x, const BFlight&
 // Completion of the earliest in-flight query (ties: lower j, A31): LBGR
 // OnlineUpdate (NLMS A8 / RLS A8b) and ReleaseLoad (A10) as in the beta = 1
 // model, unpin Gamma_j, then start the head of the waiting FIFO at c.
-__device__ bool b_complete(const BTrial& T, const BView& S, BW& x, uint32_t b) {
+template <typename Idx>
+__device__ bool b_complete(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t b) {
   const uint32_t lane = T.lane;
   const BFlight r = S.fl[b];
   __syncwarp();
@@ -440,8 +483,13 @@ __device__ bool b_complete(const BTrial& T, const BView& S, BW& x, uint32_t b) {
   bool bad = false;
   for (uint32_t d = lane; d < n; d += 32) {
     const uint32_t s = t_find(S, Hj[d]);
-    if (s == kNone || S.pin[s] == 0) bad = true;
-    else S.pin[s] = (uint8_t)(S.pin[s] - 1);
+    if (s == kNone || S.pin[s] == 0) {
+      bad = true;
+    } else {
+      const uint32_t pv = S.pin[s] - 1u;
+      S.pin[s] = (uint8_t)pv;
+      if (pv == 0 && S.nchild[s] == 0) atomicOr(&S.leafu[s >> 5], 1u << (s & 31));
+    }
   }
   if (__any_sync(kFull, bad)) return false;
   __syncwarp();
@@ -454,7 +502,8 @@ __device__ bool b_complete(const BTrial& T, const BView& S, BW& x, uint32_t b) {
   return true;
 }
 
-__device__ __forceinline__ uint32_t b_next(const BView& S, const BW& x, double* c) {
+template <typename Idx>
+__device__ __forceinline__ uint32_t b_next(const BView<Idx>& S, const BW& x, double* c) {
   uint32_t b = kNone;
   double bc = INFINITY;
   uint32_t bj = 0;
@@ -471,8 +520,14 @@ __device__ __forceinline__ uint32_t b_next(const BView& S, const BW& x, double* 
   return b;
 }
 
+// register cap: 128 per thread up to 512 threads (2 CTAs of 8 warps per SM when
+// their state fits the shared memory), 64 at 1024 threads
 template <int kMaxThreads>
-__global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_constant__ ReplayParams p) {
+struct BMinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 2 : 1); };
+
+template <typename Idx, int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
+    batch_kernel(const __grid_constant__ ReplayParams p) {
   uint8_t* smem = kvr_bsmem;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t W = p.W, B = p.B;
@@ -481,7 +536,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_cons
   uint8_t* sbase = smem + align16(sizeof(BCtrl));
   uint8_t* wbase = p.bglobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
                              : sbase + (size_t)w * L.bytes;
-  const BView S = bview(wbase, L);
+  const BView<Idx> S = bview<Idx>(wbase, L);
 
 #pragma unroll 1
   for (;;) {
@@ -509,6 +564,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_cons
     T.i = w;
     T.lane = lane;
     T.bt = T.tr.block_tokens;
+    T.nwords = L.nwords;
     T.rlt = pol.eviction == KVR_EVICT_RLT;
     T.rls = pol.router == KVR_ROUTE_LBGR_RLS;
     T.lbgr = pol.router == KVR_ROUTE_LBGR || T.rls;
@@ -528,10 +584,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_cons
                         (!T.rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
                                     pol.rls_p0 < INFINITY));
     // ---- per-trial init: empty caches, P = 0 ----
-    for (uint32_t q = lane; q < L.T; q += 32) S.table[q] = kNone;
-    for (uint32_t q = lane; q < B; q += 32) {
-      S.pin[q] = 0;
-      S.mark[q] = 0;
+    for (uint32_t q = lane; q < L.T; q += 32) S.table[q] = (Idx)BView<Idx>::NIL;
+    for (uint32_t q = lane; q < B; q += 32) S.pin[q] = 0;
+    for (uint32_t q = lane; q < L.nwords; q += 32) {
+      S.leafu[q] = 0;
+      S.markb[q] = 0;
     }
     if (T.rls && lane < 16) S.rlsP[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;
     __syncwarp();
@@ -772,15 +829,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1) batch_kernel(const __grid_cons
 
 size_t batch_ctrl_bytes() { return align16(sizeof(BCtrl)); }
 
-static const void* batch_kernel_for(uint32_t W) {
-  if (W <= 4) return (const void*)batch_kernel<128>;
-  if (W <= 8) return (const void*)batch_kernel<256>;
-  if (W <= 16) return (const void*)batch_kernel<512>;
-  return (const void*)batch_kernel<1024>;
+template <typename Idx>
+static const void* batch_kernel_t(uint32_t W) {
+  if (W <= 4) return (const void*)batch_kernel<Idx, 128>;
+  if (W <= 8) return (const void*)batch_kernel<Idx, 256>;
+  if (W <= 16) return (const void*)batch_kernel<Idx, 512>;
+  return (const void*)batch_kernel<Idx, 1024>;
 }
 
-cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W) {
-  const void* k = batch_kernel_for(W);
+// tier 1: per-worker state in shared memory, u16 slot ids; tier 2: workspace, u32
+static const void* batch_kernel_for(uint32_t W, bool global) {
+  return global ? batch_kernel_t<uint32_t>(W) : batch_kernel_t<uint16_t>(W);
+}
+
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global) {
+  const void* k = batch_kernel_for(W, global);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, 32 * W, smem);
@@ -788,7 +851,7 @@ cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W) {
 
 cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s) {
   void* args[] = {const_cast<ReplayParams*>(&p)};
-  return cudaLaunchKernel(batch_kernel_for(p.W), dim3(grid), dim3(32 * p.W), args, smem, s);
+  return cudaLaunchKernel(batch_kernel_for(p.W, p.bglobal != 0), dim3(grid), dim3(32 * p.W), args, smem, s);
 }
 
 }  // namespace kvr

@@ -141,17 +141,18 @@ struct __align__(16) BFlight {
 };
 static_assert(sizeof(BFlight) == 80, "flight record is 80 B");
 
-// Per-worker state of the batching kernel: u32 slot ids (NONE = 0xFFFFFFFF),
-// pin counts (u8, beta <= 64) and RLT marks (u8) per slot, the table
+// Per-worker state of the batching kernel: u16 (shared-memory tier) or u32
+// (global tier) slot ids, all-ones = NONE,
+// pin counts (u8, beta <= 64) per slot, LEAFU / MARK bitmaps, the table
 // (T >= 2B, linear probing, backward-shift deletion), beta in-flight records,
 // the LBGR_RLS matrix and the staged path of the query being dequeued.
 struct BatchLayout {
-  uint32_t B, T, beta, max_n;
-  size_t off_key, off_stamp, off_parent, off_nchild, off_depth, off_table, off_pin, off_mark,
-      off_fl, off_rls, off_gam, bytes;
+  uint32_t B, T, beta, max_n, nwords, _pad;
+  size_t off_key, off_stamp, off_parent, off_nchild, off_depth, off_table, off_pin, off_leafu,
+      off_mark, off_fl, off_rls, off_gam, bytes;
 };
 
-inline BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n) {
+inline BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n, uint32_t idx_bytes) {
   BatchLayout L{};
   L.B = B;
   L.beta = beta;
@@ -162,12 +163,14 @@ inline BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n) 
   size_t o = 0;
   L.off_key = o;    o = align16(o + (size_t)B * 8);
   L.off_stamp = o;  o = align16(o + (size_t)B * 4);
-  L.off_parent = o; o = align16(o + (size_t)B * 4);
-  L.off_nchild = o; o = align16(o + (size_t)B * 4);
-  L.off_depth = o;  o = align16(o + (size_t)B * 4);
-  L.off_table = o;  o = align16(o + (size_t)T * 4);
+  L.off_parent = o; o = align16(o + (size_t)B * idx_bytes);
+  L.off_nchild = o; o = align16(o + (size_t)B * idx_bytes);
+  L.off_depth = o;  o = align16(o + (size_t)B * idx_bytes);
+  L.off_table = o;  o = align16(o + (size_t)T * idx_bytes);
+  L.nwords = (B + 31) / 32;
   L.off_pin = o;    o = align16(o + (size_t)B + 4);
-  L.off_mark = o;   o = align16(o + (size_t)B + 4);
+  L.off_leafu = o;  o = align16(o + (size_t)L.nwords * 4);   // unpinned-leaf bitmap
+  L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);   // RLT marking set T
   L.off_fl = o;     o = align16(o + (size_t)beta * sizeof(BFlight));
   L.off_rls = o;    o = align16(o + 16 * 8);
   L.off_gam = o;    o = align16(o + (size_t)max_n * 8);
@@ -219,7 +222,7 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
                           cudaStream_t s, bool ext);
 // continuous-batching kernel (kvr_batch.cu)
 size_t batch_ctrl_bytes();
-cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W);
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global);
 cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s);
 // next-use index for the offline OPT analysis (kvr_nextuse.cu)
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);

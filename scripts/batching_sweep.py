@@ -1,5 +1,5 @@
 """Continuous batching on the GPU (A30-A36): a sweep of
-the per-worker batch size beta on config 2's GSP shape (W = 8, B = 512, prefix
+the per-worker batch size beta on the bench's config-2 trace (W = 8, B = 512, prefix
 ratio 0.5, LBGR), RLT vs Leaf-LRU, next to the beta = 1 model of A3/A12
 (batch_slots = 0, the tuned kernel).  The premise beta * L_max <= B caps
 beta at 3 for the 129-block paths at B = 512; beta = 4 and 8 run at B = 1,032
@@ -25,14 +25,16 @@ nq = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 148
 out_path = sys.argv[3] if len(sys.argv) > 3 else None
 
-W = 8
-tr = wl.gsp(125, max(1, nq // 125), 0.5, seed=0xC3, W=W, lengths=(128, 256, 512, 1024, 2048))
+import bench  # noqa: E402  (config 2's trace recipe: the bench's r = 0.5 GSP trace)
+
+W = bench.W_WORKERS
+tr = bench.build_traces(nq)[1]
 dt = DeviceTrace(tr)
 L_max = int(tr.max_blocks)
 rows = []
 for beta, B in ((0, 512), (1, 512), (2, 512), (3, 512), (4, 8 * L_max), (8, 8 * L_max), (0, 8 * L_max)):
     for ev, ename in ((1, "RLT"), (0, "L-LRU")):
-        sim = Simulator(W, B, pending_ring=1 << 15, batch_slots=beta)
+        sim = Simulator(W, B, pending_ring=bench.RING, batch_slots=beta)
         keys = np.arange(1, K + 1, dtype=np.uint64)
         pols = policies_array([Policy(eviction=ev) for _ in range(K)])
         b = sim.alloc([dt], K)
@@ -67,5 +69,5 @@ for beta, B in ((0, 512), (1, 512), (2, 512), (3, 512), (4, 8 * L_max), (8, 8 * 
 
 if out_path:
     with open(out_path, "w") as f:
-        json.dump(dict(workload=f"config-2 GSP r=0.5, W={W}, {tr.n_queries} queries, LBGR (App. A)",
+        json.dump(dict(workload=f"config-2 bench trace r=0.5 (bench.build_traces()[1]), W={W}, {tr.n_queries} queries, LBGR (App. A)",
                        rows=rows), f, indent=1)

@@ -1,6 +1,7 @@
 """One replay launch of a chosen slice of the bench workload (for ncu).
 
-usage: python scripts/ncu_case.py [rlt|lru|mix] [queries] [trials]
+usage: python scripts/ncu_case.py [rlt|lru|mix] [queries] [trials] [batch_slots=0]
+(batch_slots > 0 runs the continuous-batching kernel, kvr_batch.cu)
 """
 import os
 import sys
@@ -16,6 +17,7 @@ from paper_2601_18999_b200 import kvr  # noqa: E402
 mode = sys.argv[1] if len(sys.argv) > 1 else "rlt"
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 3000
 nt = int(sys.argv[3]) if len(sys.argv) > 3 else 296
+beta = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 trs = bench.build_traces(nq)
 dts = [kvr.DeviceTrace(t) for t in trs]
 t_of, ev, keys = bench.trial_plan(0, nt)
@@ -23,7 +25,7 @@ if mode == "rlt":
     ev[:] = 1
 elif mode == "lru":
     ev[:] = 0
-sim = kvr.Simulator(8, 512, pending_ring=bench.RING)
+sim = kvr.Simulator(8, 512, pending_ring=bench.RING, batch_slots=beta)
 pols = kvr.policies_array([kvr.Policy(eviction=int(e)) for e in ev])
 out = sim.run(dts, keys, pols, trial_trace=t_of)
 torch.cuda.synchronize()
