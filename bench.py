@@ -165,6 +165,17 @@ def run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads):
     return q, time.perf_counter() - t0
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -340,9 +351,12 @@ def main():
         threads = max(1, min(os.cpu_count() or 1, 16))
         nq = args.ref_queries
         q, s = run_oracle_sample(traces, trace_of, evict, keys, nq, threads)
+        q1, s1 = run_oracle_sample(traces, trace_of, evict, keys, nq, 1)   # one core
         line["cpu_baseline"] = {"value": q / s, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "single_core_value": q1 / s1, "nproc": os.cpu_count(),
+                                "cpu_model": cpu_model(),
                                 "sample": f"{threads} trials x first {nq} queries of the "
-                                          f"config-2 traces (W=8, B=512)"}
+                                          f"config-2 traces (W=8, B=512); single core: 1 trial"}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
