@@ -139,3 +139,25 @@ def test_beta_sweep_multiserver_monotone(kvr, oracle_mod):
         if prev is not None:
             assert np.all(lat <= prev)
         prev = lat
+
+
+def test_config2_full_trace_sampled(kvr, oracle_mod):
+    """The bench's full 100k-query config-2 trace (r = 0.5) through the batching kernel at
+    the largest beta the premise allows at B = 512 (beta = 3, L_max = 129), in one launch of
+    64 trials; two sampled trials (RLT, L-LRU) replayed by the oracle over all 100k queries."""
+    import bench
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
+    from parity_util import assert_result_equal
+    tr = bench.build_traces()[1]
+    sim = Simulator(bench.W_WORKERS, bench.B_BLOCKS, pending_ring=bench.RING, batch_slots=3)
+    keys = np.arange(1, 65, dtype=np.uint64)
+    pols = [kvr.Policy(eviction=int(k) % 2) for k in keys]
+    out = sim.run(DeviceTrace(tr), keys, policies_array(pols))
+    assert np.all(out.results["status"] == 0)
+    assert np.all(out.results["queries"] == tr.n_queries)
+    cfg = oracle_mod.OracleConfig(W=bench.W_WORKERS, capacity_blocks=bench.B_BLOCKS,
+                                  pending_ring=bench.RING, batch_slots=3)
+    for t in (0, 63):
+        o = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=int(keys[t]) % 2), int(keys[t]))
+        assert o.rc == 0
+        assert_result_equal(out.results[t], o.result, f"batching config2 trial {t}")
