@@ -221,7 +221,40 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
   bool hitrun = true;   // hits are a prefix of Gamma (prefix closure)
   uint32_t nv = 0;
   uint64_t V = 0;
-  for (uint32_t d = 0; d < n; ++d) {
+  // Lane-parallel hit run: 32 blocks per step, each lane looks up its own block; the
+  // leading hits are refreshed, pinned and (RLT) marked at once when no |T| = B+1
+  // reset can fall inside the step, else the step is left to the serial loop below.
+  uint32_t d = 0;
+  while (d < n) {
+    const uint32_t q = d + lane;
+    const uint32_t sl = q < n ? t_find(S, S.gam[q]) : kNone;
+    const uint32_t hb = __ballot_sync(kFull, sl != kNone);
+    const uint32_t hc = (~hb) ? (uint32_t)(__ffs(~hb) - 1) : 32u;   // leading hits of this step
+    const bool hit = lane < hc;
+    if (T.rlt) {
+      const uint32_t nnew = __popc(__ballot_sync(kFull, hit && !bit_test(S.markb, sl)));
+      if (x.cntT + nnew > B) break;                                  // a reset: serial path
+      if (hit && !bit_test(S.markb, sl)) atomicOr(&S.markb[sl >> 5], 1u << (sl & 31));
+      x.cntT += nnew;
+    }
+    if (hit) {
+      S.stamp[sl] = j;
+      const uint32_t pv = S.pin[sl];
+      S.pin[sl] = (uint8_t)(pv + 1);
+      if (pv == 0) atomicAnd(&S.leafu[sl >> 5], ~(1u << (sl & 31)));
+    }
+    __syncwarp();
+    if (hc > 0) {
+      prev = __shfl_sync(kFull, sl, hc - 1);
+      m = min(d + hc, n_in);
+    }
+    d += hc;
+    if (hc < 32) {
+      hitrun = false;   // the first miss: every later block of Gamma misses too
+      break;
+    }
+  }
+  for (; d < n; ++d) {
     const uint64_t t = S.gam[d];
     uint32_t s = hitrun ? t_find(S, t) : kNone;
     if (s == kNone) hitrun = false;
