@@ -345,8 +345,24 @@ def main():
     if world > 1 and rank == 0 and summary[0] is not None:
         line["reduced_summary"] = dict(zip(kdist.SUMMARY_FIELDS,
                                            [int(x) for x in summary[0].cpu().tolist()]))
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args)
+    if not args.no_e2e:
+        # every rank runs its own trials end to end; the job's rate is all ranks'
+        # queries over the slowest rank's time (max over ranks, like `value`)
+        if world > 1:
+            dist.barrier()
+        e = e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args)
+        if world > 1:
+            t = torch.tensor([e["ms_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            c = torch.tensor([e["queries_per_step"], e["h2d_bytes_per_step"], e["d2h_bytes_per_step"]],
+                             dtype=torch.float64, device=dev)
+            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            e["ms_per_step"] = float(t[0])
+            e["queries_per_step"], e["h2d_bytes_per_step"], e["d2h_bytes_per_step"] = \
+                float(c[0]), int(c[1]), int(c[2])
+            e["value"] = e["queries_per_step"] / (e["ms_per_step"] / 1000.0)
+        if rank == 0:
+            line["e2e"] = e
     if rank == 0 and not args.no_cpu_baseline:
         threads = max(1, min(os.cpu_count() or 1, 16))
         nq = args.ref_queries
@@ -405,7 +421,7 @@ def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):
             d.close()
     ms = float(np.mean(times))
     return {"value": q / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "queries_per_step": q}
 
 
 if __name__ == "__main__":
