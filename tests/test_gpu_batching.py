@@ -161,3 +161,24 @@ def test_config2_full_trace_sampled(kvr, oracle_mod):
         o = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=int(keys[t]) % 2), int(keys[t]))
         assert o.rc == 0
         assert_result_equal(out.results[t], o.result, f"batching config2 trial {t}")
+
+
+def test_edge_cases(kvr, oracle_mod):
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator
+    pols = [kvr.Policy(eviction=e) for e in (0, 1)] + [kvr.Policy(eviction=1, rlt_fallback=1)]
+    # B = 1, beta = 1, single-block paths, W = 1
+    tr = wl.from_paths([[k % 3] for k in range(40)], arrival_ms=np.arange(40) * 100.0)
+    compare_batched(oracle_mod, kvr, tr, 1, 1, 1, pols, [1, 2, 3])
+    # beta = 64 (the maximum) with single-block paths, everything arriving at once
+    tr = wl.from_paths([[k % 70] for k in range(300)])
+    compare_batched(oracle_mod, kvr, tr, 2, 64, 64, pols, [4, 5, 6])
+    # W = 32, both tiers
+    tr = wl.random_tree(200, 77, max_len=4, alphabet=3, max_out=1, W=32, util=2.0)
+    for ft in (1, 2):
+        compare_batched(oracle_mod, kvr, tr, 32, 2 * int(tr.max_blocks), 2, pols, [7, 8, 9],
+                        force_tier=ft)
+    # empty trace
+    sim = Simulator(2, 8, batch_slots=2)
+    out = sim.run(DeviceTrace(wl.from_paths([])), np.array([1, 2], np.uint64))
+    assert np.all(out.results["queries"] == 0) and np.all(out.results["status"] == 0)
+    assert np.all(out.results["decision_digest"] == np.array([1, 2], np.uint64))
