@@ -273,6 +273,9 @@ def main():
     buf["policies"].copy_(torch.from_numpy(pols.view(np.uint8)))
     buf["trial_trace"].copy_(torch.from_numpy(trace_of.view(np.int32)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # every rank packs the same traces; their identity checksum rides in the reduce
+    trace_hash = sum(d.identity_digest() for d in dts) & 0xFFFFFFFFFFFFFFFF
+    trace_hash = trace_hash - (1 << 64) if trace_hash >= (1 << 63) else trace_hash
     from paper_2601_18999_b200 import dist as kdist
     summary = [None]
 
@@ -285,7 +288,7 @@ def main():
         e0.record(stream)
         sim.launch(dts, n_trials, buf, with_policies=True, stream=stream)
         if world > 1:   # the single NCCL reduce of summary counters
-            vec = kdist.summary_tensor(buf["results"], n_trials)
+            vec = kdist.summary_tensor(buf["results"], n_trials, trace_hash)
             dist.reduce(vec, dst=0)
             summary[0] = vec
         e1.record(stream)
@@ -345,6 +348,9 @@ def main():
     if world > 1 and rank == 0 and summary[0] is not None:
         line["reduced_summary"] = dict(zip(kdist.SUMMARY_FIELDS,
                                            [int(x) for x in summary[0].cpu().tolist()]))
+        # sum over ranks of identical checksums = world x rank 0's (mod 2^64)
+        line["reduced_summary"]["trace_hash_consistent"] = (
+            (line["reduced_summary"]["trace_hash"] - world * trace_hash) % (1 << 64) == 0)
     if not args.no_e2e:
         # every rank runs its own trials end to end; the job's rate is all ranks'
         # queries over the slowest rank's time (max over ranks, like `value`)

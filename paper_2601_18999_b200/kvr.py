@@ -363,6 +363,18 @@ class DeviceTrace:
         off = kvr_trace_chained_hashes(self.handle) - _ptr(self.packed)
         return self.packed[off: off + 8 * n].cpu().numpy().view(np.uint64).copy()
 
+    def identity_digest(self) -> int:
+        """Order-sensitive checksum of the packed identities, computed on the device
+        (multi-GPU check that every rank packed the same trace)."""
+        import torch
+        n = self.n_blocks_total
+        if n == 0:
+            return 0
+        off = kvr_trace_chained_hashes(self.handle) - _ptr(self.packed)
+        h = self.packed[off: off + 8 * n].view(torch.int64)
+        pos = torch.arange(1, n + 1, dtype=torch.int64, device=h.device)
+        return int((h.sum() + (h ^ (pos * 0x5851F42D4C957F2D)).sum()).item()) & 0xFFFFFFFFFFFFFFFF
+
     def with_next_use(self, stream=None) -> "DeviceTrace":
         """A trace handle that also carries the next-use index (offline OPT,
         KVR_EVICT_OPT): same packed buffer, plus a u32 [n_blocks_total] index

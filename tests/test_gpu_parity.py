@@ -177,3 +177,14 @@ def test_adversarial_large_B_global_tier(kvr, oracle_mod):
     tr = wl.adv(B, 4, 2).prefix(66000)
     pols = [_pols(kvr, eviction=0, router=3), _pols(kvr, eviction=1, router=3)]
     compare(oracle_mod, kvr, tr, 1, B, pols, [1, 2], record=False)
+
+
+def test_identity_digest(kvr, oracle_mod):
+    """The multi-GPU trace checksum (bench.py reduce): same raw trace -> same digest on
+    every load; a different salt (different identities) -> a different digest."""
+    from paper_2601_18999_b200.kvr import DeviceTrace
+    tr = wl.gsp(6, 5, 0.5, seed=3)
+    a, b = DeviceTrace(tr).identity_digest(), DeviceTrace(tr).identity_digest()
+    assert a == b and a != 0
+    tr.hash_salt = 99
+    assert DeviceTrace(tr).identity_digest() != a
