@@ -973,6 +973,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   KVR_ACC(24, t_ap);   // rebuilds
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  __syncwarp();   // every lane's reads of ws->x.used / ws->active precede lane 0's writes
   if (lane == 0) {
     // decision digest: D += T_j, order-independent across queries
     uint64_t T = fmix64(ctrl->dkey ^ (uint64_t)ws->j);
