@@ -182,3 +182,21 @@ def test_edge_cases(kvr, oracle_mod):
     out = sim.run(DeviceTrace(wl.from_paths([])), np.array([1, 2], np.uint64))
     assert np.all(out.results["queries"] == 0) and np.all(out.results["status"] == 0)
     assert np.all(out.results["decision_digest"] == np.array([1, 2], np.uint64))
+
+
+def test_multi_trace_launch(kvr, oracle_mod):
+    """kvr_sim_run_multi with the batching kernel: trials over three traces in one launch."""
+    from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
+    from parity_util import assert_result_equal
+    trs = [wl.gsp(10, 8, r, seed=20 + i, W=3, lengths=(256, 512)) for i, r in enumerate((0.3, 0.5, 0.9))]
+    pols = [kvr.Policy(eviction=t % 2, router=(0, 1, 5)[t % 3]) for t in range(9)]
+    keys = np.arange(50, 59, dtype=np.uint64)
+    tt = np.array([t % 3 for t in range(9)], dtype=np.uint32)
+    sim = Simulator(3, 128, batch_slots=2)
+    out = sim.run([DeviceTrace(t) for t in trs], keys, policies_array(pols), trial_trace=tt)
+    cfg = oracle_mod.OracleConfig(W=3, capacity_blocks=128, batch_slots=2)
+    from parity_util import to_oracle_policy
+    for t in range(9):
+        o = oracle_mod.run(cfg, trs[tt[t]], to_oracle_policy(oracle_mod, pols[t]), int(keys[t]))
+        assert o.rc == 0
+        assert_result_equal(out.results[t], o.result, f"trial {t}")
