@@ -37,9 +37,10 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 5u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
+#define KVR_ABI_VERSION 6u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
                                 4: kvr_sim_config.extended_policies;
-                                5: kvr_sim_config.batch_slots (continuous batching) */
+                                5: kvr_sim_config.batch_slots (continuous batching);
+                                6: kvr_trace_collision_bytes / kvr_trace_check_collisions */
 
 typedef int32_t kvr_status;
 enum {
@@ -47,6 +48,8 @@ enum {
   KVR_ERR_INVALID_ARG = 1,        /* bad pointer / size / parameter / malformed trace */
   KVR_ERR_CAPACITY = 2,           /* some n_in+n_out > B: premise beta*L_max <= B (beta=1) */
   KVR_ERR_UNSUPPORTED = 3,        /* W > 32, B > 65536, or no state tier fits */
+  KVR_ERR_HASH_COLLISION = 4,     /* kvr_trace_check_collisions found two prefixes with one
+                                     identity: reload the trace with another hash_salt */
   KVR_ERR_WORKSPACE_TOO_SMALL = 5,
   KVR_ERR_CUDA = 6                /* a CUDA runtime call failed (message in kvr_last_error) */
 };
@@ -107,6 +110,23 @@ kvr_status kvr_trace_info(const kvr_trace* tr, uint32_t* n_queries, uint32_t* ma
 /* DEVICE pointer to the chained identities H (CSR order, [n_blocks_total]). */
 kvr_status kvr_trace_chained_hashes(const kvr_trace* tr, const uint64_t** d_hashes);
 kvr_status kvr_trace_destroy(kvr_trace* tr);
+
+/* Optional identity collision check (the chain of reading A26 is a
+ * 64-bit hash, so two different prefixes could share an identity with probability
+ * ~ n^2 / 2^65).  A block's identity is legitimately determined by (depth, parent
+ * identity, content key); the check sorts (identity, occurrence) pairs on the
+ * device and counts adjacent occurrences with equal identity but a different
+ * tuple -- by induction over depth, zero certifies that every identity names one
+ * prefix.  d_block_keys: DEVICE, the raw keys the trace was loaded from
+ * ([n_blocks_total], CSR order); d_scratch: DEVICE, caller-owned, >=
+ * kvr_trace_collision_bytes.  SYNCHRONOUS on `stream`.  Returns KVR_OK (zero
+ * collisions) or KVR_ERR_HASH_COLLISION with *n_collisions = the number of such
+ * adjacent pairs (the caller re-salts and reloads); INVALID_ARG / UNSUPPORTED
+ * (>= 2^31 blocks) / WORKSPACE_TOO_SMALL as usual. */
+kvr_status kvr_trace_collision_bytes(const kvr_trace* tr, size_t* scratch_bytes);
+kvr_status kvr_trace_check_collisions(const kvr_trace* tr, const uint64_t* d_block_keys,
+                                      void* d_scratch, size_t scratch_bytes, void* stream,
+                                      uint64_t* n_collisions);
 
 /* Next-use index for the offline Belady OPT analysis (KVR_EVICT_OPT; P:170,
  * SURVEY §8f #1): nu[o] = index of the next query after the one holding block

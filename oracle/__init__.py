@@ -17,5 +17,5 @@ from .binding import (  # noqa: F401
     ROUTE_LBGR_RLS,
     OracleConfig, OraclePolicy, build_oracle, lib,
     fmix64, philox4x32_10, chain, run, single_replay, bruteforce_min_misses, rls_step,
-    rlt_exact_expectation,
+    rlt_exact_expectation, count_collisions,
 )

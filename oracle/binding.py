@@ -83,6 +83,7 @@ def lib():
         L.kvro_fmix64.argtypes = [C.c_uint64]
         L.kvro_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.kvro_chain.argtypes = [C.POINTER(_Trace), C.c_void_p]
+        L.kvro_count_collisions.argtypes = [C.POINTER(_Trace), C.POINTER(C.c_uint64)]
         L.kvro_rls_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double]
         L.kvro_rls_step.restype = None
         L.kvro_run.argtypes = [C.POINTER(_Config), C.POINTER(_Trace), C.POINTER(_Policy),
@@ -187,6 +188,15 @@ def philox4x32_10(ctr: Sequence[int], key: Sequence[int]) -> tuple:
     o = np.zeros(4, dtype=np.uint32)
     lib().kvro_philox4x32_10(c.ctypes.data, k.ctypes.data, o.ctypes.data)
     return tuple(int(v) for v in o)
+
+
+def count_collisions(tr) -> int:
+    a = _TraceArgs(tr)
+    out = C.c_uint64(0)
+    rc = lib().kvro_count_collisions(C.byref(a.c), C.byref(out))
+    if rc:
+        raise ValueError(f"kvro_count_collisions rc={rc}")
+    return int(out.value)
 
 
 def rls_step(P: np.ndarray, theta: np.ndarray, phi, e: float, lam: float):

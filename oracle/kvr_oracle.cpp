@@ -707,6 +707,31 @@ int kvro_chain(const kvro_trace* tr, uint64_t* out) {
   return 0;
 }
 
+// Identity collisions (SURVEY §8a a0 "optional collision check"): list every block
+// occurrence as (identity, occurrence index), sort, and count adjacent pairs with
+// the same identity but a different (depth, parent identity, content key).
+int kvro_count_collisions(const kvro_trace* tr, uint64_t* count) {
+  if (validate_trace(tr) || !count) return 1;
+  const std::vector<uint64_t> H = chain_all(tr);
+  std::vector<std::pair<uint64_t, uint64_t>> occ;
+  std::vector<uint64_t> depth(H.size()), parent(H.size());
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    for (uint64_t o = tr->block_offsets[j]; o < tr->block_offsets[j + 1]; ++o) {
+      depth[o] = o - tr->block_offsets[j];
+      parent[o] = depth[o] ? H[o - 1] : 0;
+      occ.push_back({H[o], o});
+    }
+  std::sort(occ.begin(), occ.end());
+  uint64_t c = 0;
+  for (size_t i = 1; i < occ.size(); ++i) {
+    if (occ[i].first != occ[i - 1].first) continue;
+    const uint64_t a = occ[i - 1].second, b = occ[i].second;
+    if (depth[a] != depth[b] || parent[a] != parent[b] || tr->block_keys[a] != tr->block_keys[b]) c++;
+  }
+  *count = c;
+  return 0;
+}
+
 int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* pol,
              uint64_t K, kvro_result* out, kvro_query_record* records,
              uint64_t* victims, uint64_t victims_cap, uint32_t* hist, int check_invariants) {

@@ -105,6 +105,10 @@ void     kvro_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32
 /* chained block identities of every block of the trace (SURVEY §8c Definitions, A26) */
 int      kvro_chain(const kvro_trace* tr, uint64_t* out_hashes /* [offsets[N]] */);
 
+/* identity collisions: adjacent pairs (in (identity, occurrence) order) with equal
+ * identity but a different (depth, parent identity, content key) */
+int kvro_count_collisions(const kvro_trace* tr, uint64_t* count);
+
 /* one RLS step of the LBGR_RLS residual model (reading A8b): P row-major 4x4,
  * e = target - prediction; exposed for the pins */
 void kvro_rls_step(double P[16], double theta[4], const double phi[4], double e, double lam);

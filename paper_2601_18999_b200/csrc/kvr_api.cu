@@ -254,6 +254,35 @@ kvr_status kvr_trace_build_next_use(const kvr_trace* tr, uint32_t* d_nu, size_t 
   return KVR_OK;
 }
 
+kvr_status kvr_trace_collision_bytes(const kvr_trace* tr, size_t* scratch_bytes) {
+  if (!tr || !scratch_bytes) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  if (tr->total >= 0x7fffffffull) return fail(KVR_ERR_UNSUPPORTED, "collision check needs < 2^31 blocks");
+  cudaError_t e = kvr::collision_scratch_bytes(tr->total, scratch_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "collision scratch size");
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_check_collisions(const kvr_trace* tr, const uint64_t* d_block_keys,
+                                      void* d_scratch, size_t scratch_bytes, void* stream,
+                                      uint64_t* n_collisions) {
+  if (!tr || !n_collisions) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *n_collisions = 0;
+  size_t need = 0;
+  kvr_status st = kvr_trace_collision_bytes(tr, &need);
+  if (st) return st;
+  if (tr->total && (!d_block_keys || !d_scratch))
+    return fail(KVR_ERR_INVALID_ARG, "null block keys / scratch");
+  if (scratch_bytes < need)
+    return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "collision scratch %zu < %zu bytes", scratch_bytes, need);
+  unsigned long long c = 0;
+  cudaError_t e = kvr::count_collisions(tr->hdr, tr->N, tr->hash, d_block_keys, tr->total, d_scratch,
+                                        scratch_bytes, (cudaStream_t)stream, &c);
+  if (e != cudaSuccess) return cuda_fail(e, "collision check");
+  *n_collisions = c;
+  if (c) return fail(KVR_ERR_HASH_COLLISION, "%llu colliding identity pairs: reload with another hash_salt", c);
+  return KVR_OK;
+}
+
 kvr_status kvr_trace_destroy(kvr_trace* tr) {
   delete tr;
   return KVR_OK;

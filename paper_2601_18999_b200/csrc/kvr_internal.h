@@ -228,6 +228,12 @@ cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cuda
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);
 cudaError_t build_next_use(const QueryHdr* hdr, uint32_t N, const uint64_t* hash, uint64_t n,
                            uint32_t* nu, void* scratch, size_t scratch_bytes, cudaStream_t s);
+// identity collision check (kvr_nextuse.cu): adjacent equal identities with a
+// different (depth, parent identity, content key) after the (identity, occurrence) sort
+cudaError_t collision_scratch_bytes(uint64_t n_blocks, size_t* bytes);
+cudaError_t count_collisions(const QueryHdr* hdr, uint32_t N, const uint64_t* hash,
+                             const uint64_t* block_keys, uint64_t n, void* scratch,
+                             size_t scratch_bytes, cudaStream_t s, unsigned long long* h_count);
 // phase profiler (profiling build, -DKVR_PHASE_PROFILE); cudaErrorNotSupported otherwise
 cudaError_t phase_cycles(unsigned long long* out16, int reset);
 

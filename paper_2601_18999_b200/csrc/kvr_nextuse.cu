@@ -68,7 +68,67 @@ cudaError_t layout(uint64_t n, ScratchLayout* L) {
   return cudaSuccess;
 }
 
+// Identity collision check: after the (identity, occurrence) sort,
+// adjacent occurrences with equal identity must carry the same (depth, parent
+// identity, content key) -- the tuple that legitimately determines the identity
+// (reading A26).  Counts the adjacent pairs that do not.
+__global__ void collision_kernel(const uint64_t* key_sorted, const uint32_t* occ_sorted,
+                                 const uint32_t* qidx, const QueryHdr* hdr, const uint64_t* hash,
+                                 const uint64_t* block_keys, uint64_t n,
+                                 unsigned long long* count) {
+  unsigned long long c = 0;
+  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (key_sorted[i] != key_sorted[i - 1]) continue;
+    const uint32_t a = occ_sorted[i - 1], b = occ_sorted[i];
+    const uint64_t da = a - hdr[qidx[a]].block_off, db = b - hdr[qidx[b]].block_off;
+    const uint64_t pa = da ? hash[a - 1] : 0, pb = db ? hash[b - 1] : 0;
+    if (da != db || pa != pb || block_keys[a] != block_keys[b]) c++;
+  }
+  if (c) atomicAdd(count, c);
+}
+
 }  // namespace
+
+cudaError_t collision_scratch_bytes(uint64_t n_blocks, size_t* bytes) {
+  ScratchLayout L;
+  cudaError_t e = layout(n_blocks, &L);
+  if (e == cudaSuccess) *bytes = L.total + kAlign;   // + the counter
+  return e;
+}
+
+cudaError_t count_collisions(const QueryHdr* hdr, uint32_t N, const uint64_t* hash,
+                             const uint64_t* block_keys, uint64_t n, void* scratch,
+                             size_t scratch_bytes, cudaStream_t s, unsigned long long* h_count) {
+  *h_count = 0;
+  if (n < 2) return cudaSuccess;
+  ScratchLayout L;
+  cudaError_t e = layout(n, &L);
+  if (e != cudaSuccess) return e;
+  if (scratch_bytes < L.total + kAlign) return cudaErrorInvalidValue;
+  uint8_t* b = static_cast<uint8_t*>(scratch);
+  uint64_t* keys_out = reinterpret_cast<uint64_t*>(b + L.keys_out);
+  uint32_t* occ_in = reinterpret_cast<uint32_t*>(b + L.occ_in);
+  uint32_t* occ_out = reinterpret_cast<uint32_t*>(b + L.occ_out);
+  uint32_t* qidx = reinterpret_cast<uint32_t*>(b + L.qidx);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(b + L.total);
+  const int threads = 256;
+  const int grid = (int)std::min<uint64_t>((n + threads - 1) / threads, 148ull * 16);
+  e = cudaMemsetAsync(cnt, 0, 8, s);
+  if (e != cudaSuccess) return e;
+  occurrence_query_kernel<<<(N + 7) / 8, 256, 0, s>>>(hdr, N, qidx);
+  iota_kernel<<<grid, threads, 0, s>>>(occ_in, n);
+  size_t cub_bytes = L.total - L.cub;
+  e = cub::DeviceRadixSort::SortPairs(b + L.cub, cub_bytes, hash, keys_out, occ_in, occ_out, (int)n,
+                                      0, 64, s);
+  if (e != cudaSuccess) return e;
+  collision_kernel<<<grid, threads, 0, s>>>(keys_out, occ_out, qidx, hdr, hash, block_keys, n, cnt);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(h_count, cnt, 8, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
 
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes) {
   ScratchLayout L;

@@ -26,11 +26,14 @@ RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
 ROUTE_LBGR_RLS = 5   # LBGR, RLS reading of the 0.992 update (A8b)
 TRIAL_OK, TRIAL_RING_OVERFLOW, TRIAL_VICTIM_LOG_FULL, TRIAL_BAD_POLICY = 0, 1, 2, 3
+TRIAL_ADMISSION = 4
+ERR_HASH_COLLISION = 4
 
 # C-ABI entry points declared in include/kvr.h (the not-gpu test checks they are exported)
 EXPORTS = ("kvr_last_error", "kvr_abi_version", "kvr_trace_packed_bytes", "kvr_trace_load",
            "kvr_trace_info", "kvr_trace_chained_hashes", "kvr_trace_destroy",
-           "kvr_trace_next_use_bytes", "kvr_trace_build_next_use", "kvr_sim_create",
+           "kvr_trace_next_use_bytes", "kvr_trace_build_next_use", "kvr_trace_collision_bytes",
+           "kvr_trace_check_collisions", "kvr_sim_create",
            "kvr_sim_destroy", "kvr_sim_plan", "kvr_sim_workspace_bytes",
            "kvr_sim_workspace_bytes_multi", "kvr_sim_run", "kvr_sim_run_multi")
 
@@ -111,6 +114,8 @@ def lib():
             "kvr_trace_chained_hashes": [vp, vp],
             "kvr_trace_destroy": [vp],
             "kvr_trace_next_use_bytes": [vp, vp, vp],
+            "kvr_trace_collision_bytes": [vp, vp],
+            "kvr_trace_check_collisions": [vp, vp, vp, C.c_size_t, vp, vp],
             "kvr_trace_build_next_use": [vp, vp, C.c_size_t, vp, C.c_size_t, vp, vp],
             "kvr_sim_create": [vp, vp],
             "kvr_sim_destroy": [vp],
@@ -189,6 +194,22 @@ def kvr_trace_next_use_bytes(handle: int):
     a, b = C.c_size_t(0), C.c_size_t(0)
     _check(lib().kvr_trace_next_use_bytes(handle, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def kvr_trace_collision_bytes(handle: int) -> int:
+    a = C.c_size_t(0)
+    _check(lib().kvr_trace_collision_bytes(handle, C.byref(a)))
+    return a.value
+
+
+def kvr_trace_check_collisions(handle: int, block_keys, scratch, stream=None):
+    """Returns (status, n_collisions); status KVR_ERR_HASH_COLLISION (4) is not raised."""
+    n = C.c_uint64(0)
+    st = lib().kvr_trace_check_collisions(handle, _ptr(block_keys), _ptr(scratch), scratch.numel(),
+                                          _stream_ptr(stream), C.byref(n))
+    if st not in (0, ERR_HASH_COLLISION):
+        _check(st)
+    return st, n.value
 
 
 def kvr_trace_build_next_use(handle: int, nu, scratch, stream=None) -> int:
@@ -374,6 +395,13 @@ class DeviceTrace:
         h = self.packed[off: off + 8 * n].view(torch.int64)
         pos = torch.arange(1, n + 1, dtype=torch.int64, device=h.device)
         return int((h.sum() + (h ^ (pos * 0x5851F42D4C957F2D)).sum()).item()) & 0xFFFFFFFFFFFFFFFF
+
+    def collisions(self, stream=None) -> int:
+        """Identity collision pairs of the loaded trace (kvr_trace_check_collisions); 0 = none."""
+        import torch
+        nb = kvr_trace_collision_bytes(self.handle)
+        scratch = torch.empty(max(1, nb), dtype=torch.uint8, device=self.device)
+        return kvr_trace_check_collisions(self.handle, self.keys, scratch, stream)[1]
 
     def with_next_use(self, stream=None) -> "DeviceTrace":
         """A trace handle that also carries the next-use index (offline OPT,

@@ -35,7 +35,7 @@ def test_header_declares_the_north_star_entry_points():
 def test_library_exports_every_declared_symbol(libkvr):
     for name in _declared():
         assert hasattr(libkvr, name), name
-    assert libkvr.kvr_abi_version() == 5
+    assert libkvr.kvr_abi_version() == 6
 
 
 def test_struct_sizes_match_header(libkvr):

@@ -188,3 +188,23 @@ def test_identity_digest(kvr, oracle_mod):
     assert a == b and a != 0
     tr.hash_salt = 99
     assert DeviceTrace(tr).identity_digest() != a
+
+
+def test_collision_check(kvr, oracle_mod):
+    """kvr_trace_check_collisions (device sort + adjacent compare) vs the oracle's
+    count on a crafted genuine collision, after re-salting, and on normal traces."""
+    from collision_util import colliding_pair
+    from paper_2601_18999_b200.kvr import (DeviceTrace, ERR_HASH_COLLISION, kvr_trace_check_collisions,
+                                           kvr_trace_collision_bytes)
+    import torch
+    b2 = colliding_pair(11, 12, 13)
+    tr = wl.from_paths([[11, 12], [13, b2], [11, 12, 5]], n_out=[0, 0, 1])
+    dt = DeviceTrace(tr)
+    scratch = torch.empty(kvr_trace_collision_bytes(dt.handle), dtype=torch.uint8, device="cuda")
+    st, n = kvr_trace_check_collisions(dt.handle, dt.keys, scratch)
+    assert st == ERR_HASH_COLLISION and n == oracle_mod.count_collisions(tr) == 2
+    tr.hash_salt = 77
+    assert DeviceTrace(tr).collisions() == oracle_mod.count_collisions(tr) == 0
+    for t in (wl.gsp(40, 30, 0.5, seed=1), wl.mt(24, 0.9, seed=2), wl.from_paths([[1]]),
+              wl.from_paths([])):
+        assert DeviceTrace(t).collisions() == 0

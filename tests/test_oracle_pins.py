@@ -503,3 +503,25 @@ def test_p24_tracker_grain_reduces_to_no_hit_term(oracle_mod):
     c = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy(tracker_grain=1, tracker_lag=0))
     d = _record_run(oracle_mod, tr, 4, 512, oracle_mod.OraclePolicy())
     assert c.result["decision_digest"] == d.result["decision_digest"]
+
+
+# -------------------------------------------------------------------------- P30
+def test_p30_collision_check(oracle_mod):
+    """Identity collision check: a crafted genuine 64-bit collision of
+    two different depth-2 prefixes (tests/collision_util.py) is found -- the chain
+    really gives both the same identity -- and normal traces report none."""
+    from collision_util import colliding_pair, fmix64, fmix64_inv
+    for x in (0, 1, 0xDEADBEEF, (1 << 64) - 1):
+        assert fmix64_inv(fmix64(x)) == x and oracle_mod.fmix64(x) == fmix64(x)
+    a1, a2, b1 = 11, 12, 13
+    b2 = colliding_pair(a1, a2, b1)
+    tr = wl.from_paths([[a1, a2], [b1, b2], [a1, a2, 5]], n_out=[0, 0, 1])
+    H = oracle_mod.chain(tr)
+    assert H[1] == H[3] and H[0] != H[2]              # one identity, two prefixes
+    # occurrences of that identity, in CSR order: [a1,a2]@1, [b1,b2]@3, [a1,a2,..]@5
+    # -> adjacent pairs (1,3) and (3,5) differ in parent/key: 2 collisions
+    assert oracle_mod.count_collisions(tr) == 2
+    tr.hash_salt = 77                                  # re-salting dissolves it
+    assert oracle_mod.count_collisions(tr) == 0
+    for t in (wl.gsp(20, 10, 0.5, seed=1), wl.mt(12, 0.5, seed=2), wl.random_tree(300, 3)):
+        assert oracle_mod.count_collisions(t) == 0
