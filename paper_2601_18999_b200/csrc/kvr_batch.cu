@@ -89,6 +89,22 @@ __device__ __forceinline__ void t_insert(const BView<Idx>& S, uint64_t t, uint32
   while (S.table[i] != BView<Idx>::NIL) i = (i + 1) & S.tmask;
   S.table[i] = (Idx)slot;
 }
+// concurrent insert: lanes claim EMPTY entries with compare-and-swap
+__device__ __forceinline__ bool cas_claim(uint16_t* e, uint32_t slot) {
+  return atomicCAS(reinterpret_cast<unsigned short*>(e), (unsigned short)0xffffu,
+                   (unsigned short)slot) == (unsigned short)0xffffu;
+}
+__device__ __forceinline__ bool cas_claim(uint32_t* e, uint32_t slot) {
+  return atomicCAS(e, 0xffffffffu, slot) == 0xffffffffu;
+}
+template <typename Idx>
+__device__ __forceinline__ void t_insert_cas(const BView<Idx>& S, uint64_t t, uint32_t slot) {
+  uint32_t i = (uint32_t)t & S.tmask;
+  for (;;) {
+    if (S.table[i] == BView<Idx>::NIL && cas_claim(&S.table[i], slot)) return;
+    i = (i + 1) & S.tmask;
+  }
+}
 template <typename Idx>
 __device__ __forceinline__ void t_erase(const BView<Idx>& S, uint64_t t) {
   uint32_t i = (uint32_t)t & S.tmask;
@@ -254,9 +270,19 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
       break;
     }
   }
+  // Serial part: the (rare) hit steps around a mark reset, then the misses.  Table
+  // inserts of the loaded blocks are deferred to one lane-parallel pass after the
+  // loop (no lookup happens inside a miss run); gam[d] then holds block d's slot.
+  // RLT keeps |U| incrementally (a victim leaves U, its parent may join) and draws
+  // from a batch of 32 consecutive Philox counters computed lane-parallel.
+  const uint32_t d_miss0 = hitrun ? n : d;   // first block known to miss (if any)
+  uint32_t d_ins0 = n;                       // first block whose insert is deferred
+  int32_t nU_known = -1;                     // |U| when known, -1 = recount
+  uint64_t rbatch = 0, rbase = 0;            // draws for counters rbase .. rbase+31
+  bool rvalid = false;
   for (; d < n; ++d) {
     const uint64_t t = S.gam[d];
-    uint32_t s = hitrun ? t_find(S, t) : kNone;
+    uint32_t s = (hitrun && d < d_miss0) ? t_find(S, t) : kNone;
     if (s == kNone) hitrun = false;
     // Alg. 1 l.6-9: mark t; the (B+1)-th distinct mark resets T to {t}
     if (T.rlt) {
@@ -267,6 +293,7 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
           __syncwarp();
           x.cntT = 1;
           x.c[4]++;
+          nU_known = -1;
         } else {
           x.cntT++;
         }
@@ -286,17 +313,20 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
       prev = s;
       continue;
     }
+    if (d_ins0 == n) d_ins0 = d;
     uint32_t slot;
     if (x.size == B) {
       // choose the victim among unpinned leaves (A30, A33): LEAFU bitmap
       uint32_t v = kNone;
       bool use_lru = !T.rlt;
+      bool via_u = false;      // v drawn from U = LEAFU \ T (the incremental count applies)
       if (T.rlt) {
-        bool mark_ok = true;    // RLT: U = LEAFU \ T
-        uint32_t nU = cand_count(S, T, true);
+        bool mark_ok = true;
+        uint32_t nU = nU_known >= 0 ? (uint32_t)nU_known : cand_count(S, T, true);
         if (nU == 0) {   // A5: U empty
           x.c[5]++;
           mark_ok = false;
+          nU_known = -1;
           if (pol.rlt_fallback == KVR_RLT_EARLY_RESET) {
             for (uint32_t w = lane; w < T.nwords; w += 32) S.markb[w] = 0;
             __syncwarp();
@@ -308,11 +338,18 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
           if (!use_lru) nU = cand_count(S, T, false);
         }
         if (!use_lru && nU > 0) {
-          // Alg. 1 l.15: uniform over U in physical-slot order (A6)
-          const uint64_t r = philox_r64(T.K, x.e, T.i, 1);
+          // Alg. 1 l.15: uniform over U in physical-slot order (A6); counter x.e
+          if (!rvalid || x.e - rbase >= 32) {
+            rvalid = true;
+            rbase = x.e;
+            rbatch = philox_r64(T.K, rbase + lane, T.i, 1);
+          }
+          const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
           x.e++;
           x.c[3]++;
           v = cand_select(S, T, mark_ok, (uint32_t)pick_index(r, nU));
+          via_u = mark_ok;
+          if (mark_ok) nU_known = (int32_t)nU;
         }
       }
       if (use_lru) {   // least (stamp, -depth) among unpinned leaves
@@ -334,14 +371,17 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
       // Evict(S, v): table delete, parent child count (+ LEAFU), T \ {v}
       const uint64_t hv = S.key[v];
       if (bit_test(S.markb, v)) x.cntT--;
+      const uint32_t pa = S.parent[v];
+      const bool has_pa = pa != BView<Idx>::NIL;
+      const uint32_t nc = has_pa ? S.nchild[pa] - 1u : 1u;
+      const bool pa_leafu = has_pa && nc == 0 && S.pin[pa] == 0;   // parent joins LEAFU
+      if (via_u) nU_known = nU_known - 1 + ((pa_leafu && !bit_test(S.markb, pa)) ? 1 : 0);
       __syncwarp();
       if (lane == 0) {
         t_erase(S, hv);
-        const uint32_t pa = S.parent[v];
-        if (pa != BView<Idx>::NIL) {
-          const uint32_t nc = S.nchild[pa] - 1u;
+        if (has_pa) {
           S.nchild[pa] = (Idx)nc;
-          if (nc == 0 && S.pin[pa] == 0) S.leafu[pa >> 5] |= 1u << (pa & 31);
+          if (pa_leafu) S.leafu[pa >> 5] |= 1u << (pa & 31);
         }
         S.markb[v >> 5] &= ~(1u << (v & 31));
         S.leafu[v >> 5] &= ~(1u << (v & 31));
@@ -362,7 +402,8 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
     } else {
       slot = x.size++;
     }
-    // Load(S, t): pinned (not in LEAFU), stamped, marked under RLT (t in T after l.6-9)
+    // Load(S, t): pinned (not in LEAFU), stamped, marked under RLT (t in T after
+    // l.6-9); the table insert is deferred (gam[d] <- slot)
     if (lane == 0) {
       S.key[slot] = t;
       S.parent[slot] = (Idx)prev;           // kNone -> NIL (root child)
@@ -371,13 +412,19 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
       S.depth[slot] = (Idx)(d + 1);
       S.pin[slot] = 1;
       if (T.rlt) S.markb[slot >> 5] |= 1u << (slot & 31);
-      t_insert(S, t, slot);
+      S.gam[d] = slot;
       if (prev != kNone) S.nchild[prev] = (Idx)(S.nchild[prev] + 1);   // prev is pinned: never in LEAFU
     }
     __syncwarp();
     x.c[1]++;
     prev = slot;
   }
+  // deferred table inserts, lane-parallel (linear probing, CAS-claimed entries)
+  for (uint32_t q = d_ins0 + lane; q < n; q += 32) {
+    const uint32_t slot = (uint32_t)S.gam[q];
+    t_insert_cas(S, S.key[slot], slot);
+  }
+  __syncwarp();
   *nvict = nv;
   *Vout = V;
   return m;
