@@ -11,7 +11,7 @@
  * P:115-122) with RLT or Leaf-LRU, and the queue load / latency /
  * TTFT are accounted (Eq. 1-2; Eq. 6).  The exact
  * operation order and every reading of an under-specified passage are listed
- * in DESIGN.md §3 (ids A1..A28).
+ * in DESIGN.md §3 (ids A1..A36).
  *
  * Conventions
  *   - Every function returns kvr_status (0 = OK) and never throws or exits;

@@ -9,7 +9,7 @@
  * below is duplicated on purpose.
  *
  * Citation keys: P:n = PAPER.md line n (paper_2601_18999), SURVEY §8(c) = the
- * operation order and the ambiguity readings A1..A27 listed in DESIGN.md.
+ * operation order and the ambiguity readings A1..A36 listed in DESIGN.md.
  *
  * What it computes (one replay = one "trial"):
  *   per query j (trace order), t = a_j

@@ -1,5 +1,5 @@
 // kvr_internal.h — layouts shared by the host API (kvr_api.cu) and the kernels
-// (kvr_pack.cu, kvr_replay.cu).  Not part of the public ABI (include/kvr.h).
+// (kvr_pack.cu, kvr_kernel.cu, kvr_batch.cu, kvr_nextuse.cu).  Not part of the public ABI (include/kvr.h).
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -212,7 +212,7 @@ inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
          divtab_bytes(max_n);
 }
 
-// launchers (kvr_pack.cu / kvr_replay.cu)
+// launchers (kvr_pack.cu / kvr_kernel.cu)
 cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, uint32_t* scratch,
                         cudaStream_t s);
 // tier 1 = tables in shared memory (u16 slot ids), 2 = tables in global memory (u32 slot ids)
