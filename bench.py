@@ -256,10 +256,25 @@ def main():
     import torch.distributed as dist
     from paper_2601_18999_b200.kvr import DeviceTrace, Policy, Simulator, policies_array
 
+    # KVR_BENCH_BACKEND=gloo (tests only): several ranks on one GPU, collectives staged
+    # through host copies; the contract run uses NCCL, one rank per GPU
+    backend = os.environ.get("KVR_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def coll(fn, t, **kw):
+        if backend != "gloo":
+            return fn(t, **kw)
+        h = t.cpu()
+        fn(h, **kw)
+        t.copy_(h)
 
     traces = build_traces(args.queries)
     trace_of, evict, keys = trial_plan(rank, args.trials)
@@ -289,7 +304,7 @@ def main():
         sim.launch(dts, n_trials, buf, with_policies=True, stream=stream)
         if world > 1:   # the single NCCL reduce of summary counters
             vec = kdist.summary_tensor(buf["results"], n_trials, trace_hash)
-            dist.reduce(vec, dst=0)
+            coll(dist.reduce, vec, dst=0)
             summary[0] = vec
         e1.record(stream)
         torch.cuda.synchronize()
@@ -307,10 +322,15 @@ def main():
     t_local = float(np.sum(times))
     tmax = torch.tensor([t_local], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        coll(dist.all_reduce, tmax, op=dist.ReduceOp.MAX)
     t_max = float(tmax.item())
     q_per_step = float(res["queries"].sum())
-    total_q = q_per_step * args.steps * world
+    if world > 1 and summary[0] is not None:   # all ranks' queries and failed trials
+        red = summary[0].cpu().tolist()
+        q_per_step, bad = float(red[1]), int(red[11])
+    else:
+        q_per_step *= world
+    total_q = q_per_step * args.steps
     value = total_q / (t_max / 1000.0)
 
     # roofline of the dominant kernel (the replay kernel is the whole step)
@@ -359,10 +379,10 @@ def main():
         e = e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args)
         if world > 1:
             t = torch.tensor([e["ms_per_step"]], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            coll(dist.all_reduce, t, op=dist.ReduceOp.MAX)
             c = torch.tensor([e["queries_per_step"], e["h2d_bytes_per_step"], e["d2h_bytes_per_step"]],
                              dtype=torch.float64, device=dev)
-            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            coll(dist.all_reduce, c, op=dist.ReduceOp.SUM)
             e["ms_per_step"] = float(t[0])
             e["queries_per_step"], e["h2d_bytes_per_step"], e["d2h_bytes_per_step"] = \
                 float(c[0]), int(c[1]), int(c[2])

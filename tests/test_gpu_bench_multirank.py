@@ -1,0 +1,35 @@
+"""bench.py's multi-rank path end to end on one GPU: two ranks under torchrun share the
+device (KVR_BENCH_BACKEND=gloo stages the collectives through host copies).  Checks
+the contract line: whole-job value over both ranks, max-over-ranks time, the summary
+reduce with the packed-trace checksum, and e2e aggregated over ranks."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_bench_two_ranks_one_gpu():
+    env = dict(os.environ, KVR_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--queries", "3000", "--trials", "64",
+           "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["trial_status_nonzero"] == 0
+    rs = d["reduced_summary"]
+    assert rs["trials"] == 128 and rs["queries"] == 128 * 3000
+    assert rs["trace_hash_consistent"] is True and rs["status_nonzero"] == 0
+    # value = both ranks' query-replays over the slowest rank's time
+    assert abs(d["value"] - 128 * 3000 / (d["ms_per_step"] / 1e3)) <= 1e-6 * d["value"]
+    e = d["e2e"]
+    assert abs(e["value"] - e["queries_per_step"] / (e["ms_per_step"] / 1e3)) <= 1e-6 * e["value"]
+    assert e["queries_per_step"] == 128 * 3000
