@@ -97,3 +97,29 @@ def test_lean_kernel_refuses_extended_policies(kvr):
     out = sim.collect(b, 3)
     assert list(out.results["status"]) == [3, 3, 0]
     assert not sim.cfg.extended_policies
+
+
+def test_closed_form_routing_p31(kvr, oracle_mod):
+    """P31's closed forms through the GPU: cache-aware herding (all on worker 0, hit
+    tokens 16 * sum_g (Q-1) p_g) and join-shortest-queue (worker j mod W)."""
+    from paper_2601_18999_b200 import workloads as wl
+    from parity_util import compare
+    G, Q, p, u = 5, 6, (3, 5, 2, 7, 4), 3
+
+    def trace(spacing):
+        paths = []
+        for k in range(Q):
+            for g in range(G):
+                paths.append([1000 * (g + 1) + d for d in range(p[g])] +
+                             [10 ** 6 + 100 * (k * G + g) + d for d in range(u)])
+        return wl.from_paths(paths, arrival_ms=[spacing * j for j in range(len(paths))])
+
+    herd = [kvr.Policy(router=2, tau=1e300, eviction=1), kvr.Policy(router=1, w_load=0.0, w_hit=1.0)]
+    out, _ = compare(oracle_mod, kvr, trace(1.0e5), 4, 1000, herd, [3, 4], ring=64)
+    for t in range(2):
+        assert np.all(out.records[t]["worker"][:G * Q] == 0)
+        assert int(out.results[t]["hit_tokens"]) == 16 * sum((Q - 1) * pg for pg in p)
+    jsq = [kvr.Policy(router=2, tau=0.0, eviction=0), kvr.Policy(router=1, w_load=1.0, w_hit=0.0)]
+    out, _ = compare(oracle_mod, kvr, trace(0.0), 3, 1000, jsq, [5, 6], ring=64)
+    for t in range(2):
+        assert np.all(out.records[t]["worker"][:G * Q] == np.arange(G * Q) % 3)

@@ -525,3 +525,44 @@ def test_p30_collision_check(oracle_mod):
     assert oracle_mod.count_collisions(tr) == 0
     for t in (wl.gsp(20, 10, 0.5, seed=1), wl.mt(12, 0.5, seed=2), wl.random_tree(300, 3)):
         assert oracle_mod.count_collisions(t) == 0
+
+
+# -------------------------------------------------------------------------- P31
+def _groups_trace(G=5, Q=6, p=(3, 5, 2, 7, 4), u=3, spacing=1.0e5):
+    """G groups, group g's queries share a p[g]-block prefix then u unique blocks;
+    queries interleaved g = 0..G-1 round after round."""
+    paths = []
+    for k in range(Q):
+        for g in range(G):
+            paths.append([1000 * (g + 1) + d for d in range(p[g])] +
+                         [10 ** 6 + 100 * (k * G + g) + d for d in range(u)])
+    return wl.from_paths(paths, arrival_ms=[spacing * j for j in range(len(paths))]), p, G, Q
+
+
+@pytest.mark.parametrize("router,kw", [(2, dict(tau=1e300)), (1, dict(w_load=0.0, w_hit=1.0))])
+def test_p31_cache_aware_herding(oracle_mod, router, kw):
+    """Pure cache affinity (THRESHOLD that never balances, STATIC without a load term)
+    is greedy argmax-h with lowest-index ties: every query lands on worker 0, which
+    then holds every group's prefix -> hit tokens = 16 * sum_g (Q-1) p_g (no
+    evictions at ample B).  The load imbalance cache-aware routing risks."""
+    tr, p, G, Q = _groups_trace()
+    cfg = oracle_mod.OracleConfig(W=4, capacity_blocks=1000, pending_ring=0)
+    r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(router=router, eviction=1, **kw), 3,
+                       record=True, check_invariants=True)
+    assert np.all(r.records["worker"] == 0)
+    assert r.result["hit_tokens"] == 16 * sum((Q - 1) * pg for pg in p)
+    assert r.result["evictions"] == 0
+    assert r.result["sum_load_ms"] == r.result["makespan_ms"]     # one loaded worker
+
+
+@pytest.mark.parametrize("router,kw", [(2, dict(tau=0.0)), (1, dict(w_load=1.0, w_hit=0.0))])
+@pytest.mark.parametrize("W", [2, 3, 5])
+def test_p31_join_shortest_queue(oracle_mod, router, kw, W):
+    """All a_j = 0, so nothing completes: pure load balancing on pending counts
+    (THRESHOLD with tau = 0, STATIC without a hit term) is join-the-shortest-queue
+    with lowest-index ties, i.e. worker j mod W."""
+    tr, _, _, _ = _groups_trace(spacing=0.0)
+    cfg = oracle_mod.OracleConfig(W=W, capacity_blocks=1000, pending_ring=0)
+    r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(router=router, eviction=0, **kw), 3,
+                       record=True, check_invariants=True)
+    assert np.all(r.records["worker"] == np.arange(tr.n_queries) % W)
