@@ -544,7 +544,7 @@ def test_p31_cache_aware_herding(oracle_mod, router, kw):
     """Pure cache affinity (THRESHOLD that never balances, STATIC without a load term)
     is greedy argmax-h with lowest-index ties: every query lands on worker 0, which
     then holds every group's prefix -> hit tokens = 16 * sum_g (Q-1) p_g (no
-    evictions at ample B).  The load imbalance cache-aware routing risks."""
+    evictions at ample B).  The heuristics of P:41 at their hit-rate extreme."""
     tr, p, G, Q = _groups_trace()
     cfg = oracle_mod.OracleConfig(W=4, capacity_blocks=1000, pending_ring=0)
     r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(router=router, eviction=1, **kw), 3,
