@@ -146,12 +146,13 @@ def peaks():
     return p
 
 
-def run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads):
+def run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads, beta=0):
     """CPU oracle (as it stands) on host cores: `threads` trials, each on the first
     n_prefix queries of its trace.  Returns (query-replays, seconds, threads)."""
     import oracle
     from concurrent.futures import ThreadPoolExecutor
-    cfg = oracle.OracleConfig(W=W_WORKERS, capacity_blocks=B_BLOCKS, pending_ring=RING)
+    cfg = oracle.OracleConfig(W=W_WORKERS, capacity_blocks=B_BLOCKS, pending_ring=RING,
+                              batch_slots=beta)
     prefixes = [t.prefix(n_prefix) for t in traces]
 
     def one(i):
@@ -186,10 +187,11 @@ def reference_arm(args, rank, world):
     threads = max(1, min(os.cpu_count() or 1, 16))
     n_prefix = args.ref_queries
     for _ in range(args.warmup):
-        run_oracle_sample(traces, trace_of, evict, keys, max(50, n_prefix // 10), threads)
+        run_oracle_sample(traces, trace_of, evict, keys, max(50, n_prefix // 10), threads,
+                          args.batch_slots)
     tot_q, tot_s = 0, 0.0
     for _ in range(args.steps):
-        q, s = run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads)
+        q, s = run_oracle_sample(traces, trace_of, evict, keys, n_prefix, threads, args.batch_slots)
         tot_q += q
         tot_s += s
     v = tot_q / tot_s
@@ -206,8 +208,10 @@ def reference_arm(args, rank, world):
 
 
 def config_json(args):
+    beta = getattr(args, "batch_slots", 0)
+    extra = (f", continuous batching beta={beta} (SURVEY 8f #2, update at dequeue)" if beta else "")
     return {"workload": "config2: W=8, B=512 blocks, 3 GSP traces (125 groups x 800 queries, "
-                        "128-2048 tokens, prefix ratio 0.3/0.5/0.9), LBGR x {RLT, L-LRU}",
+                        "128-2048 tokens, prefix ratio 0.3/0.5/0.9), LBGR x {RLT, L-LRU}" + extra,
             "replays_per_gpu": TRIALS_PER_GPU, "queries_per_trace": N_QUERIES,
             "block_tokens": 16, "parallelism": f"replica-sharded x{args.gpus}",
             "l2": "inputs larger than L2 (3 packed traces ~250 MB) + 256 MB L2 flush between steps"}
@@ -219,7 +223,8 @@ NCU_CAPTURE = os.path.join(ROOT, "profiles", "r1_bench_replay_ncu.json")
 def ncu_capture(args):
     """DRAM traffic per launch of the replay kernel from the committed `ncu --set full`
     capture of this exact launch (scripts/profile_bench.sh); None for other sizes."""
-    if args.queries != N_QUERIES or args.trials != TRIALS_PER_GPU or not os.path.exists(NCU_CAPTURE):
+    if (args.queries != N_QUERIES or args.trials != TRIALS_PER_GPU or args.batch_slots
+            or not os.path.exists(NCU_CAPTURE)):
         return None
     with open(NCU_CAPTURE) as f:
         d = json.load(f)
@@ -238,6 +243,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--queries", type=int, default=N_QUERIES, help=argparse.SUPPRESS)
     ap.add_argument("--trials", type=int, default=TRIALS_PER_GPU, help=argparse.SUPPRESS)
+    ap.add_argument("--batch-slots", type=int, default=0,
+                    help="0: the beta = 1 model (default, the headline); 1..3: the continuous-"
+                         "batching engine with beta slots per worker (beta * 129 <= B = 512)")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling run: one launch, no warm-up / e2e / cpu baseline")
     args = ap.parse_args()
@@ -282,7 +290,7 @@ def main():
     pols = policies_array([Policy(eviction=int(e)) for e in evict])
     stream = torch.cuda.current_stream()
     dts = [DeviceTrace(t, device=dev) for t in traces]
-    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING)
+    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING, batch_slots=args.batch_slots)
     buf = sim.alloc(dts, n_trials, 0, dev)
     buf["keys"].copy_(torch.from_numpy(keys.view(np.int64)))
     buf["policies"].copy_(torch.from_numpy(pols.view(np.uint8)))
@@ -392,8 +400,9 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         threads = max(1, min(os.cpu_count() or 1, 16))
         nq = args.ref_queries
-        q, s = run_oracle_sample(traces, trace_of, evict, keys, nq, threads)
-        q1, s1 = run_oracle_sample(traces, trace_of, evict, keys, nq, 1)   # one core
+        q, s = run_oracle_sample(traces, trace_of, evict, keys, nq, threads, args.batch_slots)
+        q1, s1 = run_oracle_sample(traces, trace_of, evict, keys, nq, 1,
+                                   args.batch_slots)   # one core
         line["cpu_baseline"] = {"value": q / s, "unit": UNIT, "cores": threads, "kind": "oracle",
                                 "single_core_value": q1 / s1, "nproc": os.cpu_count(),
                                 "cpu_model": cpu_model(),
@@ -406,7 +415,7 @@ def main():
         print(json.dumps(line), flush=True)
 
 
-def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):
+def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):  # noqa: C901
     """Same metric through the public API with HOST buffers: per step the pinned raw
     traces, keys, policies and trial->trace map go host->device, kvr_trace_load packs
     (validates, chains) them, kvr_sim_run_multi replays, and the per-trial results come
@@ -414,7 +423,7 @@ def e2e_measure(traces, trace_of, evict, keys, pols, dev, stream, args):
     import torch
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator
 
-    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING)
+    sim = Simulator(W_WORKERS, B_BLOCKS, pending_ring=RING, batch_slots=args.batch_slots)
     n = len(keys)
     host = [DeviceTrace.pin(t) for t in traces]                     # pinned, outside timing
     h_keys = torch.from_numpy(keys.view(np.int64)).pin_memory()
