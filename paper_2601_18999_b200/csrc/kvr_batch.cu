@@ -162,9 +162,11 @@ struct BW {
   uint32_t size, cntT, nfl, wh, wn;
   uint64_t e, k, vcur;
   double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
-  // counters: probes, inserted, evictions, draws, resets, fallbacks, hit tokens,
-  // input tokens, queries, max pending, digest sum, victim-log overflow
-  unsigned long long c[12];
+  // counters (u32 per worker and trial; tokens counted in blocks): probes, inserted,
+  // evictions, draws, resets, fallbacks, hit blocks, input blocks, queries, max
+  // pending, (unused), victim-log overflow; the digest sum is u64
+  uint32_t c[12];
+  uint64_t dsum;
   bool dead;   // admission failure / violation: stop this worker
 };
 
@@ -463,8 +465,8 @@ __device__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFl
   x.nfl++;
   if (comp > x.F) x.F = comp;
   x.P = x.P + cost;                                                           // Eq. 2
-  x.c[6] += hh;
-  x.c[7] += q;
+  x.c[6] += m;        // hit blocks   (x bt at the end)
+  x.c[7] += n_in;     // input blocks (x bt at the end)
   x.slat = x.slat + lat;
   x.sttft = x.sttft + ttft;
   if (lat > x.mlat) x.mlat = lat;
@@ -474,7 +476,7 @@ __device__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFl
   Tj = fmix64(Tj ^ (uint64_t)m);
   Tj = fmix64(Tj ^ (uint64_t)nv);
   Tj = fmix64(Tj ^ V);
-  x.c[10] += Tj;
+  x.dsum += Tj;
   if (lane == 0) {
     if (T.rec) {
       kvr_query_record& R = T.rec[j];
@@ -678,6 +680,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     x.Pt = 0.0; x.P = 0.0; x.F = 0.0; x.slat = 0.0; x.sttft = 0.0; x.mlat = 0.0;
     x.th0 = pol.theta0[0]; x.th1 = pol.theta0[1]; x.th2 = pol.theta0[2]; x.th3 = pol.theta0[3];
     for (int c = 0; c < 12; ++c) x.c[c] = 0;
+    x.dsum = 0;
     x.dead = false;
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     const uint32_t Nrun = pol_ok ? N : 0;
@@ -857,6 +860,9 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       ctrl->sttft[w] = x.sttft;
       ctrl->mlat[w] = x.mlat;
       for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = x.c[c];
+      ctrl->cnt[w][6] = (unsigned long long)x.c[6] * T.bt;
+      ctrl->cnt[w][7] = (unsigned long long)x.c[7] * T.bt;
+      ctrl->cnt[w][10] = x.dsum;
     }
     __syncthreads();
     if (tid == 0) {
