@@ -200,3 +200,26 @@ def test_multi_trace_launch(kvr, oracle_mod):
         o = oracle_mod.run(cfg, trs[tt[t]], to_oracle_policy(oracle_mod, pols[t]), int(keys[t]))
         assert o.rc == 0
         assert_result_equal(out.results[t], o.result, f"trial {t}")
+
+
+def test_fuzz_random_configs(kvr, oracle_mod):
+    """150 random (W, beta, B, trace, policy, ring, tier) draws, 3 trials each, bit-exact."""
+    rng = np.random.default_rng(2024)
+    for it in range(150):
+        W = int(rng.integers(1, 9))
+        beta = int(rng.integers(1, 5))
+        tr = wl.random_tree(int(rng.integers(20, 120)), 900 + it, max_len=int(rng.integers(2, 9)),
+                            alphabet=int(rng.integers(2, 4)), max_out=int(rng.integers(0, 3)), W=W,
+                            util=float(rng.uniform(0.3, 3.0)))
+        B = beta * int(tr.max_blocks) + int(rng.integers(0, 6))
+        pols = []
+        for _ in range(3):
+            pols.append(kvr.Policy(eviction=int(rng.integers(0, 2)), rlt_fallback=int(rng.integers(0, 3)),
+                                   router=int(rng.integers(0, 6)), tau=float(rng.uniform(1.0, 3.0)),
+                                   w_hit=float(rng.uniform(0, 2)), w_load=float(rng.uniform(0, 2)),
+                                   mu=float(rng.uniform(0.05, 1.0)), rho=float(rng.uniform(0.5, 1.0)),
+                                   delta_t_ms=float(rng.uniform(5, 50))))
+        keys = [int(k) for k in rng.integers(1, 1 << 40, size=3)]
+        compare_batched(oracle_mod, kvr, tr, W, B, beta, pols, keys,
+                        truth=(float(rng.uniform(0, 0.5)), 1.0, float(rng.uniform(0, 5))),
+                        ring=int(rng.integers(4, 64)), force_tier=int(rng.integers(1, 3)))

@@ -208,3 +208,29 @@ def test_collision_check(kvr, oracle_mod):
     for t in (wl.gsp(40, 30, 0.5, seed=1), wl.mt(24, 0.9, seed=2), wl.from_paths([[1]]),
               wl.from_paths([])):
         assert DeviceTrace(t).collisions() == 0
+
+
+def test_fuzz_random_configs(kvr, oracle_mod):
+    """150 random (W, B, trace, policy, ring, tier, histogram) draws of the beta = 1
+    kernel, 3 trials each incl. the extended policies (LBGR_RLS, tracker bias)."""
+    rng = np.random.default_rng(7)
+    for it in range(150):
+        W = int(rng.integers(1, 12))
+        tr = wl.random_tree(int(rng.integers(20, 150)), 3000 + it, max_len=int(rng.integers(2, 9)),
+                            alphabet=int(rng.integers(2, 4)), max_out=int(rng.integers(0, 3)), W=W,
+                            util=float(rng.uniform(0.3, 3.0)))
+        B = int(tr.max_blocks) + int(rng.integers(0, 12))
+        pols = []
+        for _ in range(3):
+            pols.append(kvr.Policy(eviction=int(rng.integers(0, 2)), rlt_fallback=int(rng.integers(0, 3)),
+                                   router=int(rng.integers(0, 6)), tau=float(rng.uniform(1.0, 3.0)),
+                                   w_hit=float(rng.uniform(0, 2)), w_load=float(rng.uniform(0, 2)),
+                                   mu=float(rng.uniform(0.05, 1.0)), rho=float(rng.uniform(0.5, 1.0)),
+                                   delta_t_ms=float(rng.uniform(5, 50)),
+                                   tracker_lag=int(rng.integers(0, 2)),
+                                   tracker_grain=int(rng.integers(1, 4))))
+        keys = [int(k) for k in rng.integers(1, 1 << 40, size=3)]
+        compare(oracle_mod, kvr, tr, W, B, pols, keys,
+                truth=(float(rng.uniform(0, 0.5)), 1.0, float(rng.uniform(0, 5))),
+                ring=int(rng.integers(4, 64)), force_tier=int(rng.integers(1, 3)),
+                bins=int(rng.integers(0, 2)) * 32)
