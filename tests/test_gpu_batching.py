@@ -223,3 +223,26 @@ def test_fuzz_random_configs(kvr, oracle_mod):
         compare_batched(oracle_mod, kvr, tr, W, B, beta, pols, keys,
                         truth=(float(rng.uniform(0, 0.5)), 1.0, float(rng.uniform(0, 5))),
                         ring=int(rng.integers(4, 64)), force_tier=int(rng.integers(1, 3)))
+
+
+def test_fuzz_larger_caches(kvr, oracle_mod):
+    """Batching kernel on random GSP / multi-turn / long-document traces, B up to 2048."""
+    rng = np.random.default_rng(13)
+    for it in range(18):
+        W = int(rng.integers(1, 17))
+        beta = int(rng.integers(1, 4))
+        kind = it % 3
+        if kind == 0:
+            tr = wl.gsp(int(rng.integers(4, 12)), int(rng.integers(3, 10)), float(rng.uniform(0.2, 0.9)),
+                        seed=400 + it, W=W, lengths=(128, 256, 512), util=2.0)
+        elif kind == 1:
+            tr = wl.mt(int(rng.integers(4, 16)), float(rng.uniform(0.2, 0.9)), seed=500 + it, W=W,
+                       user_blocks=int(rng.integers(2, 8)), util=2.0)
+        else:
+            tr = wl.ld(int(rng.integers(4, 12)), int(rng.integers(2, 6)), seed=600 + it, W=W,
+                       lengths=(256, 512), util=2.0)
+        B = max(beta * int(tr.max_blocks), int(rng.integers(64, 2049)))
+        pols = [kvr.Policy(eviction=int(rng.integers(0, 2)), rlt_fallback=int(rng.integers(0, 3)),
+                           router=int(rng.integers(0, 6))) for _ in range(2)]
+        keys = [int(k) for k in rng.integers(1, 1 << 40, size=2)]
+        compare_batched(oracle_mod, kvr, tr, W, B, beta, pols, keys)

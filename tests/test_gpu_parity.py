@@ -234,3 +234,26 @@ def test_fuzz_random_configs(kvr, oracle_mod):
                 truth=(float(rng.uniform(0, 0.5)), 1.0, float(rng.uniform(0, 5))),
                 ring=int(rng.integers(4, 64)), force_tier=int(rng.integers(1, 3)),
                 bins=int(rng.integers(0, 2)) * 32)
+
+
+def test_fuzz_larger_caches(kvr, oracle_mod):
+    """Random GSP / multi-turn / long-document traces at B in [64, 2048] (crossing the
+    1,024-slot register-bitmap / deferred-apply limit) and W in [1, 16], both tiers."""
+    rng = np.random.default_rng(11)
+    for it in range(24):
+        W = int(rng.integers(1, 17))
+        kind = it % 3
+        if kind == 0:
+            tr = wl.gsp(int(rng.integers(4, 12)), int(rng.integers(3, 10)), float(rng.uniform(0.2, 0.9)),
+                        seed=100 + it, W=W, lengths=(128, 256, 512, 1024))
+        elif kind == 1:
+            tr = wl.mt(int(rng.integers(4, 16)), float(rng.uniform(0.2, 0.9)), seed=200 + it, W=W,
+                       user_blocks=int(rng.integers(2, 8)))
+        else:
+            tr = wl.ld(int(rng.integers(4, 12)), int(rng.integers(2, 6)), seed=300 + it, W=W,
+                       lengths=(256, 512, 1024))
+        B = max(int(tr.max_blocks), int(rng.integers(64, 2049)))
+        pols = [kvr.Policy(eviction=int(rng.integers(0, 2)), rlt_fallback=int(rng.integers(0, 3)),
+                           router=int(rng.integers(0, 6))) for _ in range(2)]
+        keys = [int(k) for k in rng.integers(1, 1 << 40, size=2)]
+        compare(oracle_mod, kvr, tr, W, B, pols, keys, force_tier=int(rng.integers(0, 3)))
