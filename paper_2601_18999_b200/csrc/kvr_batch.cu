@@ -230,7 +230,7 @@ __device__ __forceinline__ uint32_t cand_select(const BView<Idx>& S, const BTria
 // P:225-245), pinning every block as it is accessed (A30, A33).
 // Returns the number of leading input hits m, or kNone on an admission failure.
 template <typename Idx>
-__device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t j, uint32_t n,
+__device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t j, uint32_t n,
                              uint32_t n_in, uint32_t* nvict, uint64_t* Vout) {
   const uint32_t lane = T.lane, B = T.B;
   const kvr_policy& pol = *T.pol;
@@ -435,7 +435,7 @@ __device__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32
 // Dequeue r on worker T.i at time s (A30): stage Gamma_j, UpdateCache with
 // pinning, true h, Eq. 1 truth, record/digest/histogram, into a batch slot.
 template <typename Idx>
-__device__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFlight& r, double s) {
+__device__ __forceinline__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFlight& r, double s) {
   const uint32_t j = r.j, lane = T.lane;
   const QueryHdr& h = T.tr.hdr[j];
   const uint32_t n_in = h.n_in, n = h.n_in + h.n_out;
@@ -497,7 +497,7 @@ __device__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, BW& x, const BFl
 // OnlineUpdate (NLMS A8 / RLS A8b) and ReleaseLoad (A10) as in the beta = 1
 // model, unpin Gamma_j, then start the head of the waiting FIFO at c.
 template <typename Idx>
-__device__ bool b_complete(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t b) {
+__device__ __forceinline__ bool b_complete(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t b) {
   const uint32_t lane = T.lane;
   const BFlight r = S.fl[b];
   __syncwarp();
@@ -616,8 +616,11 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
   const BatchLayout& L = p.blay;
   BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem);
   uint8_t* sbase = smem + align16(sizeof(BCtrl));
-  uint8_t* wbase = p.bglobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
-                             : sbase + (size_t)w * L.bytes;
+  // tier 1 (u16 ids) keeps the state in shared memory, tier 2 (u32) in the workspace;
+  // deciding it at compile time lets the compiler use 32-bit shared addressing (LDS/STS)
+  uint8_t* wbase;
+  if constexpr (sizeof(Idx) == 4) wbase = p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes;
+  else wbase = sbase + (size_t)w * L.bytes;
   const BView<Idx> S = bview<Idx>(wbase, L);
 
 #pragma unroll 1
