@@ -194,6 +194,13 @@ void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
           if (!best || lru_less(kv.second, *best)) { best = &kv.second; v = kv.first; found = true; }
         }
         if (found && C.S[v].nchild != 0) x.invariant_violation = true;
+        if (found && x.pinning) {
+          // under pinning the minimum over ALL unpinned nodes is that leaf too (a
+          // child's stamp never exceeds its parent's; an unpinned node's children
+          // are unpinned) -- the basis of a one-selection Leaf-LRU
+          for (auto& kv : C.S)
+            if (kv.second.pin == 0 && lru_less(kv.second, C.S[v])) x.invariant_violation = true;
+        }
       } else if (x.eviction == KVRO_EVICT_RLT) {
         // U = leaf tokens \ T, excluding parent(t) (A4)
         std::vector<std::pair<uint32_t, uint64_t>> U;  // (slot, id)
