@@ -704,12 +704,11 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
         for (;;) {
           double c;
           const uint32_t b = b_next(S, x, &c);
-          if (T.lbgr) {
-            const double tau = (double)(x.k + 1) * dt;
-            if (tau <= t && tau <= c) {
+          if (T.lbgr) {   // every tick up to min(a_j, next completion): tick first on ties
+            const double lim = c < t ? c : t;
+            while ((double)(x.k + 1) * dt <= lim) {
               x.Pt = rho * x.Pt;
               x.k++;
-              continue;
             }
           }
           if (b != kNone && c <= t) {
