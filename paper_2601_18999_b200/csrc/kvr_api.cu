@@ -113,7 +113,7 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   pl->tier = tier;
   pl->blay = tier == 1 ? l16 : l32;
   pl->smem = tier == 1 ? smem1 : ctrl;
-  cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W, tier == 2);
+  cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W, tier == 2, c.capacity_blocks);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query (batching kernel)");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "batching kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();

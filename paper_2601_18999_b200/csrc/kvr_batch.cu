@@ -53,8 +53,30 @@ struct BView {
   uint32_t tmask;
 };
 
-template <typename Idx>
-__device__ __forceinline__ BView<Idx> bview(uint8_t* base, const BatchLayout& L) {
+// kFixedB > 0: the capacity is a compile-time constant (B = 512, every BASELINE config
+// that replays W > 1 workers), so the offsets of the fixed-size arrays fold into the
+// shared-memory instructions instead of being rematerialised from the parameters
+template <typename Idx, int kFixedB>
+__device__ __forceinline__ BView<Idx> bview(uint8_t* base, const BatchLayout& Lr) {
+  constexpr BatchLayout LF = make_batch_layout(kFixedB > 0 ? kFixedB : 64, 1, 1, sizeof(Idx));
+  const BatchLayout& L = Lr;
+  if constexpr (kFixedB > 0) {
+    BView<Idx> v;
+    v.key = reinterpret_cast<uint64_t*>(base + LF.off_key);
+    v.stamp = reinterpret_cast<uint32_t*>(base + LF.off_stamp);
+    v.parent = reinterpret_cast<Idx*>(base + LF.off_parent);
+    v.nchild = reinterpret_cast<Idx*>(base + LF.off_nchild);
+    v.depth = reinterpret_cast<Idx*>(base + LF.off_depth);
+    v.table = reinterpret_cast<Idx*>(base + LF.off_table);
+    v.pin = base + LF.off_pin;
+    v.leafu = reinterpret_cast<uint32_t*>(base + LF.off_leafu);
+    v.markb = reinterpret_cast<uint32_t*>(base + LF.off_mark);
+    v.fl = reinterpret_cast<BFlight*>(base + LF.off_fl);       // depends on B only
+    v.rlsP = reinterpret_cast<double*>(base + L.off_rls);      // after the beta records
+    v.gam = reinterpret_cast<uint64_t*>(base + L.off_gam);
+    v.tmask = LF.T - 1;
+    return v;
+  }
   BView<Idx> v;
   v.key = reinterpret_cast<uint64_t*>(base + L.off_key);
   v.stamp = reinterpret_cast<uint32_t*>(base + L.off_stamp);
@@ -607,7 +629,7 @@ __device__ __forceinline__ uint32_t b_next(const BView<Idx>& S, const BW& x, dou
 template <int kMaxThreads>
 struct BMinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxThreads <= 256 ? 2 : 1); };
 
-template <typename Idx, int kMaxThreads>
+template <typename Idx, int kMaxThreads, int kFixedB>
 __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     batch_kernel(const __grid_constant__ ReplayParams p) {
   uint8_t* smem = kvr_bsmem;
@@ -621,7 +643,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
   uint8_t* wbase;
   if constexpr (sizeof(Idx) == 4) wbase = p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes;
   else wbase = sbase + (size_t)w * L.bytes;
-  const BView<Idx> S = bview<Idx>(wbase, L);
+  const BView<Idx> S = bview<Idx, kFixedB>(wbase, L);
 
 #pragma unroll 1
   for (;;) {
@@ -917,21 +939,23 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
 
 size_t batch_ctrl_bytes() { return align16(sizeof(BCtrl)); }
 
-template <typename Idx>
+template <typename Idx, int kFixedB>
 static const void* batch_kernel_t(uint32_t W) {
-  if (W <= 4) return (const void*)batch_kernel<Idx, 128>;
-  if (W <= 8) return (const void*)batch_kernel<Idx, 256>;
-  if (W <= 16) return (const void*)batch_kernel<Idx, 512>;
-  return (const void*)batch_kernel<Idx, 1024>;
+  if (W <= 4) return (const void*)batch_kernel<Idx, 128, kFixedB>;
+  if (W <= 8) return (const void*)batch_kernel<Idx, 256, kFixedB>;
+  if (W <= 16) return (const void*)batch_kernel<Idx, 512, kFixedB>;
+  return (const void*)batch_kernel<Idx, 1024, kFixedB>;
 }
 
-// tier 1: per-worker state in shared memory, u16 slot ids; tier 2: workspace, u32
-static const void* batch_kernel_for(uint32_t W, bool global) {
-  return global ? batch_kernel_t<uint32_t>(W) : batch_kernel_t<uint16_t>(W);
+// tier 1: per-worker state in shared memory, u16 slot ids (B = 512 with compile-time
+// offsets); tier 2: workspace, u32
+static const void* batch_kernel_for(uint32_t W, bool global, uint32_t B) {
+  if (global) return batch_kernel_t<uint32_t, 0>(W);
+  return B == 512 ? batch_kernel_t<uint16_t, 512>(W) : batch_kernel_t<uint16_t, 0>(W);
 }
 
-cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global) {
-  const void* k = batch_kernel_for(W, global);
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global, uint32_t B) {
+  const void* k = batch_kernel_for(W, global, B);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, 32 * W, smem);
@@ -939,7 +963,7 @@ cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global) 
 
 cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s) {
   void* args[] = {const_cast<ReplayParams*>(&p)};
-  return cudaLaunchKernel(batch_kernel_for(p.W, p.bglobal != 0), dim3(grid), dim3(32 * p.W), args, smem, s);
+  return cudaLaunchKernel(batch_kernel_for(p.W, p.bglobal != 0, p.B), dim3(grid), dim3(32 * p.W), args, smem, s);
 }
 
 }  // namespace kvr

@@ -36,7 +36,7 @@ struct TraceDev {
 inline size_t packed_hash_offset(uint32_t N) { return ((size_t)N * sizeof(QueryHdr) + 15) & ~(size_t)15; }
 inline size_t packed_bytes(uint32_t N, uint64_t total) { return packed_hash_offset(N) + total * 8 + 16; }
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // Per-worker cache state (one worker = one warp), latency-critical part, held in
 // shared memory (tier 1, u16 slot ids) or global memory (tier 2, u32 slot ids):
@@ -152,7 +152,8 @@ struct BatchLayout {
       off_mark, off_fl, off_rls, off_gam, bytes;
 };
 
-inline BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n, uint32_t idx_bytes) {
+__host__ __device__ constexpr BatchLayout make_batch_layout(uint32_t B, uint32_t beta, uint32_t max_n,
+                                                        uint32_t idx_bytes) {
   BatchLayout L{};
   L.B = B;
   L.beta = beta;
@@ -222,7 +223,7 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
                           cudaStream_t s, bool ext);
 // continuous-batching kernel (kvr_batch.cu)
 size_t batch_ctrl_bytes();
-cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global);
+cudaError_t batch_attrs(size_t smem, int* ctas_per_sm, uint32_t W, bool global, uint32_t B);
 cudaError_t launch_batch(const ReplayParams& p, uint32_t grid, size_t smem, cudaStream_t s);
 // next-use index for the offline OPT analysis (kvr_nextuse.cu)
 cudaError_t next_use_scratch_bytes(uint64_t n_blocks, size_t* bytes);
