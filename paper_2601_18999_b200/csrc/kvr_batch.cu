@@ -128,9 +128,9 @@ __device__ __forceinline__ void t_insert_cas(const BView<Idx>& S, uint64_t t, ui
   }
 }
 template <typename Idx>
-__device__ __forceinline__ void t_erase(const BView<Idx>& S, uint64_t t) {
+__device__ __forceinline__ void t_erase(const BView<Idx>& S, uint64_t t, uint32_t slot) {
   uint32_t i = (uint32_t)t & S.tmask;
-  while (S.key[S.table[i]] != t) i = (i + 1) & S.tmask;   // present (caller's contract)
+  while (S.table[i] != (Idx)slot) i = (i + 1) & S.tmask;   // present (caller's contract)
   uint32_t j = i;
   for (;;) {
     j = (j + 1) & S.tmask;
@@ -402,7 +402,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       if (via_u) nU_known = nU_known - 1 + ((pa_leafu && !bit_test(S.markb, pa)) ? 1 : 0);
       __syncwarp();
       if (lane == 0) {
-        t_erase(S, hv);
+        t_erase(S, hv, v);
         if (has_pa) {
           S.nchild[pa] = (Idx)nc;
           if (pa_leafu) S.leafu[pa >> 5] |= 1u << (pa & 31);
