@@ -1,4 +1,4 @@
-"""bench.py's multi-rank path end to end on one GPU: two ranks under torchrun share the
+"""bench.py's multi-rank path end to end on one GPU: 2 or 4 ranks under torchrun share the
 device (KVR_BENCH_BACKEND=gloo stages the collectives through host copies).  Checks
 the contract line: whole-job value over both ranks, max-over-ranks time, the summary
 reduce with the packed-trace checksum, and e2e aggregated over ranks."""
@@ -20,10 +20,11 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def test_bench_two_ranks_one_gpu():
+@pytest.mark.parametrize("N", [2, 4])
+def test_bench_ranks_one_gpu(N):
     env = dict(os.environ, KVR_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(N),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(N),
            "--steps", "2", "--warmup", "3", "--queries", "3000", "--trials", "64",
            "--no-cpu-baseline"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
@@ -31,12 +32,12 @@ def test_bench_two_ranks_one_gpu():
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["trial_status_nonzero"] == 0
+    assert d["n_gpus"] == N and d["trial_status_nonzero"] == 0
     rs = d["reduced_summary"]
-    assert rs["trials"] == 128 and rs["queries"] == 128 * 3000
+    assert rs["trials"] == 64 * N and rs["queries"] == 64 * N * 3000
     assert rs["trace_hash_consistent"] is True and rs["status_nonzero"] == 0
     # value = both ranks' query-replays over the slowest rank's time
-    assert abs(d["value"] - 128 * 3000 / (d["ms_per_step"] / 1e3)) <= 1e-6 * d["value"]
+    assert abs(d["value"] - 64 * N * 3000 / (d["ms_per_step"] / 1e3)) <= 1e-6 * d["value"]
     e = d["e2e"]
     assert abs(e["value"] - e["queries_per_step"] / (e["ms_per_step"] / 1e3)) <= 1e-6 * e["value"]
-    assert e["queries_per_step"] == 128 * 3000
+    assert e["queries_per_step"] == 64 * N * 3000
