@@ -86,7 +86,7 @@ int smem_optin() {
 }
 
 struct Plan {
-  uint32_t tier;
+  uint32_t tier, ktier;   // tier reported (1 shared, 2 global); kernel tier (3 = global, u16 ids)
   size_t smem;
   int ctas_per_sm;
   uint32_t grid;
@@ -111,6 +111,7 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   if (tier == 1 && !fit1)
     return fail(KVR_ERR_UNSUPPORTED, "batching: shared-memory tier needs %zu B > %d B", smem1, optin);
   pl->tier = tier;
+  pl->ktier = tier;
   pl->blay = tier == 1 ? l16 : l32;
   pl->smem = tier == 1 ? smem1 : ctrl;
   cudaError_t e = kvr::batch_attrs(pl->smem, &pl->ctas_per_sm, c.W, tier == 2, c.capacity_blocks);
@@ -141,9 +142,12 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan
   if (tier == 2 && base > (size_t)optin)
     return fail(KVR_ERR_UNSUPPORTED, "query staging needs %zu B of shared memory", base);
   pl->tier = tier;
-  pl->lay = tier == 1 ? l16 : l32;
+  // global tier with W > 16 (1,024 threads): u16 slot ids halve the L1/L2 footprint of the
+  // tables (kernel tier 3); below that the u32 kernel keeps its registers
+  pl->ktier = (tier == 2 && c.W > 16 && c.capacity_blocks <= 65533) ? 3u : tier;
+  pl->lay = (tier == 1 || pl->ktier == 3) ? l16 : l32;
   pl->smem = tier == 1 ? smem1 : base;
-  cudaError_t e = kvr::replay_attrs(tier, pl->smem, &pl->ctas_per_sm, c.W, sim_extended(c));
+  cudaError_t e = kvr::replay_attrs(pl->ktier, pl->smem, &pl->ctas_per_sm, c.W, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
@@ -444,7 +448,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
     if (e != cudaSuccess) return cuda_fail(e, "batching replay launch");
     return KVR_OK;
   }
-  e = kvr::launch_replay(pl.tier, p, pl.grid, pl.smem, s, sim_extended(c));
+  e = kvr::launch_replay(pl.ktier, p, pl.grid, pl.smem, s, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   return KVR_OK;
 }

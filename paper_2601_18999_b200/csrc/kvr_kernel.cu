@@ -1802,6 +1802,7 @@ static const void* kernel_for_t(uint32_t tier, uint32_t W) {
   if (W <= 4) return (const void*)replay_kernel<uint32_t, true, 128, kExt>;
   if (W <= 8) return (const void*)replay_kernel<uint32_t, true, 256, kExt>;
   if (W <= 16) return (const void*)replay_kernel<uint32_t, true, 512, kExt>;
+  if (tier == 3) return (const void*)replay_kernel<uint16_t, true, 1024, kExt>;
   return (const void*)replay_kernel<uint32_t, true, 1024, kExt>;
 }
 
