@@ -30,10 +30,10 @@
  *   in-flight paths pinned, completions in time order (run_batched).
  *
  * Pins (tests/test_oracle_pins.py, tests/test_oracle_batching_pins.py; DESIGN.md
- * §2 P1-P31) fix every function here against the paper, closed forms, brute
+ * §2 P1-P32) fix every function here against the paper, closed forms, brute
  * force or textbook reductions.  Parity unpinned (only the oracle<->GPU
  * agreement checks them): LBGR theta trajectories and routing on
- * realistic traces beyond P4/P5/P14/P15/P18, STATIC / THRESHOLD outcomes between
+ * realistic traces beyond P4/P5/P14/P15/P18/P32, STATIC / THRESHOLD outcomes between
  * the extremes of P31, and absolute latency / TTFT / makespan magnitudes on the
  * synthetic workloads.
  *

@@ -566,3 +566,49 @@ def test_p31_join_shortest_queue(oracle_mod, router, kw, W):
     r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(router=router, eviction=0, **kw), 3,
                        record=True, check_invariants=True)
     assert np.all(r.records["worker"] == np.arange(tr.n_queries) % W)
+
+
+# -------------------------------------------------------------------------- P32
+def _constant_feature_trace(n=40, L=4, gap=1.0e5):
+    """Unique equal-length paths, spaced so every query finishes (and releases its load,
+    rho = 1) before the next arrives: phi = (0, 16L/1000, 0, 1) and E = cost every time."""
+    paths = [[100 * j + d for d in range(L)] for j in range(n)]
+    return wl.from_paths(paths, arrival_ms=[gap * j for j in range(n)], out_tokens=[3] * n)
+
+
+@pytest.mark.parametrize("mu", [0.05, 0.5, 0.992, 1.5])
+def test_p32_nlms_trajectory_closed_form(oracle_mod, mu):
+    """NLMS (A8) with constant features phi and constant target E: the residual
+    r_j = E - E^_j obeys r_{j+1} = r_j (1 - mu |phi|^2 / (1 + |phi|^2)) exactly in real
+    arithmetic (theta moves along phi only) -> geometric decay, checked over 40 steps."""
+    tr = _constant_feature_trace()
+    cfg = oracle_mod.OracleConfig(W=1, capacity_blocks=64, out_ms_per_token=5.0)
+    r = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=0, mu=mu, rho=1.0), 0, record=True)
+    E, Eh = r.records["latency_ms"], r.records["score"]
+    assert np.all(E == E[0])
+    phi = np.array([0.0, 16 * 4 / 1000.0, 0.0, 1.0])
+    g = 1.0 - mu * (phi @ phi) / (1.0 + phi @ phi)
+    res = E - Eh
+    pred = res[0] * g ** np.arange(len(res))
+    assert np.allclose(res, pred, rtol=1e-9, atol=1e-9 * abs(res[0]))
+
+
+@pytest.mark.parametrize("lam,p0", [(0.992, 1000.0), (0.5, 10.0), (1.0, 1.0)])
+def test_p32_rls_trajectory_closed_form(oracle_mod, lam, p0):
+    """RLS (A8b) with constant phi: s_j = phi' P_j phi follows s_{j+1} = s_j / (lam + s_j)
+    from s_0 = p0 |phi|^2 and the residual r_{j+1} = r_j lam / (lam + s_j)."""
+    tr = _constant_feature_trace()
+    cfg = oracle_mod.OracleConfig(W=1, capacity_blocks=64, out_ms_per_token=5.0)
+    pol = oracle_mod.OraclePolicy(eviction=0, router=oracle_mod.ROUTE_LBGR_RLS, mu=lam,
+                                  rls_p0=p0, rho=1.0)
+    r = oracle_mod.run(cfg, tr, pol, 0, record=True)
+    res = r.records["latency_ms"] - r.records["score"]
+    phi = np.array([0.0, 16 * 4 / 1000.0, 0.0, 1.0])
+    s = p0 * (phi @ phi)
+    pred = [res[0]]
+    for _ in range(len(res) - 1):
+        pred.append(pred[-1] * lam / (lam + s))
+        s = s / (lam + s)
+    pred = np.array(pred)
+    scale = abs(res[0])
+    assert np.allclose(res, pred, rtol=1e-8, atol=1e-8 * scale)
