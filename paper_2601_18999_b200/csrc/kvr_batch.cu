@@ -184,9 +184,10 @@ struct BW {
   uint32_t size, cntT, nfl, wh, wn;
   uint64_t e, k, vcur;
   double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
-  // counters (u32 per worker and trial; tokens counted in blocks): probes, inserted,
-  // evictions, draws, resets, fallbacks, hit blocks, input blocks, queries, max
-  // pending, (unused), victim-log overflow; the digest sum is u64
+  // counters, u32 in registers and flushed into the worker's u64 accumulators in shared
+  // memory every 4,096 queries (at most 65,536 blocks per query per counter, so no
+  // wrap): probes, inserted, evictions, draws, resets, fallbacks, hit blocks, input
+  // blocks, queries, max pending, (unused), victim-log overflow
   uint32_t c[12];
   uint64_t dsum;
   bool dead;   // admission failure / violation: stop this worker
@@ -707,6 +708,8 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     for (int c = 0; c < 12; ++c) x.c[c] = 0;
     x.dsum = 0;
     x.dead = false;
+    if (lane == 0)
+      for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = 0;
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     const uint32_t Nrun = pol_ok ? N : 0;
     const double rho = pol.rho, dt = pol.delta_t_ms;
@@ -721,6 +724,11 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       const double t = hq.arrival_ms;
       const uint32_t n_in = hq.n_in;
       const uint32_t q = T.bt * n_in;
+      if ((j & 4095u) == 4095u) {   // flush the u32 counters (sums only; 9 = max, 11 = flag)
+        if (lane == 0)
+          for (int c = 0; c < 9; ++c) ctrl->cnt[w][c] += x.c[c];
+        for (int c = 0; c < 9; ++c) x.c[c] = 0;
+      }
       // 1. catch-up: ticks, completions and the dequeues they start, in time order (A31)
       if (!x.dead) {
         for (;;) {
@@ -883,10 +891,12 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       ctrl->slat[w] = x.slat;
       ctrl->sttft[w] = x.sttft;
       ctrl->mlat[w] = x.mlat;
-      for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = x.c[c];
-      ctrl->cnt[w][6] = (unsigned long long)x.c[6] * T.bt;
-      ctrl->cnt[w][7] = (unsigned long long)x.c[7] * T.bt;
+      for (int c = 0; c < 9; ++c) ctrl->cnt[w][c] += x.c[c];
+      ctrl->cnt[w][6] *= T.bt;     // hit / input blocks -> tokens
+      ctrl->cnt[w][7] *= T.bt;
+      ctrl->cnt[w][9] = x.c[9];
       ctrl->cnt[w][10] = x.dsum;
+      ctrl->cnt[w][11] = x.c[11];
     }
     __syncthreads();
     if (tid == 0) {
