@@ -47,7 +47,8 @@ enum {
   KVR_OK = 0,
   KVR_ERR_INVALID_ARG = 1,        /* bad pointer / size / parameter / malformed trace */
   KVR_ERR_CAPACITY = 2,           /* some n_in+n_out > B: premise beta*L_max <= B (beta=1) */
-  KVR_ERR_UNSUPPORTED = 3,        /* W > 32, B > 65536, or no state tier fits */
+  KVR_ERR_UNSUPPORTED = 3,        /* W > 32, B > 65536, no state tier fits, or a trace of
+                                     >= 2^32 - 1 blocks (per-worker counters are 32-bit) */
   KVR_ERR_HASH_COLLISION = 4,     /* kvr_trace_check_collisions found two prefixes with one
                                      identity: reload the trace with another hash_salt */
   KVR_ERR_WORKSPACE_TOO_SMALL = 5,

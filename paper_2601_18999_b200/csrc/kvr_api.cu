@@ -385,6 +385,11 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
       return fail(KVR_ERR_CAPACITY,
                   "trace %u: beta*L_max = %u*%u blocks > capacity B=%u (premise beta*L_max<=B, P:197)",
                   i, (uint32_t)beta, t->max_n, c.capacity_blocks);
+    // the replay kernel keeps per-worker insert/eviction/draw counts in u32 registers: a
+    // worker's count is at most the trace's total blocks
+    if (t->total >= 0xffffffffull)
+      return fail(KVR_ERR_UNSUPPORTED, "trace %u has %llu blocks; at most 2^32 - 1 per trace", i,
+                  (unsigned long long)t->total);
     max_n = std::max(max_n, t->max_n);
     max_N = std::max(max_N, t->N);
     if (!d_policies && c.default_policy.eviction == KVR_EVICT_OPT && !t->nu && t->total)
