@@ -37,10 +37,12 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 6u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
+#define KVR_ABI_VERSION 7u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
                                 4: kvr_sim_config.extended_policies;
                                 5: kvr_sim_config.batch_slots (continuous batching);
-                                6: kvr_trace_collision_bytes / kvr_trace_check_collisions */
+                                6: kvr_trace_collision_bytes / kvr_trace_check_collisions;
+                                7: KVR_TRIAL_BAD_TRACE, kvr_build_id, pooled pending FIFOs
+                                   (pending_ring may be as large as the trace) */
 
 typedef int32_t kvr_status;
 enum {
@@ -61,15 +63,22 @@ enum {
   KVR_TRIAL_RING_OVERFLOW = 1,    /* a worker's pending-completion FIFO exceeded pending_ring:
                                      the trial stops before the overflowing query's cache update */
   KVR_TRIAL_VICTIM_LOG_FULL = 2,  /* recorded trial produced more victims than its log share */
-  KVR_TRIAL_BAD_POLICY = 3,       /* per-trial policy out of range (trial not run) */
-  KVR_TRIAL_ADMISSION = 4         /* batching engine: full cache and every leaf in flight
+  KVR_TRIAL_BAD_POLICY = 3,       /* per-trial policy out of range (trial not run): an enum out
+                                     of range, rho not in (0,1], delta_t <= 0, a non-finite
+                                     parameter (delta_t = +inf allowed), NLMS mu not in [0,2)
+                                     (A8), RLS mu not in (0,1] or rls_p0 not finite > 0 */
+  KVR_TRIAL_ADMISSION = 4,        /* batching engine: full cache and every leaf in flight
                                      (SPEC S:137); impossible when beta*L_max <= B, which
                                      kvr_sim_run enforces.  Counters of a trial with a nonzero
                                      status are unspecified in the batching engine. */
+  KVR_TRIAL_BAD_TRACE = 5         /* kvr_sim_run_multi: d_trial_trace[t] >= n_traces (trial not run) */
 };
 
 const char* kvr_last_error(void);
 uint32_t kvr_abi_version(void);
+/* Hex SHA-256 prefix of the sources this library was compiled from (build provenance:
+ * paper_2601_18999_b200/build.py recompiles whenever it differs from the tree's). */
+const char* kvr_build_id(void);
 
 /* ------------------------------------------------------------------ trace */
 /* Raw trace: block-hashed queries.  Gamma_j = n_in_j input blocks followed by
@@ -190,7 +199,12 @@ typedef struct {
   uint32_t capacity_blocks;        /* B per worker, 1..65536 */
   kvr_service_model truth;
   kvr_policy default_policy;
-  uint32_t pending_ring;           /* per-worker FIFO capacity (>= 1) */
+  uint32_t pending_ring;           /* per-worker cap on pending completions (>= 1; a worker that
+                                      would exceed it stops the trial, KVR_TRIAL_RING_OVERFLOW).
+                                      beta = 1 engine: the FIFOs of a trial's W workers share one
+                                      pool of min(N, W*pending_ring) records in 32-record chunks,
+                                      so pending_ring >= N (the trace length) never overflows at a
+                                      workspace of ~64 B x N per resident CTA */
   uint32_t record_trials;          /* the first R trials emit per-query records + victim logs */
   uint32_t latency_hist_bins;      /* 0, or 1..256 log-bucket bins (4 per octave, bin 0 = <1 ms) */
   uint32_t force_tier;             /* 0 auto, 1 shared-memory tables, 2 global-memory tables */

@@ -112,7 +112,9 @@ class OraclePolicy:
     est_alpha_miss_ms: float = 1.0
     rho: float = 31.0 / 32.0
     delta_t_ms: float = 20.0
-    mu: float = 0.992
+    # NLMS step of router 0 (A8, revised r2: 1 - 0.992 = 0.008) or the RLS forgetting
+    # factor of router 5 (A8b: 0.992); None = that router's default
+    mu: Optional[float] = None
     theta0: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
     tau: float = 1.5
     w_hit: float = 1.0
@@ -125,7 +127,8 @@ class OraclePolicy:
         p = _Policy()
         p.eviction, p.rlt_fallback, p.router = self.eviction, self.rlt_fallback, self.router
         p.est_alpha_cached_ms, p.est_alpha_miss_ms = self.est_alpha_cached_ms, self.est_alpha_miss_ms
-        p.rho, p.delta_t_ms, p.mu = self.rho, self.delta_t_ms, self.mu
+        mu = self.mu if self.mu is not None else (0.992 if self.router == ROUTE_LBGR_RLS else 0.008)
+        p.rho, p.delta_t_ms, p.mu = self.rho, self.delta_t_ms, float(mu)
         for k in range(4):
             p.theta0[k] = float(self.theta0[k])
         p.tau, p.w_hit, p.w_load = self.tau, self.w_hit, self.w_load

@@ -71,6 +71,35 @@ uint64_t pick(uint64_t r, uint64_t m) {
   return (uint64_t)(((unsigned __int128)r * (unsigned __int128)m) >> 64);
 }
 
+// i* = argmin over the scores, first index on ties (A15).  A NaN score (possible only
+// through fp overflow, e.g. inf - inf in theta' phi) ranks after every number; all NaN
+// -> worker 0 (reading A37).
+uint32_t first_min(const std::vector<double>& s, uint32_t W) {
+  uint32_t best = 0;
+  for (uint32_t i = 1; i < W; ++i)
+    if (!std::isnan(s[i]) && (std::isnan(s[best]) || s[i] < s[best])) best = i;
+  return best;
+}
+
+// per-trial policy checks shared by both engines (A8: NLMS needs 0 <= mu < 2;
+// every parameter finite except delta_t_ms = +inf, which means no decay)
+bool policy_valid(const kvro_policy* p) {
+  if (p->eviction > KVRO_EVICT_OPT || p->rlt_fallback > KVRO_RLT_LRU_MARKED ||
+      p->router > KVRO_ROUTE_LBGR_RLS)
+    return false;
+  if (p->tracker_lag > 1 || p->tracker_grain < 1) return false;
+  if (!(p->rho > 0.0 && p->rho <= 1.0) || !(p->delta_t_ms > 0.0)) return false;
+  const double fin[] = {p->est_alpha_cached_ms, p->est_alpha_miss_ms, p->mu, p->theta0[0],
+                        p->theta0[1], p->theta0[2], p->theta0[3], p->tau, p->w_hit, p->w_load};
+  for (double v : fin)
+    if (!std::isfinite(v)) return false;
+  if (p->router == KVRO_ROUTE_LBGR && !(p->mu >= 0.0 && p->mu < 2.0)) return false;
+  if (p->router == KVRO_ROUTE_LBGR_RLS &&
+      (!(p->mu > 0.0 && p->mu <= 1.0) || !(p->rls_p0 > 0.0) || !std::isfinite(p->rls_p0)))
+    return false;
+  return true;
+}
+
 int validate_trace(const kvro_trace* tr) {
   if (!tr || tr->block_tokens == 0) return 1;
   if (tr->n_queries && (!tr->arrival_ms || !tr->n_in_blocks || !tr->n_out_blocks ||
@@ -606,17 +635,16 @@ int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy*
         Ehat[i] = (C + w[i].Pt) + d;                                               // Eq. 4
         Chat[i] = C; phi0[i] = f0; phi1[i] = f1; phi2[i] = f2;
       }
-      for (uint32_t i = 1; i < W; ++i)
-        if (Ehat[i] < Ehat[best]) best = i;
+      best = first_min(Ehat, W);
       score_best = Ehat[best];
     } else if (pol->router == KVRO_ROUTE_STATIC_LINEAR) {
-      double bs = 0.0;
+      std::vector<double> s(W);
       for (uint32_t i = 0; i < W; ++i) {
         double x = (double)(tr->block_tokens * m[i]);
-        double s = (pol->w_load * (double)pending(i)) - (pol->w_hit * (x / (double)q));
-        if (i == 0 || s < bs) { bs = s; best = i; }
+        s[i] = (pol->w_load * (double)pending(i)) - (pol->w_hit * (x / (double)q));
       }
-      score_best = bs;
+      best = first_min(s, W);
+      score_best = s[best];
     } else if (pol->router == KVRO_ROUTE_THRESHOLD) {
       size_t mx = pending(0), mn = pending(0);
       for (uint32_t i = 1; i < W; ++i) {
@@ -746,16 +774,9 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   if (validate_trace(tr)) return 1;
   const uint32_t W = cfg->W, B = cfg->capacity_blocks;
   if (W < 1 || W > 32 || B < 1 || B > 65536) return 1;
-  if (pol->eviction > KVRO_EVICT_OPT || pol->rlt_fallback > KVRO_RLT_LRU_MARKED ||
-      pol->router > KVRO_ROUTE_LBGR_RLS)
-    return 1;
-  if (pol->tracker_lag > 1 || pol->tracker_grain < 1) return 1;
-  if (pol->router == KVRO_ROUTE_LBGR_RLS &&
-      (!(pol->mu > 0.0 && pol->mu <= 1.0) || !(pol->rls_p0 > 0.0) || !std::isfinite(pol->rls_p0)))
-    return 1;
+  if (!policy_valid(pol)) return 1;
   // Belady OPT is defined for one cache: the offline analysis runs it at W = 1
   if (pol->eviction == KVRO_EVICT_OPT && W != 1) return 1;
-  if (!(pol->rho > 0.0 && pol->rho <= 1.0) || !(pol->delta_t_ms > 0.0)) return 1;
   // beta * L_max <= B (beta = 1 in the default model)
   const uint64_t beta = cfg->batch_slots > 0 ? cfg->batch_slots : 1;
   if (cfg->batch_slots > 64) return 1;
@@ -886,17 +907,16 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
         Ehat[i] = (C + w[i].Pt) + d;                                               // Eq. 4
         Chat[i] = C; phi0[i] = f0; phi1[i] = f1; phi2[i] = f2;
       }
-      for (uint32_t i = 1; i < W; ++i)
-        if (Ehat[i] < Ehat[best]) best = i;
+      best = first_min(Ehat, W);
       score_best = Ehat[best];
     } else if (pol->router == KVRO_ROUTE_STATIC_LINEAR) {   // A17
-      double bs = 0.0;
+      std::vector<double> s(W);
       for (uint32_t i = 0; i < W; ++i) {
         double x = (double)(tr->block_tokens * mt[i]);
-        double s = (pol->w_load * (double)w[i].fifo.size()) - (pol->w_hit * (x / (double)q));
-        if (i == 0 || s < bs) { bs = s; best = i; }
+        s[i] = (pol->w_load * (double)w[i].fifo.size()) - (pol->w_hit * (x / (double)q));
       }
-      score_best = bs;
+      best = first_min(s, W);
+      score_best = s[best];
     } else if (pol->router == KVRO_ROUTE_THRESHOLD) {       // A16
       size_t mx = w[0].fifo.size(), mn = w[0].fifo.size();
       for (uint32_t i = 1; i < W; ++i) {

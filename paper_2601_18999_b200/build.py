@@ -1,6 +1,7 @@
 """Build libkvr.so (the C-ABI replay engine) in-tree with nvcc for sm_100a."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -31,12 +32,35 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def source_hash() -> str:
+    """SHA-256 prefix over the compiled sources, the header and the nvcc flags; compiled
+    into the library as kvr_build_id() (build provenance, VERDICT r1 #11)."""
+    h = hashlib.sha256()
+    for path in [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "kvr.h")]:
+        h.update(os.path.basename(path).encode())
+        with open(path, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+_MARK = b"KVR_BUILD_ID="
+
+
+def embedded_hash(lib: str) -> str:
+    """The source hash a built library carries (read from the file, not loaded)."""
+    try:
+        with open(lib, "rb") as f:
+            data = f.read()
+    except OSError:
+        return ""
+    i = data.find(_MARK)
+    return data[i + len(_MARK): i + len(_MARK) + 16].decode(errors="replace") if i >= 0 else ""
+
+
 def stale(lib: str = LIB) -> bool:
-    if not os.path.exists(lib):
-        return True
-    t = os.path.getmtime(lib)
-    deps = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "kvr.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    """True unless `lib` was compiled from exactly the current sources and flags."""
+    return embedded_hash(lib) != source_hash()
 
 
 PROF_LIB = os.path.join(PKG, "libkvr_prof.so")
@@ -48,7 +72,8 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     lib = PROF_LIB if profile else LIB
     if not force and not stale(lib):
         return lib
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"]
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
+                                   f"-DKVR_BUILD_ID=\"{source_hash()}\""]
     if profile:
         cmd.append("-DKVR_PHASE_PROFILE")
     cmd += [os.path.join(CSRC, f) for f in SOURCES]
@@ -63,7 +88,8 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
 def build_variant(name: str, defines: list[str]) -> str:
     """Experiment build libkvr_<name>.so with extra -D flags (scripts only, via KVR_LIB)."""
     lib = os.path.join(PKG, f"libkvr_{name}.so")
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"]
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
+                                   f"-DKVR_BUILD_ID=\"{source_hash()}\""]
     cmd += [f"-D{d}" for d in defines] + [os.path.join(CSRC, f) for f in SOURCES]
     subprocess.run(cmd, check=True)
     os.replace(lib + ".tmp", lib)

@@ -68,7 +68,9 @@ bool policy_ok(const kvr_policy& p, std::string* why) {
                         p.theta0[2], p.theta0[3], p.tau, p.w_hit, p.w_load};
   for (double v : fin)
     if (!std::isfinite(v)) return bad("parameters must be finite");
-  return true;
+  if (p.router == KVR_ROUTE_LBGR && !(p.mu >= 0.0 && p.mu < 2.0))
+    return bad("LBGR NLMS step mu must be in [0, 2) (reading A8)");
+  return kvr::policy_valid(p) ? true : bad("invalid policy");
 }
 
 int num_sms() {
@@ -92,8 +94,9 @@ struct Plan {
   uint32_t grid;
   kvr::WorkerLayout lay;
   kvr::AuxLayout aux;
+  kvr::FifoLayout fifo;
   kvr::BatchLayout blay;
-  size_t ws_aux, ws_state, ws_total;
+  size_t ws_aux, ws_fifo, ws_state, ws_total;
 };
 
 // continuous batching (kvr_batch.cu): per-worker state in shared memory when W
@@ -120,12 +123,13 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
   pl->ws_aux = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * sizeof(kvr::BFlight));
+  pl->ws_fifo = 0;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->blay.bytes : 0;
   pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
   return KVR_OK;
 }
 
-kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan* pl) {
+kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t max_N, uint32_t n_trials, Plan* pl) {
   const kvr_sim_config& c = sim->cfg;
   const int optin = smem_optin();
   if (optin <= 0) return fail(KVR_ERR_CUDA, "no CUDA device available");
@@ -152,10 +156,12 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
-  pl->aux = kvr::make_aux(c.capacity_blocks, c.pending_ring, max_n);
+  pl->aux = kvr::make_aux(c.capacity_blocks, max_n);
   pl->ws_aux = (size_t)pl->grid * c.W * pl->aux.bytes;
+  pl->fifo = kvr::make_fifo(c.W, c.pending_ring, max_N);
+  pl->ws_fifo = (size_t)pl->grid * pl->fifo.bytes;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->lay.bytes : 0;
-  pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
+  pl->ws_total = 256 + pl->ws_aux + pl->ws_fifo + pl->ws_state;
   return KVR_OK;
 }
 
@@ -164,6 +170,13 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials, Plan
 extern "C" {
 
 const char* kvr_last_error(void) { return g_err.c_str(); }
+
+#ifndef KVR_BUILD_ID
+#define KVR_BUILD_ID "unknown"
+#endif
+// the marker makes the id readable from the file without loading it (build.py)
+static const char kBuildIdMarked[] = "KVR_BUILD_ID=" KVR_BUILD_ID;
+const char* kvr_build_id(void) { return kBuildIdMarked + 13; }
 uint32_t kvr_abi_version(void) { return KVR_ABI_VERSION; }
 
 kvr_status kvr_trace_packed_bytes(const kvr_trace_desc* d, size_t* packed, size_t* scratch) {
@@ -334,7 +347,7 @@ kvr_status kvr_sim_plan(const kvr_sim* sim, uint32_t max_path_blocks, uint32_t* 
                         size_t* smem_bytes, uint32_t* ctas_per_sm) {
   if (!sim) return fail(KVR_ERR_INVALID_ARG, "null sim");
   Plan pl;
-  kvr_status st = make_plan(sim, max_path_blocks, 1u << 30, &pl);
+  kvr_status st = make_plan(sim, max_path_blocks, 0, 1u << 30, &pl);
   if (st) return st;
   if (tier) *tier = pl.tier;
   if (smem_bytes) *smem_bytes = pl.smem;
@@ -346,13 +359,14 @@ kvr_status kvr_sim_workspace_bytes_multi(const kvr_sim* sim, uint32_t n_traces,
                                          const kvr_trace* const* traces, uint32_t n_trials,
                                          size_t* bytes) {
   if (!sim || !traces || !bytes || n_traces == 0) return fail(KVR_ERR_INVALID_ARG, "null argument");
-  uint32_t max_n = 1;
+  uint32_t max_n = 1, max_N = 0;
   for (uint32_t i = 0; i < n_traces; ++i) {
     if (!traces[i]) return fail(KVR_ERR_INVALID_ARG, "null trace %u", i);
     max_n = std::max(max_n, traces[i]->max_n);
+    max_N = std::max(max_N, traces[i]->N);
   }
   Plan pl;
-  kvr_status st = make_plan(sim, max_n, n_trials, &pl);
+  kvr_status st = make_plan(sim, max_n, max_N, n_trials, &pl);
   if (st) return st;
   *bytes = pl.ws_total;
   return KVR_OK;
@@ -398,7 +412,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   const uint32_t R = std::min(c.record_trials, n_trials);
   if (R && !d_records) return fail(KVR_ERR_INVALID_ARG, "record_trials > 0 needs d_records");
   Plan pl;
-  kvr_status st = make_plan(sim, max_n, n_trials, &pl);
+  kvr_status st = make_plan(sim, max_n, max_N, n_trials, &pl);
   if (st) return st;
   if (ws_bytes < pl.ws_total)
     return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, pl.ws_total);
@@ -426,6 +440,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   p.scratch_bytes = (uint32_t)kvr::scratch_bytes(max_n);
   p.max_n = max_n;
   p.aux = pl.aux;
+  p.fifo = pl.fifo;
   p.lay = pl.lay;
   p.truth = c.truth;
   p.defpol = c.default_policy;
@@ -439,7 +454,8 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   uint8_t* ws = (uint8_t*)d_ws;
   p.work_counter = (unsigned int*)ws;
   p.aux_base = ws + 256;
-  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux : nullptr;
+  p.fifo_base = ws + 256 + pl.ws_aux;
+  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux + pl.ws_fifo : nullptr;
 
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);

@@ -185,9 +185,10 @@ struct BW {
   uint64_t e, k, vcur;
   double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
   // counters, u32 in registers and flushed into the worker's u64 accumulators in shared
-  // memory every 4,096 queries (at most 65,536 blocks per query per counter, so no
-  // wrap): probes, inserted, evictions, draws, resets, fallbacks, hit blocks, input
-  // blocks, queries, max pending, (unused), victim-log overflow
+  // memory as soon as one of the sums reaches 2^31 (checked after every arrival and
+  // every completion; one event adds at most 65,536 to a counter, so none wraps):
+  // probes, inserted, evictions, draws, resets, fallbacks, hit blocks, input blocks,
+  // queries, max pending, (unused), victim-log overflow
   uint32_t c[12];
   uint64_t dsum;
   bool dead;   // admission failure / violation: stop this worker
@@ -607,6 +608,19 @@ __device__ __forceinline__ bool b_complete(const BTrial& T, const BView<Idx>& S,
   return true;
 }
 
+// flush the u32 sum counters (0..8; 9 = max, 11 = flag) once one reaches 2^31
+__device__ __forceinline__ void b_flush(BW& x, unsigned long long* acc, uint32_t lane) {
+  uint32_t any = 0;
+#pragma unroll
+  for (int c = 0; c < 9; ++c) any |= x.c[c];
+  if (any & 0x80000000u) {
+    if (lane == 0)
+      for (int c = 0; c < 9; ++c) acc[c] += x.c[c];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) x.c[c] = 0;
+  }
+}
+
 template <typename Idx>
 __device__ __forceinline__ uint32_t b_next(const BView<Idx>& S, const BW& x, double* c) {
   uint32_t b = kNone;
@@ -663,7 +677,9 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     const kvr_policy& pol = ctrl->pol;
     BTrial T;
     T.p = &p;
-    T.tr = p.traces[p.trial_trace ? p.trial_trace[trial] : 0];
+    const uint32_t tix = p.trial_trace ? p.trial_trace[trial] : 0u;
+    const bool tr_ok = tix < p.n_traces;   // else KVR_TRIAL_BAD_TRACE, trial not run
+    T.tr = p.traces[tr_ok ? tix : 0u];
     T.pol = &pol;
     T.K = p.keys[trial];
     T.W = W;
@@ -686,11 +702,8 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     const uint32_t N = T.tr.N;
 
     // a per-trial policy from device memory is validated here (A36)
-    const bool pol_ok = pol.eviction <= KVR_EVICT_RLT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
-                        pol.router <= KVR_ROUTE_LBGR_RLS && pol.rho > 0.0 && pol.rho <= 1.0 &&
-                        pol.delta_t_ms > 0.0 && pol.tracker_lag == 0 && pol.tracker_grain == 1 &&
-                        (!T.rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
-                                    pol.rls_p0 < INFINITY));
+    const bool pol_ok = policy_valid(pol) && pol.eviction <= KVR_EVICT_RLT &&
+                        pol.tracker_lag == 0 && pol.tracker_grain == 1;
     // ---- per-trial init: empty caches, P = 0 ----
     for (uint32_t q = lane; q < L.T; q += 32) S.table[q] = (Idx)BView<Idx>::NIL;
     for (uint32_t q = lane; q < B; q += 32) S.pin[q] = 0;
@@ -711,7 +724,8 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     if (lane == 0)
       for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = 0;
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
-    const uint32_t Nrun = pol_ok ? N : 0;
+    if (!tr_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_TRACE;
+    const uint32_t Nrun = (pol_ok && tr_ok) ? N : 0;
     const double rho = pol.rho, dt = pol.delta_t_ms;
     bool aborted = false;
     // Ehat / C^ / phi of this worker for the current query (used if it is chosen)
@@ -724,11 +738,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       const double t = hq.arrival_ms;
       const uint32_t n_in = hq.n_in;
       const uint32_t q = T.bt * n_in;
-      if ((j & 4095u) == 4095u) {   // flush the u32 counters (sums only; 9 = max, 11 = flag)
-        if (lane == 0)
-          for (int c = 0; c < 9; ++c) ctrl->cnt[w][c] += x.c[c];
-        for (int c = 0; c < 9; ++c) x.c[c] = 0;
-      }
+      b_flush(x, ctrl->cnt[w], lane);
       // 1. catch-up: ticks, completions and the dequeues they start, in time order (A31)
       if (!x.dead) {
         for (;;) {
@@ -746,6 +756,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
               x.dead = true;
               break;
             }
+            b_flush(x, ctrl->cnt[w], lane);
             continue;
           }
           break;
@@ -802,9 +813,11 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       // 3. argmin (lowest index on ties, A15), identical in every warp
       uint32_t best = 0;
       const uint32_t router = pol.router;
-      if (T.lbgr || router == KVR_ROUTE_STATIC_LINEAR) {
-        for (uint32_t i = 1; i < W; ++i)
-          if (ctrl->score[par][i] < ctrl->score[par][best]) best = i;
+      if (T.lbgr || router == KVR_ROUTE_STATIC_LINEAR) {   // NaN ranks last (A37)
+        for (uint32_t i = 1; i < W; ++i) {
+          const double si = ctrl->score[par][i], sb = ctrl->score[par][best];
+          if (!isnan(si) && (isnan(sb) || si < sb)) best = i;
+        }
       } else if (router == KVR_ROUTE_THRESHOLD) {   // A16 on pending = waiting + in flight
         uint32_t mx = ctrl->pend[par][0], mn = mx;
         for (uint32_t i = 1; i < W; ++i) {
@@ -883,6 +896,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
           if (lane == 0) atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_ADMISSION);
           break;
         }
+        b_flush(x, ctrl->cnt[w], lane);
       }
     }
     if (lane == 0) {

@@ -14,6 +14,7 @@ constexpr uint32_t kAhead = 2;          // queries staged ahead; a buffer lives 
                                         // after its query for the deferred apply
 constexpr uint32_t kMaxTraces = 64;     // traces per multi-trace launch
 constexpr uint32_t kFifoRecBytes = 64;  // one pending completion {c,a,E^,phi0..2,C^,k_a}
+constexpr uint32_t kFifoChunk = 32;     // records per chunk of a CTA's pending-FIFO pool
 constexpr uint32_t kMaxHistBins = 256;
 constexpr uint32_t kMaxW = 32;
 
@@ -37,6 +38,27 @@ inline size_t packed_hash_offset(uint32_t N) { return ((size_t)N * sizeof(QueryH
 inline size_t packed_bytes(uint32_t N, uint64_t total) { return packed_hash_offset(N) + total * 8 + 16; }
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Per-trial policy checks applied on the device to every per-trial policy (the host
+// checks the default one with messages in kvr_api.cu): enums in range, rho in (0, 1],
+// delta_t > 0 (+inf = no decay), every other parameter finite (x - x == 0 iff finite),
+// NLMS step 0 <= mu < 2 (reading A8), RLS forgetting factor in (0, 1] (A8b).
+__host__ __device__ inline bool policy_valid(const kvr_policy& p) {
+  auto fin = [](double v) { return (v - v) == 0.0; };
+  if (p.eviction > KVR_EVICT_OPT || p.rlt_fallback > KVR_RLT_LRU_MARKED ||
+      p.router > KVR_ROUTE_LBGR_RLS || p.tracker_lag > 1 || p.tracker_grain < 1)
+    return false;
+  if (!(p.rho > 0.0 && p.rho <= 1.0) || !(p.delta_t_ms > 0.0)) return false;
+  if (!fin(p.est_alpha_cached_ms) || !fin(p.est_alpha_miss_ms) || !fin(p.mu) ||
+      !fin(p.theta0[0]) || !fin(p.theta0[1]) || !fin(p.theta0[2]) || !fin(p.theta0[3]) ||
+      !fin(p.tau) || !fin(p.w_hit) || !fin(p.w_load))
+    return false;
+  if (p.router == KVR_ROUTE_LBGR && !(p.mu >= 0.0 && p.mu < 2.0)) return false;
+  if (p.router == KVR_ROUTE_LBGR_RLS &&
+      !(p.mu > 0.0 && p.mu <= 1.0 && p.rls_p0 > 0.0 && fin(p.rls_p0)))
+    return false;
+  return true;
+}
 
 // Per-worker cache state (one worker = one warp), latency-critical part, held in
 // shared memory (tier 1, u16 slot ids) or global memory (tier 2, u32 slot ids):
@@ -68,26 +90,47 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   return L;
 }
 
-// Per-worker auxiliary state in global memory (L2-resident): the pending
-// completion FIFO and the Leaf-LRU recency log (append-only ring of (stamp, slot),
-// compacted when full; validated by the per-slot stamps of the worker state).
+// Per-worker auxiliary state in global memory (L2-resident): the Leaf-LRU recency
+// log (append-only ring of (stamp, slot), compacted when full; validated by the
+// per-slot stamps of the worker state) and the LBGR_RLS matrix.
 struct AuxLayout {
-  uint32_t ring, log_cap;
-  size_t off_fifo, off_log, off_rls, bytes;   // rls: LBGR_RLS P (4x4, fp64)
+  uint32_t log_cap;
+  size_t off_log, off_rls, bytes;   // rls: LBGR_RLS P (4x4, fp64)
 };
 
-inline AuxLayout make_aux(uint32_t B, uint32_t ring, uint32_t max_n) {
+inline AuxLayout make_aux(uint32_t B, uint32_t max_n) {
   AuxLayout A{};
-  A.ring = ring;
+  // live entries after a compaction <= B; 4x headroom keeps the amortised compaction
+  // cost at ~1.25 entries read per entry appended and the log L2-resident
   uint32_t C = 64;
-  while (C < 8 * (B + max_n + 32)) C <<= 1;
+  while (C < 4 * (B + max_n + 32)) C <<= 1;
   A.log_cap = C;
   size_t o = 0;
-  A.off_fifo = o;  o = align16(o + (size_t)ring * kFifoRecBytes);
   A.off_log = o;   o = align16(o + (size_t)C * 8);
   A.off_rls = o;   o = align16(o + 16 * 8);
   A.bytes = (o + 127) & ~(size_t)127;
   return A;
+}
+
+// Pending-completion FIFOs of one CTA's trial: every worker's FIFO is a linked list
+// of 32-record chunks from one per-CTA pool (link words, then the chunks).  Chunks a
+// worker empties go to that worker's free list and are reused first (LIFO, so the
+// few chunks in use stay in L2); new ones come from a bump counter.  A worker holds
+// at most ceil(pending/32) + 1 chunks, so ceil(N/32) + 2W chunks never run out, and
+// W (ceil(ring/32) + 2) bound it when the per-worker cap `ring` is smaller.
+struct FifoLayout {
+  uint32_t chunks;
+  size_t off_rec, bytes;
+};
+
+inline FifoLayout make_fifo(uint32_t W, uint32_t ring, uint32_t max_N) {
+  FifoLayout F{};
+  const uint64_t by_trace = ((uint64_t)max_N + kFifoChunk - 1) / kFifoChunk + 2ull * W;
+  const uint64_t by_ring = (uint64_t)W * (((uint64_t)ring + kFifoChunk - 1) / kFifoChunk + 2);
+  F.chunks = (uint32_t)(by_trace < by_ring ? by_trace : by_ring);
+  F.off_rec = ((size_t)F.chunks * 4 + 127) & ~(size_t)127;
+  F.bytes = F.off_rec + (size_t)F.chunks * kFifoChunk * kFifoRecBytes;
+  return F;
 }
 
 // Control block at the start of dynamic shared memory.
@@ -102,6 +145,7 @@ struct __align__(16) Ctrl {
   unsigned long long cnt[10];   // probes, inserted, evictions, draws, resets, fallbacks, hit, in, queries, maxpend
   kvr_policy pol;                      // this trial's policy
   uint32_t trial, status, abortf[2];   // abort flag double-buffered by query parity
+  uint32_t fifo_bump, _pad_f[3];       // next never-used chunk of the CTA's FIFO pool
   uint32_t hist[kMaxHistBins];
 };
 
@@ -122,7 +166,8 @@ struct __align__(16) WarpSm {
   unsigned long long vc;           // victim-log offset of the pending update
   unsigned long long c_probes, c_hit, c_in;
   uint32_t active, j, buf, n, kf, M, m, nev, h, ltail0, wq, p0;
-  uint32_t c_q, c_maxp, _pad[2];
+  uint32_t c_q, c_maxp;
+  uint32_t ftail, ffree;           // FIFO: next record index to write; free-chunk list head
   WorkerRegs x;                    // RLT decision state in/out, e_i and counters
   uint32_t x_ri, _pad2[3];         // next unused draw of x_rbuf
   unsigned long long x_rbuf[32];   // RLT: 32 counter-based draws, one per lane
@@ -188,6 +233,8 @@ struct ReplayParams {
   uint32_t max_n, _pad1;
   WorkerLayout lay;
   AuxLayout aux;
+  FifoLayout fifo;
+  uint8_t* fifo_base;            // [grid][fifo.bytes] pending-FIFO pools (beta = 1 engine)
   kvr_service_model truth;
   kvr_policy defpol;
   const kvr_policy* policies;

@@ -1034,7 +1034,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
                            : sbase + (size_t)w * L.bytes;
   const WorkerView<Idx> S = make_view<Idx>(wbase, L);
   uint8_t* abase = p.aux_base + ((size_t)blockIdx.x * W + w) * p.aux.bytes;
-  double* fifo = reinterpret_cast<double*>(abase + p.aux.off_fifo);
+  // this CTA's pending-FIFO pool: chunk links, then 32-record chunks (FifoLayout)
+  uint32_t* flink = reinterpret_cast<uint32_t*>(p.fifo_base + (size_t)blockIdx.x * p.fifo.bytes);
+  double* fifo = reinterpret_cast<double*>(p.fifo_base + (size_t)blockIdx.x * p.fifo.bytes +
+                                           p.fifo.off_rec);
   RecencyLog R;
   R.log = reinterpret_cast<uint64_t*>(abase + p.aux.off_log);
   R.stamp = reinterpret_cast<uint16_t*>(wbase + L.off_stamp);
@@ -1059,7 +1062,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     const uint32_t trial = ctrl->trial;
     if (trial >= p.n_trials) break;
 
-    const TraceDev tr = p.traces[p.trial_trace ? p.trial_trace[trial] : 0];
+    const uint32_t tix = p.trial_trace ? p.trial_trace[trial] : 0u;
+    const bool tr_ok = tix < p.n_traces;   // else KVR_TRIAL_BAD_TRACE, trial not run
+    const TraceDev tr = p.traces[tr_ok ? tix : 0u];
     const kvr_policy& pol = ctrl->pol;   // shared memory, read on demand
     const uint64_t K = p.keys[trial];
     const uint32_t N = tr.N, bt = tr.block_tokens;
@@ -1109,6 +1114,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     if (lane == 0) {
       ws->active = 0;
       ws->c_probes = 0; ws->c_hit = 0; ws->c_in = 0; ws->c_q = 0; ws->c_maxp = 0;
+      ws->ftail = 0;        // record index of the next push (chunk boundary: allocate first)
+      ws->ffree = ~0u;      // this worker's free-chunk list (empty)
     }
     vmap[lane] = 0u;
     if (tid == 0) {
@@ -1121,6 +1128,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       ctrl->abortf[0] = 0;
       ctrl->abortf[1] = 0;
       ctrl->status = 0;
+      ctrl->fifo_bump = 0;
       for (int c = 0; c < 10; ++c) ctrl->cnt[c] = 0;
     }
     for (uint32_t b = tid; b < p.bins; b += blockDim.x) ctrl->hist[b] = 0;
@@ -1128,17 +1136,14 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     for (uint32_t kk = tid; kk <= p.max_n; kk += blockDim.x) divtab[kk] = (double)(bt * kk) / 1000.0;
 
     // a per-trial policy from device memory is validated here (host validated the default)
-    const bool pol_ok = pol.eviction <= KVR_EVICT_OPT && pol.rlt_fallback <= KVR_RLT_LRU_MARKED &&
-                        pol.router <= KVR_ROUTE_LBGR_RLS && pol.rho > 0.0 && pol.rho <= 1.0 &&
-                        (!rls || (pol.mu > 0.0 && pol.mu <= 1.0 && pol.rls_p0 > 0.0 &&
-                                  pol.rls_p0 < INFINITY)) &&
-                        pol.delta_t_ms > 0.0 &&
+    const bool pol_ok = policy_valid(pol) &&
                         (!opt || (W == 1 && (tr.nu != nullptr || N == 0))) &&
-                        pol.tracker_lag <= 1 && pol.tracker_grain >= 1 && (!pol.tracker_lag || defer) &&
+                        (!pol.tracker_lag || defer) &&
                         (kExt || (pol.eviction <= KVR_EVICT_RLT && pol.router <= KVR_ROUTE_RANDOM &&
                                   pol.tracker_lag == 0 && pol.tracker_grain == 1));
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
-    const uint32_t Nrun = pol_ok ? N : 0;
+    if (!tr_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_TRACE;
+    const uint32_t Nrun = (pol_ok && tr_ok) ? N : 0;
 
     // staging prologue: queries 0 .. kAhead-1
     uint32_t issued = min(Nrun, kAhead);
@@ -1208,8 +1213,22 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             }
           }
           if (fn != 0 && fr_c <= aq) {
-            fh = (fh + 1 == p.ring) ? 0 : fh + 1;
+            // pop the front record (its fields are in fr); an emptied chunk goes to this
+            // worker's free list and the head follows the chunk link
+            const uint32_t nh = fh + 1;
             --fn;
+            if ((nh & (kFifoChunk - 1)) == 0) {
+              const uint32_t c0 = (nh - 1) / kFifoChunk;
+              const uint32_t nxt = fn ? flink[c0] : 0u;
+              __syncwarp();
+              if (lane == 0) {
+                flink[c0] = ws->ffree;
+                ws->ffree = c0;
+              }
+              fh = fn ? nxt * kFifoChunk : nh;
+            } else {
+              fh = nh;
+            }
             if (lbgr) {
               const double fa = __shfl_sync(kFull, fr, 1), fE = __shfl_sync(kFull, fr, 2);
               const double g0 = __shfl_sync(kFull, fr, 3), g1 = __shfl_sync(kFull, fr, 4);
@@ -1421,7 +1440,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         double v = lane < W ? ctrl->score[par][lane] : INFINITY;
         if (v == 0.0) v = 0.0;
         const uint64_t bits = (uint64_t)__double_as_longlong(v);
-        const uint64_t key = (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+        // NaN ranks after every number (A37), padding lanes (+inf) after real workers
+        const uint64_t key = isnan(v) ? 0xfffffffffffffffeull
+                             : (lane >= W ? ~0ull
+                                          : ((bits >> 63) ? ~bits : (bits | 0x8000000000000000ull)));
         const uint32_t khi = (uint32_t)(key >> 32), klo = (uint32_t)key;
         const uint32_t mhi = __reduce_min_sync(kFull, khi);
         const uint32_t mlo = __reduce_min_sync(kFull, khi == mhi ? klo : 0xffffffffu);
@@ -1478,6 +1500,30 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         }
         continue;
       }
+      // FIFO push position: the tail chunk's next record, or a new chunk (own free list
+      // first, else the pool's bump counter) linked behind the tail
+      uint32_t ftail = ws->ftail;
+      if ((ftail & (kFifoChunk - 1)) == 0) {
+        uint32_t c = ws->ffree;
+        const bool reuse = c != ~0u;
+        const uint32_t nf = reuse ? flink[c] : 0u;
+        if (!reuse) c = ctrl->fifo_bump;
+        if (c >= p.fifo.chunks) {   // cannot happen with the FifoLayout bound; fail safe
+          if (lane == 0) {
+            ctrl->status = KVR_TRIAL_RING_OVERFLOW;
+            ctrl->abortf[par ^ 1] = 1;
+          }
+          continue;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (reuse) ws->ffree = nf;
+          else ctrl->fifo_bump = c + 1;
+          if (fn) flink[(ftail - 1) / kFifoChunk] = c;
+        }
+        ftail = c * kFifoChunk;
+      }
+      if (lane == 0) ws->ftail = ftail + 1;
       ++wr.wq;
       // log room for this query's n entries (Leaf-LRU order)
       if (use_list && wr.ltail - wr.lhead + n > p.aux.log_cap) {
@@ -1568,7 +1614,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       P = P + cost;
       KVR_T0(ta);
       {
-        const uint32_t slotf = (fh + fn >= p.ring) ? fh + fn - p.ring : fh + fn;
+        const uint32_t slotf = ftail;
+        if (fn == 0) fh = ftail;
         const double rE = lbgr ? score : 0.0, r0 = lbgr ? f0 : 0.0, r1 = lbgr ? f1 : 0.0,
                      r2 = lbgr ? f2 : 0.0, rC = lbgr ? Chat : 0.0;
         double val = 0.0;

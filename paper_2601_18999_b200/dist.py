@@ -1,11 +1,19 @@
 """Multi-GPU plumbing: trial sharding and the single summary reduce.
 
 Trials are independent replays (no exchange inside a replay), so a run shards
-them across ranks with no data-path collective.  Each rank runs one
-kvr_sim_run_multi over its trials; at the end one `torch.distributed.reduce`
-(NCCL over NVLink on a GPU box, gloo in the CPU tests) sums an int64 vector of
-summary counters to rank 0.  Floating-point aggregates stay per trial (the
-per-trial result buffers) so that 1-GPU and N-GPU reports are byte-identical.
+them across ranks with no data-path collective.  Each rank runs its
+kvr_sim_run_multi launches over its trials; at the end one
+`torch.distributed.reduce` (NCCL over NVLink on a GPU box, gloo in the CPU tests)
+sums an int64 vector of summary counters to rank 0.  Floating-point aggregates
+stay per trial (the per-trial result buffers).
+
+Two sharding modes are used by bench.py:
+* strong scaling (config 5, the default): ONE fixed trial list, trial t on rank
+  (t div 2) mod N (`bench.c5_shard`); a trial's key and policy depend on t only, so
+  its result bytes are identical at every N (P20; tests/test_gpu_bench_multirank.py);
+* weak scaling (config 2, `--workload c2`): every rank runs its own trials with
+  distinct keys (`weak_scaling_keys`), so N-GPU runs cover a different trial set.
+`shard_trials` (t mod N) is the plain strided split for other fixed lists.
 """
 from __future__ import annotations
 

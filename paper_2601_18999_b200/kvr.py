@@ -26,11 +26,11 @@ RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
 ROUTE_LBGR_RLS = 5   # LBGR, RLS reading of the 0.992 update (A8b)
 TRIAL_OK, TRIAL_RING_OVERFLOW, TRIAL_VICTIM_LOG_FULL, TRIAL_BAD_POLICY = 0, 1, 2, 3
-TRIAL_ADMISSION = 4
+TRIAL_ADMISSION, TRIAL_BAD_TRACE = 4, 5
 ERR_HASH_COLLISION = 4
 
 # C-ABI entry points declared in include/kvr.h (the not-gpu test checks they are exported)
-EXPORTS = ("kvr_last_error", "kvr_abi_version", "kvr_trace_packed_bytes", "kvr_trace_load",
+EXPORTS = ("kvr_last_error", "kvr_abi_version", "kvr_build_id", "kvr_trace_packed_bytes", "kvr_trace_load",
            "kvr_trace_info", "kvr_trace_chained_hashes", "kvr_trace_destroy",
            "kvr_trace_next_use_bytes", "kvr_trace_build_next_use", "kvr_trace_collision_bytes",
            "kvr_trace_check_collisions", "kvr_sim_create",
@@ -107,6 +107,7 @@ def lib():
         vp, u32, u64, st = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
         L.kvr_last_error.restype = C.c_char_p
         L.kvr_abi_version.restype = u32
+        L.kvr_build_id.restype = C.c_char_p
         sig = {
             "kvr_trace_packed_bytes": [vp, vp, vp],
             "kvr_trace_load": [vp, vp, C.c_size_t, vp, C.c_size_t, vp, vp],
@@ -158,6 +159,10 @@ def kvr_abi_version() -> int:
 
 def kvr_last_error() -> str:
     return lib().kvr_last_error().decode(errors="replace")
+
+
+def kvr_build_id() -> str:
+    return lib().kvr_build_id().decode()
 
 
 def kvr_trace_packed_bytes(desc: kvr_trace_desc):
@@ -280,7 +285,9 @@ class Policy:
     est_alpha_miss_ms: float = 1.0
     rho: float = 31.0 / 32.0
     delta_t_ms: float = 20.0
-    mu: float = 0.992
+    # NLMS step of router 0 (reading A8, revised r2: 1 - 0.992 = 0.008) or the RLS forgetting
+    # factor of router 5 (A8b: 0.992); None = that router's default
+    mu: Optional[float] = None
     theta0: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
     tau: float = 1.5
     w_hit: float = 1.0
@@ -288,6 +295,14 @@ class Policy:
     rls_p0: float = 1000.0     # LBGR_RLS initial covariance P = rls_p0 * I
     tracker_lag: int = 0       # A29: router's h~ lags the previous query's update
     tracker_grain: int = 1     # A29: router sees whole grains of matched blocks
+
+    def mu_value(self) -> float:
+        if self.mu is not None:
+            return float(self.mu)
+        return 0.992 if self.router == ROUTE_LBGR_RLS else 0.008
+
+    def _get(self, f):
+        return self.mu_value() if f == "mu" else getattr(self, f)
 
     def c(self) -> kvr_policy:
         p = kvr_policy()
@@ -298,14 +313,14 @@ class Policy:
                 for k in range(4):
                     p.theta0[k] = float(self.theta0[k])
             else:
-                setattr(p, f, getattr(self, f))
+                setattr(p, f, self._get(f))
         return p
 
     def row(self) -> np.ndarray:
         r = np.zeros((), dtype=POLICY_DTYPE)
         for f in POLICY_DTYPE.names:
             if f != "_pad":
-                r[f] = getattr(self, f)
+                r[f] = self._get(f)
         return r
 
 

@@ -27,14 +27,14 @@ out_path = sys.argv[3] if len(sys.argv) > 3 else None
 
 import bench  # noqa: E402  (config 2's trace recipe: the bench's r = 0.5 GSP trace)
 
-W = bench.W_WORKERS
-tr = bench.build_traces(nq)[1]
+W = bench.C2_W
+tr = bench.c2_traces(nq)[1]
 dt = DeviceTrace(tr)
 L_max = int(tr.max_blocks)
 rows = []
 for beta, B in ((0, 512), (1, 512), (2, 512), (3, 512), (4, 8 * L_max), (8, 8 * L_max), (0, 8 * L_max)):
     for ev, ename in ((1, "RLT"), (0, "L-LRU")):
-        sim = Simulator(W, B, pending_ring=bench.RING, batch_slots=beta)
+        sim = Simulator(W, B, pending_ring=16384, batch_slots=beta)
         keys = np.arange(1, K + 1, dtype=np.uint64)
         pols = policies_array([Policy(eviction=ev) for _ in range(K)])
         b = sim.alloc([dt], K)
@@ -69,5 +69,5 @@ for beta, B in ((0, 512), (1, 512), (2, 512), (3, 512), (4, 8 * L_max), (8, 8 * 
 
 if out_path:
     with open(out_path, "w") as f:
-        json.dump(dict(workload=f"config-2 bench trace r=0.5 (bench.build_traces()[1]), W={W}, {tr.n_queries} queries, LBGR (App. A)",
+        json.dump(dict(workload=f"config-2 bench trace r=0.5 (bench.c2_traces()[1]), W={W}, {tr.n_queries} queries, LBGR (App. A)",
                        rows=rows), f, indent=1)

@@ -35,7 +35,13 @@ def test_header_declares_the_north_star_entry_points():
 def test_library_exports_every_declared_symbol(libkvr):
     for name in _declared():
         assert hasattr(libkvr, name), name
-    assert libkvr.kvr_abi_version() == 6
+    assert libkvr.kvr_abi_version() == 7
+
+
+def test_library_is_built_from_these_sources(libkvr):
+    """Build provenance: the loaded libkvr.so carries the source hash of this tree."""
+    from paper_2601_18999_b200 import build, kvr
+    assert kvr.kvr_build_id() == build.source_hash()
 
 
 def test_struct_sizes_match_header(libkvr):

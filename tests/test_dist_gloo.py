@@ -81,3 +81,46 @@ def test_gloo_world2_reduce_matches_single_process():
     got = np.array(got, dtype=np.int64).view(np.uint64)
     ref[12] = 2 * 123          # the trace-hash slot sums one copy per rank
     assert np.array_equal(got, ref)
+
+
+def test_c5_fixed_list_sharding():
+    """bench.py's config-5 plan: one fixed list of trials, rank r takes (t div 2) mod N == r;
+    the union over ranks is the list at every N, shares differ by at most 2 trials, and
+    every rank gets both evictions (RLT on even keys t + 1, Leaf-LRU on odd)."""
+    import bench
+    n = 65536
+    cell = bench.c5_cell_of(n)
+    sizes = np.bincount(cell, minlength=48)
+    assert sizes.min() >= n // 48 and sizes.max() <= n // 48 + 1
+    for world in (1, 2, 3, 4, 8):
+        parts = [bench.c5_shard(n, r, world) for r in range(world)]
+        allt = np.sort(np.concatenate(parts))
+        assert np.array_equal(allt, np.arange(n))
+        lens = [len(p) for p in parts]
+        assert max(lens) - min(lens) <= 2
+        for p in parts:
+            keys = p + 1
+            assert (keys % 2 == 0).any() and (keys % 2 == 1).any()
+            # balanced per cell as well: each rank's share of a cell is within 2 of n/48/world
+            per = np.bincount(cell[p], minlength=48)
+            assert per.max() - per.min() <= 3
+
+
+def test_c5_plan_launches_cover_the_share():
+    """The per-W launches of a rank hold exactly its share, longest trace first."""
+    import bench
+
+    class _T:   # stand-in traces: only n_queries matters to the plan
+        def __init__(self, n):
+            self.n_queries = n
+    traces = {W: [_T(100 * (k + 1) + W) for k in range(12)] for W in bench.C5_WS}
+    n, world = 960, 4
+    for r in range(world):
+        ls = bench.c5_plan(r, world, n, traces=traces)
+        got = np.sort(np.concatenate([L.tids for L in ls]))
+        assert np.array_equal(got, bench.c5_shard(n, r, world))
+        for L in ls:
+            nq = np.array([L.traces[i].n_queries for i in L.trial_trace])
+            assert np.all(np.diff(nq) <= 0)
+            assert np.array_equal(L.keys, (L.tids + 1).astype(np.uint64))
+            assert np.array_equal(L.evict, (L.keys % 2 == 0).astype(np.uint32))

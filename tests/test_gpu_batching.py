@@ -148,15 +148,15 @@ def test_config2_full_trace_sampled(kvr, oracle_mod):
     import bench
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
     from parity_util import assert_result_equal
-    tr = bench.build_traces()[1]
-    sim = Simulator(bench.W_WORKERS, bench.B_BLOCKS, pending_ring=bench.RING, batch_slots=3)
+    tr = bench.c2_traces()[1]
+    sim = Simulator(bench.C2_W, bench.B_BLOCKS, pending_ring=16384, batch_slots=3)
     keys = np.arange(1, 65, dtype=np.uint64)
     pols = [kvr.Policy(eviction=int(k) % 2) for k in keys]
     out = sim.run(DeviceTrace(tr), keys, policies_array(pols))
     assert np.all(out.results["status"] == 0)
     assert np.all(out.results["queries"] == tr.n_queries)
-    cfg = oracle_mod.OracleConfig(W=bench.W_WORKERS, capacity_blocks=bench.B_BLOCKS,
-                                  pending_ring=bench.RING, batch_slots=3)
+    cfg = oracle_mod.OracleConfig(W=bench.C2_W, capacity_blocks=bench.B_BLOCKS,
+                                  pending_ring=16384, batch_slots=3)
     for t in (0, 63):
         o = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=int(keys[t]) % 2), int(keys[t]))
         assert o.rc == 0
