@@ -406,7 +406,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2601_18999_b200 import dist as kdist
-    from paper_2601_18999_b200.kvr import RESULT_DTYPE, DeviceTrace, Simulator
+    from paper_2601_18999_b200.kvr import POLICY_DTYPE, RESULT_DTYPE, DeviceTrace, Simulator
 
     # KVR_BENCH_BACKEND=gloo (tests only): several ranks on one GPU, collectives staged
     # through host copies; the contract run uses NCCL, one rank per GPU
@@ -439,7 +439,7 @@ def main():
         buf = sim.alloc(dts, max(1, n), 0, dev)
         if n:
             buf["keys"][:n].copy_(torch.from_numpy(L.keys.view(np.int64)))
-            buf["policies"][: n * 128].copy_(torch.from_numpy(L.policies().view(np.uint8)))
+            buf["policies"][: n * POLICY_DTYPE.itemsize].copy_(torch.from_numpy(L.policies().view(np.uint8)))
             buf["trial_trace"][:n].copy_(torch.from_numpy(L.trial_trace.view(np.int32)))
         # every rank packs the same traces; their identity checksum rides in the reduce
         trace_hash += sum(d.identity_digest() for d in dts)
@@ -590,7 +590,7 @@ def e2e_measure(launches, dev, stream, args):  # noqa: C901
     (validates, chains) them, kvr_sim_run_multi replays, and the per-trial results come
     back device->host into pinned memory, all inside the timed region."""
     import torch
-    from paper_2601_18999_b200.kvr import RESULT_DTYPE, DeviceTrace, Simulator
+    from paper_2601_18999_b200.kvr import POLICY_DTYPE, RESULT_DTYPE, DeviceTrace, Simulator
 
     per = []
     h2d, d2h = 0, 0

@@ -37,12 +37,16 @@
 extern "C" {
 #endif
 
-#define KVR_ABI_VERSION 7u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
+#define KVR_ABI_VERSION 8u   /* 2: OPT, next-use index, LBGR_RLS; 3: tracker_lag / tracker_grain;
                                 4: kvr_sim_config.extended_policies;
                                 5: kvr_sim_config.batch_slots (continuous batching);
                                 6: kvr_trace_collision_bytes / kvr_trace_check_collisions;
                                 7: KVR_TRIAL_BAD_TRACE, kvr_build_id, pooled pending FIFOs
-                                   (pending_ring may be as large as the trace) */
+                                   (pending_ring may be as large as the trace);
+                                8: KVR_ROUTE_CACHE_AWARE + kvr_policy.ca_* (160-B policy),
+                                   tracker_lag up to KVR_MAX_TRACKER_LAG at any capacity,
+                                   phase ledger (kvr_trace_build_phases, kvr_sim_run_ledger) */
+#define KVR_MAX_TRACKER_LAG 32u
 
 typedef int32_t kvr_status;
 enum {
@@ -152,6 +156,25 @@ kvr_status kvr_trace_build_next_use(const kvr_trace* tr, uint32_t* d_nu, size_t 
                                     void* d_scratch, size_t scratch_bytes, void* stream,
                                     kvr_trace** out);
 
+/* Phase index for the phase-ledger analysis ("we partition Q~ into
+ * disjoint phases, where each phase contains exactly B_i distinct tokens"; SURVEY
+ * §8f #1; reading A39): the flattened block-access sequence (Gamma_1 || Gamma_2 ...)
+ * is cut greedily into phases of exactly B distinct identities (the last possibly
+ * fewer).  d_phase (DEVICE, caller-owned, >= phase_bytes) receives
+ *   u32 ph[n_blocks_total]  phase of occurrence o | 0x80000000 if o is the first
+ *                           appearance of its identity in that phase ("new" token)
+ *   u32 nx[n_blocks_total]  index of the identity's next occurrence, 0xFFFFFFFF if none
+ *   u32 distinct[n_phases]  distinct identities per phase
+ * and *n_phases (host, written before return: SYNCHRONOUS on `stream`) the phase count.
+ * d_scratch (DEVICE, caller-owned) is only used during the call.  Returns a NEW handle
+ * that borrows tr's packed buffer, tr's next-use index (if any) and d_phase; tr is
+ * unchanged.  INVALID_ARG for B = 0 / null buffers, WORKSPACE_TOO_SMALL,
+ * UNSUPPORTED for >= 2^31 blocks. */
+kvr_status kvr_trace_phase_bytes(const kvr_trace* tr, size_t* phase_bytes, size_t* scratch_bytes);
+kvr_status kvr_trace_build_phases(const kvr_trace* tr, uint32_t B, uint32_t* d_phase,
+                                  size_t phase_bytes, void* d_scratch, size_t scratch_bytes,
+                                  void* stream, uint32_t* n_phases, kvr_trace** out);
+
 /* --------------------------------------------------------------- policies */
 /* KVR_EVICT_OPT: offline Belady for competitive ratios: evict the leaf
  * != parent(t) whose next use is furthest; leaves never used again first (lowest
@@ -170,10 +193,19 @@ typedef enum { KVR_ROUTE_LBGR = 0,           /* Alg. 2 / Eq. 4-6 */
                KVR_ROUTE_THRESHOLD = 2,      /* cache-aware: balance if max>tau*max(1,min) (A16) */
                KVR_ROUTE_ROUND_ROBIN = 3,    /* j mod W */
                KVR_ROUTE_RANDOM = 4,         /* Philox(K,(j,0xFFFFFFFF,2)) */
-               KVR_ROUTE_LBGR_RLS = 5        /* LBGR with the RLS reading of "learning rate
+               KVR_ROUTE_LBGR_RLS = 5,       /* LBGR with the RLS reading of "learning rate
                                                 0.992" (reading A8b): exponentially
                                                 weighted least squares, forgetting factor mu,
                                                 P(0) = rls_p0 * I */
+               KVR_ROUTE_CACHE_AWARE = 6     /* SGLang-style cache-aware rule ("switches
+                                                between the highest-hit-rate and the least-loaded
+                                                routing based on a predefined heuristic load-balance
+                                                threshold"; reading A38): pending
+                                                loads imbalanced iff max-min > ca_balance_abs AND
+                                                max > ca_balance_rel*min -> least loaded; else the
+                                                highest match h~ if h~/|q| > ca_cache_threshold,
+                                                else the worker with the fewest cached blocks.
+                                                Lowest index on ties (A15). */
 } kvr_router;
 
 /* Eq. 1 ground truth: Cost = aC*h + aM*(|q|-h) + o*|a| (A13, A14) */
@@ -188,10 +220,16 @@ typedef struct {
   double tau;                                     /* THRESHOLD */
   double w_hit, w_load;                           /* STATIC_LINEAR */
   double rls_p0;                                  /* LBGR_RLS: initial covariance scale (> 0) */
-  uint32_t tracker_lag;    /* App. E / reading A29: 1 = the router's hit estimate h~ does not
-                              yet include the previous query's cache update (needs B <= 1024) */
+  uint32_t tracker_lag;    /* App. E ("staleness ... caused by concurrent updates") /
+                              reading A29: k in 0..KVR_MAX_TRACKER_LAG; the router's hit
+                              estimate h~ for query j is matched on the caches as they were
+                              after query j-1-k (the last k cache updates are not yet seen) */
   uint32_t tracker_grain;  /* A29: the router sees grain*floor(m/grain) matched blocks (>= 1);
                               service times (Eq. 1) always use the true h */
+  double ca_balance_abs;   /* KVR_ROUTE_CACHE_AWARE (A38): absolute pending-load gap */
+  double ca_balance_rel;   /*   relative pending-load ratio */
+  double ca_cache_threshold; /* minimum match rate h~/|q| for the highest-match branch */
+  uint64_t _pad2;
 } kvr_policy;
 
 typedef struct {
@@ -282,6 +320,24 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
                              kvr_query_record* d_records, uint64_t* d_victims,
                              uint64_t victims_cap, void* d_workspace, size_t workspace_bytes,
                              void* stream);
+
+/* Phase-ledger run (Lemmas 1-3, Thm 3): the same replay as
+ * kvr_sim_run on a trace from kvr_trace_build_phases (built for this sim's B), W = 1
+ * only (the single-cache analysis of §3.2), every trial counting per phase v:
+ *   d_ledger[t*4*n_phases + 4v + 0]  distinct identities of the phase
+ *                             + 1    misses
+ *                             + 2    misses at first appearances ("new" tokens; the
+ *                                    misses on "old" tokens are [1] - [2])
+ *                             + 3    clean tokens: first appearances of identities that
+ *                                    were not in this trial's cache at the end of phase
+ *                                    v-1 (reading A39)
+ * d_ledger: DEVICE u32 [n_trials * 4 * n_phases].  Records / histograms / victims are
+ * not produced.  INVALID_ARG for W != 1, a trace without a phase index or one built
+ * for another B, or batch_slots > 0.  Asynchronous on `stream`. */
+kvr_status kvr_sim_run_ledger(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
+                              const uint64_t* d_philox_keys, const kvr_policy* d_policies,
+                              kvr_trial_result* d_results, uint32_t* d_ledger,
+                              void* d_workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

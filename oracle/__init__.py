@@ -14,8 +14,8 @@ from .binding import (  # noqa: F401
     EVICT_LRU, EVICT_RLT, EVICT_OPT,
     RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED,
     ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM,
-    ROUTE_LBGR_RLS,
+    ROUTE_LBGR_RLS, ROUTE_CACHE_AWARE, MAX_TRACKER_LAG, LEDGER_FIELDS,
     OracleConfig, OraclePolicy, build_oracle, lib,
     fmix64, philox4x32_10, chain, run, single_replay, bruteforce_min_misses, rls_step,
-    rlt_exact_expectation, count_collisions,
+    rlt_exact_expectation, count_collisions, phase_ledger,
 )

@@ -18,6 +18,8 @@ EVICT_LRU, EVICT_RLT, EVICT_OPT = 0, 1, 2
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
 ROUTE_LBGR_RLS = 5   # LBGR with the RLS reading of the 0.992 update (A8b)
+ROUTE_CACHE_AWARE = 6   # SGLang-style cache-aware rule (A38)
+MAX_TRACKER_LAG = 32
 
 
 def build_oracle(force: bool = False) -> str:
@@ -47,7 +49,9 @@ class _Policy(C.Structure):
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
                 ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double),
-                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32)]
+                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32),
+                ("ca_balance_abs", C.c_double), ("ca_balance_rel", C.c_double),
+                ("ca_cache_threshold", C.c_double), ("_pad2", C.c_uint64)]
 
 
 class _Config(C.Structure):
@@ -93,6 +97,9 @@ def lib():
                                          C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64),
                                          C.c_void_p, C.c_void_p, C.c_uint32,
                                          C.POINTER(C.c_uint32)]
+        L.kvro_phase_ledger.argtypes = [C.POINTER(_Trace), C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_uint64, C.c_void_p, C.c_uint32,
+                                        C.POINTER(C.c_uint32)]
         L.kvro_bruteforce_min_misses.argtypes = [C.POINTER(_Trace), C.c_uint32,
                                                  C.POINTER(C.c_uint64)]
         L.kvro_rlt_exact_expectation.argtypes = [C.POINTER(_Trace), C.c_uint32, C.c_uint32,
@@ -120,8 +127,11 @@ class OraclePolicy:
     w_hit: float = 1.0
     w_load: float = 1.0
     rls_p0: float = 1000.0
-    tracker_lag: int = 0       # A29: router lags the previous query's update
+    tracker_lag: int = 0       # A29: router lags the last k queries' updates
     tracker_grain: int = 1     # A29: router sees whole grains of matched blocks
+    ca_balance_abs: float = 32.0        # A38 (router 6): imbalance iff max-min > abs
+    ca_balance_rel: float = 1.0001      #   and max > rel * min (pending queries)
+    ca_cache_threshold: float = 0.5     #   highest match if h~/|q| > threshold
 
     def _c(self) -> _Policy:
         p = _Policy()
@@ -134,6 +144,8 @@ class OraclePolicy:
         p.tau, p.w_hit, p.w_load = self.tau, self.w_hit, self.w_load
         p.rls_p0 = self.rls_p0
         p.tracker_lag, p.tracker_grain = self.tracker_lag, self.tracker_grain
+        p.ca_balance_abs, p.ca_balance_rel = self.ca_balance_abs, self.ca_balance_rel
+        p.ca_cache_threshold = self.ca_cache_threshold
         return p
 
 
@@ -260,6 +272,28 @@ def single_replay(tr, B: int, eviction: int, fallback: int = RLT_EARLY_RESET,
     if rc:
         raise ValueError(f"kvro_single_replay rc={rc}")
     return int(tm.value), flags[:total]
+
+
+LEDGER_FIELDS = ("distinct", "misses", "first_misses", "clean")
+
+
+def phase_ledger(tr, B: int, eviction: int, fallback: int = RLT_EARLY_RESET,
+                 philox_key: int = 0) -> np.ndarray:
+    """Per-phase ledger of one single-cache replay (A39): u32 array
+    [n_phases, 4] of (distinct, misses, first_misses, clean); old-token misses are
+    misses - first_misses."""
+    a = _TraceArgs(tr)
+    n = C.c_uint32(0)
+    rc = lib().kvro_phase_ledger(C.byref(a.c), B, eviction, fallback, C.c_uint64(philox_key),
+                                 None, 0, C.byref(n))
+    if rc not in (0, 1, 3):
+        raise ValueError(f"kvro_phase_ledger rc={rc}")
+    out = np.zeros((max(1, n.value), 4), dtype=np.uint32)
+    rc = lib().kvro_phase_ledger(C.byref(a.c), B, eviction, fallback, C.c_uint64(philox_key),
+                                 out.ctypes.data, n.value, C.byref(n))
+    if rc:
+        raise ValueError(f"kvro_phase_ledger rc={rc}")
+    return out[: n.value]
 
 
 def bruteforce_min_misses(tr, B: int) -> int:

@@ -81,16 +81,50 @@ uint32_t first_min(const std::vector<double>& s, uint32_t W) {
   return best;
 }
 
+// Cache-aware routing as SGLang's router does it ("switches between the
+// highest-hit-rate and the least-loaded routing based on a predefined heuristic
+// load-balance threshold"; reading A38): the load is imbalanced iff
+// max - min > abs AND max > rel * min (pending queries); then the least loaded
+// worker; else the highest match (router's view h~) if its rate h~/|q| exceeds the
+// cache threshold, else the worker holding the fewest cached blocks (the most free
+// capacity).  Lowest index on every tie (A15).
+uint32_t cache_aware_choice(const kvro_policy* pol, const std::vector<uint64_t>& pending,
+                            const std::vector<uint32_t>& mview, const std::vector<uint64_t>& size,
+                            uint32_t W, uint32_t block_tokens, uint32_t q) {
+  uint64_t mx = pending[0], mn = pending[0];
+  for (uint32_t i = 1; i < W; ++i) {
+    mx = std::max(mx, pending[i]);
+    mn = std::min(mn, pending[i]);
+  }
+  const bool imbalanced = ((double)(mx - mn) > pol->ca_balance_abs) &&
+                          ((double)mx > pol->ca_balance_rel * (double)mn);
+  uint32_t best = 0;
+  if (imbalanced) {
+    for (uint32_t i = 1; i < W; ++i)
+      if (pending[i] < pending[best]) best = i;
+    return best;
+  }
+  for (uint32_t i = 1; i < W; ++i)
+    if (mview[i] > mview[best]) best = i;
+  const double rate = (double)(block_tokens * mview[best]) / (double)q;
+  if (rate > pol->ca_cache_threshold) return best;
+  best = 0;
+  for (uint32_t i = 1; i < W; ++i)
+    if (size[i] < size[best]) best = i;
+  return best;
+}
+
 // per-trial policy checks shared by both engines (A8: NLMS needs 0 <= mu < 2;
 // every parameter finite except delta_t_ms = +inf, which means no decay)
 bool policy_valid(const kvro_policy* p) {
   if (p->eviction > KVRO_EVICT_OPT || p->rlt_fallback > KVRO_RLT_LRU_MARKED ||
-      p->router > KVRO_ROUTE_LBGR_RLS)
+      p->router > KVRO_ROUTE_CACHE_AWARE)
     return false;
-  if (p->tracker_lag > 1 || p->tracker_grain < 1) return false;
+  if (p->tracker_lag > KVRO_MAX_TRACKER_LAG || p->tracker_grain < 1) return false;
   if (!(p->rho > 0.0 && p->rho <= 1.0) || !(p->delta_t_ms > 0.0)) return false;
   const double fin[] = {p->est_alpha_cached_ms, p->est_alpha_miss_ms, p->mu, p->theta0[0],
-                        p->theta0[1], p->theta0[2], p->theta0[3], p->tau, p->w_hit, p->w_load};
+                        p->theta0[1], p->theta0[2], p->theta0[3], p->tau, p->w_hit, p->w_load,
+                        p->ca_balance_abs, p->ca_balance_rel, p->ca_cache_threshold};
   for (double v : fin)
     if (!std::isfinite(v)) return false;
   if (p->router == KVRO_ROUTE_LBGR && !(p->mu >= 0.0 && p->mu < 2.0)) return false;
@@ -167,6 +201,9 @@ struct UpdateCtx {
   // accessed, and only unpinned leaves are eviction candidates
   bool pinning = false;
   bool admission_fail = false;  // full cache and no unpinned leaf
+  // phase ledger (kvro_phase_ledger): called with the cache as it stands before the
+  // d-th block access of the path is processed
+  std::function<void(const Cache&, uint32_t)> before_access;
 };
 
 // (stamp, -depth) order of Leaf-LRU (A7): true if a is less recently used.
@@ -179,6 +216,7 @@ bool lru_less(const Node& a, const Node& b) {
 // Leaf-LRU, block by block in path order.
 void update_cache(Cache& C, const uint64_t* H, uint32_t n, UpdateCtx& x) {
   for (uint32_t d = 0; d < n; ++d) {
+    if (x.before_access) x.before_access(C, d);
     const uint64_t t = H[d];
     const bool has_p = d > 0;
     const uint64_t p = has_p ? H[d - 1] : 0;
@@ -658,6 +696,13 @@ int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy*
         for (uint32_t i = 1; i < W; ++i)
           if (m[i] > m[best]) best = i;
       }
+    } else if (pol->router == KVRO_ROUTE_CACHE_AWARE) {   // A38; pending = waiting + in flight
+      std::vector<uint64_t> pend(W), size(W);
+      for (uint32_t i = 0; i < W; ++i) {
+        pend[i] = pending(i);
+        size[i] = w[i].cache.S.size();
+      }
+      best = cache_aware_choice(pol, pend, m, size, W, tr->block_tokens, q);
     } else if (pol->router == KVRO_ROUTE_ROUND_ROBIN) {
       best = j % W;
     } else {
@@ -816,8 +861,10 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
   uint64_t vcursor = 0;
   bool vlog_full = false;
   std::vector<uint32_t> m(W), mt(W);   // true match, and the tracker's view of it (A29)
-  Cache prev_cache;                      // the previous chooser's cache before its update
-  int64_t prev_worker = -1;
+  // global tracker lag (A29): the caches of the last k choosers as they were before
+  // their updates, oldest first; the router's view of worker i is the oldest copy of
+  // i in the window (the cache after query j-1-k), else its current cache
+  std::deque<std::pair<uint32_t, Cache>> lagged;
   std::vector<double> Ehat(W), Chat(W), phi0(W), phi1(W), phi2(W);
 
   for (uint32_t j = 0; j < tr->n_queries; ++j) {
@@ -886,8 +933,10 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
       out->probes += std::min<uint64_t>(m[i] + 1, n_in);
       // global tracker (App. E; reading A29): the router's estimate h~
       // lags the previous query's update and is coarsened to whole grains
-      uint32_t v = (pol->tracker_lag && (int64_t)i == prev_worker)
-                       ? match_prefix(prev_cache, Hj, n_in) : m[i];
+      const Cache* view = &w[i].cache;
+      for (auto it = lagged.rbegin(); it != lagged.rend(); ++it)
+        if (it->first == i) view = &it->second;   // ends at the oldest copy of worker i
+      uint32_t v = view == &w[i].cache ? m[i] : match_prefix(*view, Hj, n_in);
       mt[i] = pol->tracker_grain * (v / pol->tracker_grain);
     }
 
@@ -930,6 +979,13 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
         for (uint32_t i = 1; i < W; ++i)
           if (mt[i] > mt[best]) best = i;
       }
+    } else if (pol->router == KVRO_ROUTE_CACHE_AWARE) {     // A38
+      std::vector<uint64_t> pend(W), size(W);
+      for (uint32_t i = 0; i < W; ++i) {
+        pend[i] = w[i].fifo.size();
+        size[i] = w[i].cache.S.size();
+      }
+      best = cache_aware_choice(pol, pend, mt, size, W, tr->block_tokens, q);
     } else if (pol->router == KVRO_ROUTE_ROUND_ROBIN) {
       best = j % W;
     } else {  // RANDOM
@@ -963,9 +1019,9 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
       if (it == v.end()) return {UINT64_MAX, 0};
       return {*it, depth_of[id]};
     };
-    if (pol->tracker_lag) {   // the tracker will still see this cache at the next query
-      prev_cache = xs.cache;
-      prev_worker = best;
+    if (pol->tracker_lag) {   // the tracker still sees this cache for the next k queries
+      lagged.emplace_back(best, xs.cache);
+      if (lagged.size() > pol->tracker_lag) lagged.pop_front();
     }
     update_cache(xs.cache, Hj, n_in + n_out, ux);
     if (ux.invariant_violation) return 9;
@@ -1169,6 +1225,95 @@ struct BF {
   }
 };
 }  // namespace
+
+// Phase ledger (reading A39): phases of exactly B distinct blocks over the
+// flattened access sequence, and per phase the misses of one single-cache replay and
+// the clean tokens relative to that replay's own cache at the end of the previous phase.
+int kvro_phase_ledger(const kvro_trace* tr, uint32_t B, uint32_t eviction, uint32_t fallback,
+                      uint64_t K, uint32_t* ledger, uint32_t max_phases, uint32_t* n_phases) {
+  if (validate_trace(tr) || B < 1 || eviction > KVRO_EVICT_OPT || fallback > KVRO_RLT_LRU_MARKED ||
+      !n_phases)
+    return 1;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)
+    if ((uint64_t)tr->n_in_blocks[j] + tr->n_out_blocks[j] > B) return 2;
+  const std::vector<uint64_t> H = chain_all(tr);
+  const uint64_t total = H.size();
+  // 1. greedy phases over the access sequence: a phase ends just before the access
+  //    that would be its (B+1)-th distinct block
+  std::vector<uint32_t> phase_of(total);
+  std::vector<uint8_t> first(total);
+  std::vector<uint64_t> start;   // first access of every phase
+  {
+    std::unordered_set<uint64_t> seen;
+    for (uint64_t o = 0; o < total; ++o) {
+      if (!seen.count(H[o])) {
+        if (seen.size() == B || start.empty()) {
+          start.push_back(o);
+          seen.clear();
+        }
+        seen.insert(H[o]);
+        first[o] = 1;
+      }
+      phase_of[o] = (uint32_t)start.size() - 1;
+    }
+  }
+  *n_phases = (uint32_t)start.size();
+  if (start.size() > max_phases) return 3;
+  if (!ledger) return 1;
+  std::memset(ledger, 0, sizeof(uint32_t) * 4 * start.size());
+  // 2. the single-cache replay; the cache is copied at every phase start
+  std::unordered_map<uint64_t, std::vector<uint64_t>> occ;
+  std::unordered_map<uint64_t, uint32_t> depth_of;
+  if (eviction == KVRO_EVICT_OPT)
+    for (uint32_t j = 0; j < tr->n_queries; ++j)
+      for (uint64_t o = tr->block_offsets[j]; o < tr->block_offsets[j + 1]; ++o) {
+        occ[H[o]].push_back(j);
+        depth_of[H[o]] = (uint32_t)(o - tr->block_offsets[j]) + 1;
+      }
+  Cache C;
+  C.B = B;
+  std::vector<uint8_t> flags;
+  std::unordered_set<uint64_t> at_start;   // cache content at the start of the current phase
+  uint64_t e = 0;
+  for (uint32_t j = 0; j < tr->n_queries; ++j) {
+    const uint64_t off = tr->block_offsets[j];
+    UpdateCtx ux;
+    ux.eviction = eviction;
+    ux.fallback = fallback;
+    ux.j = j;
+    ux.miss_flags = &flags;
+    ux.choose = [&](uint64_t nU) -> uint64_t { return pick(philox_r64(K, e++, 0, 1), nU); };
+    const uint64_t jj = j;
+    ux.next_use = [&](uint64_t id) -> std::pair<uint64_t, uint32_t> {
+      const std::vector<uint64_t>& v = occ[id];
+      auto it = std::upper_bound(v.begin(), v.end(), jj);
+      if (it == v.end()) return {UINT64_MAX, 0};
+      return {*it, depth_of[id]};
+    };
+    ux.before_access = [&](const Cache& c, uint32_t d) {
+      const uint64_t o = off + d;
+      if (o == start[phase_of[o]]) {   // the end of phase v-1: remember the cache
+        at_start.clear();
+        for (auto& kv : c.S) at_start.insert(kv.first);
+      }
+      uint32_t* L = ledger + 4 * (size_t)phase_of[o];
+      if (first[o]) {
+        L[0] += 1;
+        if (!at_start.count(H[o])) L[3] += 1;   // clean: not cached when the phase began
+      }
+    };
+    const uint32_t n = (uint32_t)(tr->block_offsets[j + 1] - off);
+    update_cache(C, H.data() + off, n, ux);
+    if (ux.invariant_violation) return 9;
+    for (uint32_t d = 0; d < n; ++d)
+      if (flags[off + d]) {
+        uint32_t* L = ledger + 4 * (size_t)phase_of[off + d];
+        L[1] += 1;
+        if (first[off + d]) L[2] += 1;
+      }
+  }
+  return 0;
+}
 
 int kvro_bruteforce_min_misses(const kvro_trace* tr, uint32_t B, uint64_t* min_misses) {
   if (validate_trace(tr) || B < 1 || !min_misses) return 1;

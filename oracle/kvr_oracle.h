@@ -52,7 +52,9 @@ enum { KVRO_EVICT_LRU = 0, KVRO_EVICT_RLT = 1, KVRO_EVICT_OPT = 2 /* Belady, P:1
 enum { KVRO_RLT_EARLY_RESET = 0, KVRO_RLT_UNIFORM_LEAF = 1, KVRO_RLT_LRU_MARKED = 2 };
 enum { KVRO_ROUTE_LBGR = 0, KVRO_ROUTE_STATIC_LINEAR = 1, KVRO_ROUTE_THRESHOLD = 2,
        KVRO_ROUTE_ROUND_ROBIN = 3, KVRO_ROUTE_RANDOM = 4,
-       KVRO_ROUTE_LBGR_RLS = 5 /* LBGR with the RLS reading of "0.992" (A8b) */ };
+       KVRO_ROUTE_LBGR_RLS = 5 /* LBGR with the RLS reading of "0.992" (A8b) */,
+       KVRO_ROUTE_CACHE_AWARE = 6 /* SGLang-style cache-aware rule (reading A38) */ };
+#define KVRO_MAX_TRACKER_LAG 32u
 /* per-trial status codes */
 enum { KVRO_TRIAL_OK = 0, KVRO_TRIAL_RING_OVERFLOW = 1, KVRO_TRIAL_VICTIM_LOG_FULL = 2,
        KVRO_TRIAL_ADMISSION = 4 /* batched: full cache, every leaf in flight */ };
@@ -77,8 +79,14 @@ typedef struct {
   double tau;
   double w_hit, w_load;
   double rls_p0;                  /* LBGR_RLS: initial covariance P = rls_p0 * I */
-  uint32_t tracker_lag;           /* A29: 1 = the router does not yet see the previous query's update */
+  uint32_t tracker_lag;           /* A29: k = the router does not yet see the last k queries'
+                                     cache updates (0..KVRO_MAX_TRACKER_LAG) */
   uint32_t tracker_grain;         /* A29: the router sees grain * floor(m / grain) matched blocks (>= 1) */
+  double ca_balance_abs;          /* A38 cache-aware: imbalanced iff max-min pending > abs */
+  double ca_balance_rel;          /*   and max pending > rel * min pending */
+  double ca_cache_threshold;      /*   else highest match if its rate h~/|q| > threshold,
+                                       else the worker with the fewest cached blocks */
+  uint64_t _pad2;
 } kvro_policy;
 
 typedef struct {
@@ -139,6 +147,20 @@ int kvro_run(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy* po
 int kvro_single_replay(const kvro_trace* tr, uint32_t B, uint32_t eviction, uint32_t rlt_fallback,
                        uint64_t philox_key, uint8_t* miss_flags, uint64_t* total_misses,
                        const uint32_t* choices, uint32_t* arity, uint32_t max_draws, uint32_t* n_draws);
+
+/* Phase ledger: the flattened block-access sequence of
+ * the complete paths is cut greedily into phases of exactly B distinct blocks (the
+ * last possibly fewer), and the single-cache replay (same arguments as
+ * kvro_single_replay, Philox draws) is counted per phase v:
+ *   ledger[4v+0] distinct blocks of the phase ("new" tokens: first appearance in it)
+ *   ledger[4v+1] misses
+ *   ledger[4v+2] misses at first appearances (misses on "old" tokens = [1] - [2])
+ *   ledger[4v+3] clean tokens: first appearances of blocks that were not in this
+ *                eviction policy's cache at the end of phase v-1 (reading A39)
+ * *n_phases receives the number of phases; returns 3 if it exceeds max_phases. */
+int kvro_phase_ledger(const kvro_trace* tr, uint32_t B, uint32_t eviction, uint32_t rlt_fallback,
+                      uint64_t philox_key, uint32_t* ledger, uint32_t max_phases,
+                      uint32_t* n_phases);
 
 /* exhaustive minimum number of misses over all leaf-eviction choices
  * (SPEC S:246-254); refuses (returns 3) when the instance is too large */

@@ -16,6 +16,8 @@ struct kvr_trace {
   kvr::QueryHdr* hdr;
   uint64_t* hash;
   const uint32_t* nu = nullptr;   // next-use index (offline OPT), borrowed
+  const uint32_t* ph = nullptr;   // phase index (phase ledger), borrowed: ph, nx, distinct
+  uint32_t n_phases = 0, phase_B = 0;
 };
 
 struct kvr_sim {
@@ -42,8 +44,8 @@ kvr_status cuda_fail(cudaError_t e, const char* what) {
 
 // policies that need the extended kernel instantiation
 bool policy_extended(const kvr_policy& p) {
-  return p.eviction == KVR_EVICT_OPT || p.router == KVR_ROUTE_LBGR_RLS || p.tracker_lag != 0 ||
-         p.tracker_grain != 1;
+  return p.eviction == KVR_EVICT_OPT || p.router == KVR_ROUTE_LBGR_RLS ||
+         p.router == KVR_ROUTE_CACHE_AWARE || p.tracker_lag != 0 || p.tracker_grain != 1;
 }
 
 bool sim_extended(const kvr_sim_config& c) {
@@ -55,8 +57,8 @@ bool policy_ok(const kvr_policy& p, std::string* why) {
   auto bad = [&](const char* s) { snprintf(b, sizeof b, "policy: %s", s); *why = b; return false; };
   if (p.eviction > KVR_EVICT_OPT) return bad("eviction must be LRU(0), RLT(1) or OPT(2)");
   if (p.rlt_fallback > KVR_RLT_LRU_MARKED) return bad("rlt_fallback must be 0..2");
-  if (p.router > KVR_ROUTE_LBGR_RLS) return bad("router must be 0..5");
-  if (p.tracker_lag > 1) return bad("tracker_lag must be 0 or 1");
+  if (p.router > KVR_ROUTE_CACHE_AWARE) return bad("router must be 0..6");
+  if (p.tracker_lag > kvr::kMaxLag) return bad("tracker_lag must be in 0..32");
   if (p.tracker_grain < 1) return bad("tracker_grain must be >= 1");
   if (p.router == KVR_ROUTE_LBGR_RLS && !(p.mu > 0.0 && p.mu <= 1.0))
     return bad("LBGR_RLS forgetting factor mu must be in (0, 1]");
@@ -65,7 +67,8 @@ bool policy_ok(const kvr_policy& p, std::string* why) {
   if (!(p.rho > 0.0 && p.rho <= 1.0)) return bad("rho must be in (0, 1]");
   if (!(p.delta_t_ms > 0.0)) return bad("delta_t_ms must be > 0 (inf allowed)");
   const double fin[] = {p.est_alpha_cached_ms, p.est_alpha_miss_ms, p.mu, p.theta0[0], p.theta0[1],
-                        p.theta0[2], p.theta0[3], p.tau, p.w_hit, p.w_load};
+                        p.theta0[2], p.theta0[3], p.tau, p.w_hit, p.w_load,
+                        p.ca_balance_abs, p.ca_balance_rel, p.ca_cache_threshold};
   for (double v : fin)
     if (!std::isfinite(v)) return bad("parameters must be finite");
   if (p.router == KVR_ROUTE_LBGR && !(p.mu >= 0.0 && p.mu < 2.0))
@@ -96,7 +99,7 @@ struct Plan {
   kvr::AuxLayout aux;
   kvr::FifoLayout fifo;
   kvr::BatchLayout blay;
-  size_t ws_aux, ws_fifo, ws_state, ws_total;
+  size_t ws_aux, ws_fifo, ws_lag, ws_state, ws_total;
 };
 
 // continuous batching (kvr_batch.cu): per-worker state in shared memory when W
@@ -124,6 +127,7 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
   pl->ws_aux = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * sizeof(kvr::BFlight));
   pl->ws_fifo = 0;
+  pl->ws_lag = 0;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->blay.bytes : 0;
   pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
   return KVR_OK;
@@ -156,12 +160,14 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t max_N, uint32_
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
-  pl->aux = kvr::make_aux(c.capacity_blocks, max_n);
+  const bool ext = sim_extended(c);
+  pl->aux = kvr::make_aux(c.capacity_blocks, max_n, pl->lay.T, ext);
   pl->ws_aux = (size_t)pl->grid * c.W * pl->aux.bytes;
   pl->fifo = kvr::make_fifo(c.W, c.pending_ring, max_N);
   pl->ws_fifo = (size_t)pl->grid * pl->fifo.bytes;
+  pl->ws_lag = ext ? (size_t)pl->grid * kvr::kLagRing * kvr::lag_entry_bytes(max_n) : 0;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->lay.bytes : 0;
-  pl->ws_total = 256 + pl->ws_aux + pl->ws_fifo + pl->ws_state;
+  pl->ws_total = 256 + pl->ws_aux + pl->ws_fifo + pl->ws_lag + pl->ws_state;
   return KVR_OK;
 }
 
@@ -271,6 +277,40 @@ kvr_status kvr_trace_build_next_use(const kvr_trace* tr, uint32_t* d_nu, size_t 
   return KVR_OK;
 }
 
+kvr_status kvr_trace_phase_bytes(const kvr_trace* tr, size_t* phase_bytes, size_t* scratch_bytes) {
+  if (!tr || !phase_bytes || !scratch_bytes) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  if (tr->total >= 0x7fffffffull) return fail(KVR_ERR_UNSUPPORTED, "phase index needs < 2^31 blocks");
+  *phase_bytes = (size_t)tr->total * 12 + 16;   // ph, nx, distinct (<= one phase per access)
+  cudaError_t e = kvr::phase_scratch_bytes(tr->total, scratch_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "phase scratch size");
+  return KVR_OK;
+}
+
+kvr_status kvr_trace_build_phases(const kvr_trace* tr, uint32_t B, uint32_t* d_phase,
+                                  size_t phase_bytes, void* d_scratch, size_t scratch_bytes,
+                                  void* stream, uint32_t* n_phases, kvr_trace** out) {
+  if (!tr || !out || !n_phases) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  *n_phases = 0;
+  if (B == 0) return fail(KVR_ERR_INVALID_ARG, "B must be >= 1");
+  size_t need_ph = 0, need_scr = 0;
+  kvr_status st = kvr_trace_phase_bytes(tr, &need_ph, &need_scr);
+  if (st) return st;
+  if (tr->total && (!d_phase || !d_scratch)) return fail(KVR_ERR_INVALID_ARG, "null phase/scratch buffer");
+  if (phase_bytes < need_ph || scratch_bytes < need_scr)
+    return fail(KVR_ERR_WORKSPACE_TOO_SMALL, "phase buffers too small (%zu/%zu < %zu/%zu)", phase_bytes,
+                scratch_bytes, need_ph, need_scr);
+  cudaError_t e = kvr::build_phases(tr->hash, tr->total, B, d_phase, d_scratch, scratch_bytes,
+                                    (cudaStream_t)stream, n_phases);
+  if (e != cudaSuccess) return cuda_fail(e, "phase index");
+  kvr_trace* t = new kvr_trace(*tr);
+  t->ph = d_phase;
+  t->n_phases = *n_phases;
+  t->phase_B = B;
+  *out = t;
+  return KVR_OK;
+}
+
 kvr_status kvr_trace_collision_bytes(const kvr_trace* tr, size_t* scratch_bytes) {
   if (!tr || !scratch_bytes) return fail(KVR_ERR_INVALID_ARG, "null argument");
   if (tr->total >= 0x7fffffffull) return fail(KVR_ERR_UNSUPPORTED, "collision check needs < 2^31 blocks");
@@ -322,8 +362,6 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
     return fail(KVR_ERR_INVALID_ARG, "service model must be finite");
   std::string why;
   if (!policy_ok(cfg->default_policy, &why)) return fail(KVR_ERR_INVALID_ARG, "%s", why.c_str());
-  if (cfg->default_policy.tracker_lag && cfg->capacity_blocks > 1024)
-    return fail(KVR_ERR_UNSUPPORTED, "policy: tracker_lag needs capacity_blocks <= 1024");
   if (cfg->default_policy.eviction == KVR_EVICT_OPT && cfg->W != 1)
     return fail(KVR_ERR_INVALID_ARG, "policy: OPT (offline Belady) is defined for W = 1");
   if (cfg->batch_slots > 64) return fail(KVR_ERR_INVALID_ARG, "batch_slots must be in 0..64");
@@ -377,12 +415,14 @@ kvr_status kvr_sim_workspace_bytes(const kvr_sim* sim, const kvr_trace* trace, u
   return kvr_sim_workspace_bytes_multi(sim, 1, &trace, n_trials, bytes);
 }
 
-kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* traces,
-                             const uint32_t* d_trial_trace, uint32_t n_trials,
-                             const uint64_t* d_keys, const kvr_policy* d_policies,
-                             kvr_trial_result* d_results, uint32_t* d_hist,
-                             kvr_query_record* d_records, uint64_t* d_victims, uint64_t victims_cap,
-                             void* d_ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+kvr_status run_impl(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* traces,
+                    const uint32_t* d_trial_trace, uint32_t n_trials, const uint64_t* d_keys,
+                    const kvr_policy* d_policies, kvr_trial_result* d_results, uint32_t* d_hist,
+                    kvr_query_record* d_records, uint64_t* d_victims, uint64_t victims_cap,
+                    void* d_ws, size_t ws_bytes, void* stream, uint32_t* d_ledger) {
   if (!sim || !traces) return fail(KVR_ERR_INVALID_ARG, "null argument");
   if (n_traces == 0 || n_traces > kvr::kMaxTraces)
     return fail(KVR_ERR_UNSUPPORTED, "n_traces must be in 1..%u", kvr::kMaxTraces);
@@ -409,7 +449,7 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
     if (!d_policies && c.default_policy.eviction == KVR_EVICT_OPT && !t->nu && t->total)
       return fail(KVR_ERR_INVALID_ARG, "OPT needs a next-use index (kvr_trace_build_next_use) on trace %u", i);
   }
-  const uint32_t R = std::min(c.record_trials, n_trials);
+  const uint32_t R = d_ledger ? 0u : std::min(c.record_trials, n_trials);   // ledger runs record nothing
   if (R && !d_records) return fail(KVR_ERR_INVALID_ARG, "record_trials > 0 needs d_records");
   Plan pl;
   kvr_status st = make_plan(sim, max_n, max_N, n_trials, &pl);
@@ -426,6 +466,12 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
     p.traces[i].N = traces[i]->N;
     p.traces[i].max_n = traces[i]->max_n;
     p.traces[i].block_tokens = traces[i]->block_tokens;
+    if (traces[i]->ph) {
+      p.traces[i].ph = traces[i]->ph;
+      p.traces[i].nx = traces[i]->ph + traces[i]->total;
+      p.traces[i].distinct = traces[i]->ph + 2 * traces[i]->total;
+      p.traces[i].n_phases = traces[i]->n_phases;
+    }
   }
   p.trial_trace = n_traces > 1 ? d_trial_trace : nullptr;
   p.n_traces = n_traces;
@@ -455,7 +501,13 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   p.work_counter = (unsigned int*)ws;
   p.aux_base = ws + 256;
   p.fifo_base = ws + 256 + pl.ws_aux;
-  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux + pl.ws_fifo : nullptr;
+  p.lag_base = pl.ws_lag ? ws + 256 + pl.ws_aux + pl.ws_fifo : nullptr;
+  p.lag_entry = (uint32_t)kvr::lag_entry_bytes(max_n);
+  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux + pl.ws_fifo + pl.ws_lag : nullptr;
+  if (d_ledger) {
+    p.ledger = d_ledger;
+    p.ledger_stride = 4 * traces[0]->n_phases;
+  }
 
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, s);
@@ -473,6 +525,38 @@ kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* c
   if (e != cudaSuccess) return cuda_fail(e, "replay launch");
   return KVR_OK;
 }
+}  // namespace
+
+extern "C" {
+
+kvr_status kvr_sim_run_multi(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* traces,
+                             const uint32_t* d_trial_trace, uint32_t n_trials,
+                             const uint64_t* d_keys, const kvr_policy* d_policies,
+                             kvr_trial_result* d_results, uint32_t* d_hist,
+                             kvr_query_record* d_records, uint64_t* d_victims, uint64_t victims_cap,
+                             void* d_ws, size_t ws_bytes, void* stream) {
+  return run_impl(sim, n_traces, traces, d_trial_trace, n_trials, d_keys, d_policies, d_results,
+                  d_hist, d_records, d_victims, victims_cap, d_ws, ws_bytes, stream, nullptr);
+}
+
+kvr_status kvr_sim_run_ledger(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
+                              const uint64_t* d_keys, const kvr_policy* d_policies,
+                              kvr_trial_result* d_results, uint32_t* d_ledger, void* d_ws,
+                              size_t ws_bytes, void* stream) {
+  if (!sim || !trace) return fail(KVR_ERR_INVALID_ARG, "null argument");
+  if (sim->cfg.W != 1) return fail(KVR_ERR_INVALID_ARG, "phase ledger: W must be 1 (single-cache analysis)");
+  if (sim->cfg.batch_slots) return fail(KVR_ERR_INVALID_ARG, "phase ledger: beta = 1 model only");
+  if (!sim_extended(sim->cfg))
+    return fail(KVR_ERR_INVALID_ARG, "phase ledger: create the sim with extended_policies = 1");
+  if (!trace->ph) return fail(KVR_ERR_INVALID_ARG, "phase ledger: trace has no phase index");
+  if (trace->phase_B != sim->cfg.capacity_blocks)
+    return fail(KVR_ERR_INVALID_ARG, "phase ledger: phases built for B=%u, sim has B=%u", trace->phase_B,
+                sim->cfg.capacity_blocks);
+  if (n_trials && trace->n_phases && !d_ledger) return fail(KVR_ERR_INVALID_ARG, "null ledger");
+  return run_impl(sim, 1, &trace, nullptr, n_trials, d_keys, d_policies, d_results, nullptr,
+                  nullptr, nullptr, 0, d_ws, ws_bytes, stream, d_ledger ? d_ledger : nullptr);
+}
+
 
 kvr_status kvr_sim_run(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
                        const uint64_t* d_keys, const kvr_policy* d_policies,

@@ -170,6 +170,7 @@ struct __align__(16) BCtrl {
   double score[2][kMaxW];
   uint32_t mhit[2][kMaxW];
   uint32_t pend[2][kMaxW];
+  uint32_t csize[2][kMaxW];   // cached blocks (CACHE_AWARE router, A38)
   uint32_t abortf[2];
   uint32_t trial, status;
   kvr_policy pol;
@@ -804,6 +805,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
         ctrl->score[par][w] = sc;
         ctrl->mhit[par][w] = m;
         ctrl->pend[par][w] = pend;
+        ctrl->csize[par][w] = x.size;
       }
       __syncthreads();
       if (ctrl->abortf[par]) {
@@ -830,6 +832,24 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
         } else {
           for (uint32_t i = 1; i < W; ++i)
             if (ctrl->mhit[par][i] > ctrl->mhit[par][best]) best = i;
+        }
+      } else if (router == KVR_ROUTE_CACHE_AWARE) {   // A38 on pending = waiting + in flight
+        uint32_t mx = ctrl->pend[par][0], mn = mx;
+        for (uint32_t i = 1; i < W; ++i) {
+          mx = max(mx, ctrl->pend[par][i]);
+          mn = min(mn, ctrl->pend[par][i]);
+        }
+        if (((double)(mx - mn) > pol.ca_balance_abs) && ((double)mx > pol.ca_balance_rel * (double)mn)) {
+          for (uint32_t i = 1; i < W; ++i)
+            if (ctrl->pend[par][i] < ctrl->pend[par][best]) best = i;
+        } else {
+          for (uint32_t i = 1; i < W; ++i)
+            if (ctrl->mhit[par][i] > ctrl->mhit[par][best]) best = i;
+          if (!((double)(T.bt * ctrl->mhit[par][best]) / (double)q > pol.ca_cache_threshold)) {
+            best = 0;
+            for (uint32_t i = 1; i < W; ++i)
+              if (ctrl->csize[par][i] < ctrl->csize[par][best]) best = i;
+          }
         }
       } else if (router == KVR_ROUTE_ROUND_ROBIN) {
         best = j % W;

@@ -17,6 +17,8 @@ constexpr uint32_t kFifoRecBytes = 64;  // one pending completion {c,a,E^,phi0..
 constexpr uint32_t kFifoChunk = 32;     // records per chunk of a CTA's pending-FIFO pool
 constexpr uint32_t kMaxHistBins = 256;
 constexpr uint32_t kMaxW = 32;
+constexpr uint32_t kMaxLag = KVR_MAX_TRACKER_LAG;   // stale-tracker lag k (A29)
+constexpr uint32_t kLagRing = kMaxLag + 2;          // per-CTA ring of the last updates
 
 // Packed trace, per query: a 32-byte header, bulk-copied with the query's hashes.
 struct __align__(16) QueryHdr {
@@ -30,7 +32,10 @@ struct TraceDev {
   const QueryHdr* hdr;  // [N]
   const uint64_t* hash; // [total] chained identities, CSR order
   const uint32_t* nu;   // [total] next-use index (offline OPT) or null
-  uint32_t N, max_n, block_tokens, _pad;
+  const uint32_t* ph;   // [total] phase | first-appearance bit (phase ledger) or null
+  const uint32_t* nx;   // [total] next occurrence of the identity (phase ledger)
+  const uint32_t* distinct;   // [n_phases] distinct identities per phase
+  uint32_t N, max_n, block_tokens, n_phases;
 };
 
 // packed buffer = [QueryHdr x N][pad to 16][u64 hash x total]
@@ -46,12 +51,13 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(siz
 __host__ __device__ inline bool policy_valid(const kvr_policy& p) {
   auto fin = [](double v) { return (v - v) == 0.0; };
   if (p.eviction > KVR_EVICT_OPT || p.rlt_fallback > KVR_RLT_LRU_MARKED ||
-      p.router > KVR_ROUTE_LBGR_RLS || p.tracker_lag > 1 || p.tracker_grain < 1)
+      p.router > KVR_ROUTE_CACHE_AWARE || p.tracker_lag > kMaxLag || p.tracker_grain < 1)
     return false;
   if (!(p.rho > 0.0 && p.rho <= 1.0) || !(p.delta_t_ms > 0.0)) return false;
   if (!fin(p.est_alpha_cached_ms) || !fin(p.est_alpha_miss_ms) || !fin(p.mu) ||
       !fin(p.theta0[0]) || !fin(p.theta0[1]) || !fin(p.theta0[2]) || !fin(p.theta0[3]) ||
-      !fin(p.tau) || !fin(p.w_hit) || !fin(p.w_load))
+      !fin(p.tau) || !fin(p.w_hit) || !fin(p.w_load) || !fin(p.ca_balance_abs) ||
+      !fin(p.ca_balance_rel) || !fin(p.ca_cache_threshold))
     return false;
   if (p.router == KVR_ROUTE_LBGR && !(p.mu >= 0.0 && p.mu < 2.0)) return false;
   if (p.router == KVR_ROUTE_LBGR_RLS &&
@@ -92,25 +98,41 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
 
 // Per-worker auxiliary state in global memory (L2-resident): the Leaf-LRU recency
 // log (append-only ring of (stamp, slot), compacted when full; validated by the
-// per-slot stamps of the worker state) and the LBGR_RLS matrix.
+// per-slot stamps of the worker state), the LBGR_RLS matrix, and for the extended
+// policies the stale tracker's mirror of the worker's cache (identity per slot and a
+// table identity -> slot, reading A29) and the per-slot last access (phase ledger).
 struct AuxLayout {
-  uint32_t log_cap;
-  size_t off_log, off_rls, bytes;   // rls: LBGR_RLS P (4x4, fp64)
+  uint32_t log_cap, T;
+  size_t off_log, off_rls, off_mkey, off_mtab, off_last, bytes;
 };
 
-inline AuxLayout make_aux(uint32_t B, uint32_t max_n) {
+inline AuxLayout make_aux(uint32_t B, uint32_t max_n, uint32_t T, bool ext) {
   AuxLayout A{};
   // live entries after a compaction <= B; 4x headroom keeps the amortised compaction
   // cost at ~1.25 entries read per entry appended and the log L2-resident
   uint32_t C = 64;
   while (C < 4 * (B + max_n + 32)) C <<= 1;
   A.log_cap = C;
+  A.T = T;
   size_t o = 0;
   A.off_log = o;   o = align16(o + (size_t)C * 8);
   A.off_rls = o;   o = align16(o + 16 * 8);
+  A.off_mkey = o;  o = align16(o + (ext ? (size_t)B * 8 : 0));
+  A.off_mtab = o;  o = align16(o + (ext ? (size_t)T * 4 : 0));
+  A.off_last = o;  o = align16(o + (ext ? (size_t)B * 4 : 0));
   A.bytes = (o + 127) & ~(size_t)127;
   return A;
 }
+
+// Per-CTA ring of the last kLagRing cache updates of the trial (stale tracker, A29):
+// entry = header, then the update's per-miss slots (slot | evicted << 31).
+struct __align__(16) LagHdr {
+  uint64_t block_off;     // the query's first identity in the trace
+  uint32_t j, worker, kf, M;
+  uint32_t _pad[2];
+};
+static_assert(sizeof(LagHdr) == 32, "lag header is 32 B");
+inline size_t lag_entry_bytes(uint32_t max_n) { return align16(sizeof(LagHdr) + 4 * (size_t)max_n); }
 
 // Pending-completion FIFOs of one CTA's trial: every worker's FIFO is a linked list
 // of 32-record chunks from one per-CTA pool (link words, then the chunks).  Chunks a
@@ -139,6 +161,7 @@ struct __align__(16) Ctrl {
   double score[2][kMaxW];
   uint32_t mhit[2][kMaxW];
   uint32_t npend[2][kMaxW];
+  uint32_t csize[2][kMaxW];    // cached blocks per worker (CACHE_AWARE router, A38)
   double P[kMaxW], F[kMaxW];
   double sum_lat, sum_ttft, max_lat;
   unsigned long long digest, dkey, vcursor;
@@ -146,6 +169,9 @@ struct __align__(16) Ctrl {
   kvr_policy pol;                      // this trial's policy
   uint32_t trial, status, abortf[2];   // abort flag double-buffered by query parity
   uint32_t fifo_bump, _pad_f[3];       // next never-used chunk of the CTA's FIFO pool
+  uint32_t* led;                       // phase ledger of this trial (extended policies) or null
+  const uint32_t* lph;                 // its trace's phase index (ph, nx)
+  const uint32_t* lnx;
   uint32_t hist[kMaxHistBins];
 };
 
@@ -169,7 +195,8 @@ struct __align__(16) WarpSm {
   uint32_t c_q, c_maxp;
   uint32_t ftail, ffree;           // FIFO: next record index to write; free-chunk list head
   WorkerRegs x;                    // RLT decision state in/out, e_i and counters
-  uint32_t x_ri, _pad2[3];         // next unused draw of x_rbuf
+  uint32_t x_ri;                   // next unused draw of x_rbuf
+  uint32_t m_used, m_size, m_cur;  // stale-tracker mirror: table fill, slots, next ring entry
   unsigned long long x_rbuf[32];   // RLT: 32 counter-based draws, one per lane
   uint32_t slot[4];                // [max_n] slots | [max_n] victims | [32] bitmap
 };
@@ -235,6 +262,9 @@ struct ReplayParams {
   AuxLayout aux;
   FifoLayout fifo;
   uint8_t* fifo_base;            // [grid][fifo.bytes] pending-FIFO pools (beta = 1 engine)
+  uint8_t* lag_base;             // [grid][kLagRing][lag_entry] update rings (extended policies)
+  uint32_t lag_entry, ledger_stride;   // bytes per ring entry; u32 per trial of the ledger
+  uint32_t* ledger;              // phase ledger [n_trials][ledger_stride] or null
   kvr_service_model truth;
   kvr_policy defpol;
   const kvr_policy* policies;
@@ -282,6 +312,10 @@ cudaError_t collision_scratch_bytes(uint64_t n_blocks, size_t* bytes);
 cudaError_t count_collisions(const QueryHdr* hdr, uint32_t N, const uint64_t* hash,
                              const uint64_t* block_keys, uint64_t n, void* scratch,
                              size_t scratch_bytes, cudaStream_t s, unsigned long long* h_count);
+// phase index of the phase ledger (kvr_nextuse.cu): out = [n] ph | [n] nx | [<= n] distinct
+cudaError_t phase_scratch_bytes(uint64_t n_blocks, size_t* bytes);
+cudaError_t build_phases(const uint64_t* hash, uint64_t n, uint32_t B, uint32_t* out, void* scratch,
+                         size_t scratch_bytes, cudaStream_t s, uint32_t* h_n_phases);
 // phase profiler (profiling build, -DKVR_PHASE_PROFILE); cudaErrorNotSupported otherwise
 cudaError_t phase_cycles(unsigned long long* out16, int reset);
 

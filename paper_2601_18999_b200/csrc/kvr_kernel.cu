@@ -896,10 +896,78 @@ __device__ __noinline__ void opt_decide(const ReplayParams& p_, uint32_t M, uint
   __syncwarp();
 }
 
+// ---------------------------------------------- stale global tracker (reading A29)
+// The router's view of worker i under a lag of k events is the worker's cache as it
+// was after query j-1-k: a mirror (identity per slot + table identity -> slot, in the
+// worker's aux region) that replays the worker's own updates k queries late from
+// the per-CTA ring of the trial's last kLagRing updates (header + per-miss slots).
+template <typename Idx>
+__device__ __forceinline__ WorkerView<Idx> mirror_view(const ReplayParams& p, uint32_t w) {
+  uint8_t* a = p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes;
+  WorkerView<Idx> v{};
+  v.key = reinterpret_cast<uint64_t*>(a + p.aux.off_mkey);
+  v.table = reinterpret_cast<Idx*>(a + p.aux.off_mtab);
+  return v;
+}
+__device__ __forceinline__ LagHdr* lag_entry(const ReplayParams& p, uint32_t j) {
+  return reinterpret_cast<LagHdr*>(p.lag_base +
+                                   ((size_t)blockIdx.x * kLagRing + j % kLagRing) * p.lag_entry);
+}
+__device__ __forceinline__ uint32_t* last_access(const ReplayParams& p, uint32_t w) {
+  return reinterpret_cast<uint32_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
+                                     p.aux.off_last);
+}
+
+// apply ring entry jj (an update of this warp's worker) to the worker's mirror: the
+// same table deletes / slot overwrites / inserts as apply_update, nothing else
+template <typename Idx, int kTag>
+__device__ __noinline__ void mirror_apply(const ReplayParams& p, const uint64_t* hash, uint32_t w,
+                                          uint32_t lane, uint32_t jj) {
+  const LagHdr* e = lag_entry(p, jj);
+  const uint32_t M = e->M, kf = e->kf;
+  const uint64_t off = e->block_off;
+  const uint32_t* sl = reinterpret_cast<const uint32_t*>(e + 1);
+  const WorkerView<Idx> V = mirror_view<Idx>(p, w);
+  const uint32_t tmask = p.lay.T - 1;
+  WarpSm* ws = warp_sm(p, w);
+  uint32_t add = 0, sub = 0, fresh = 0;
+#pragma unroll 1
+  for (uint32_t cb = 0; cb < M; cb += 32) {
+    const uint32_t q = cb + lane;
+    const bool act = q < M;
+    const uint32_t sv = act ? sl[q] : 0u;
+    const uint32_t slot = sv & 0x7fffffffu;
+    const bool ev = (sv >> 31) != 0;
+    const uint64_t t = act ? hash[off + kf + q] : 0ull;
+    uint32_t cleared = 0;
+    if (act && ev) cleared = tbl_erase<Idx>(V, tmask, V.key[slot], (Idx)slot);
+    __syncwarp();
+    if (act) V.key[slot] = t;
+    __syncwarp();
+    const uint32_t claimed = act ? tbl_insert<Idx>(V, tmask, t, (Idx)slot) : 0u;
+    add += __popc(__ballot_sync(kFull, claimed != 0));
+    sub += __popc(__ballot_sync(kFull, cleared != 0));
+    fresh += __popc(__ballot_sync(kFull, act && !ev));
+    __syncwarp();
+  }
+  uint32_t used = ws->m_used + add - sub;
+  const uint32_t size = ws->m_size + fresh;
+  if (used > (p.lay.T >> 1)) {
+    tbl_rebuild<Idx>(V, p.lay.T, size, lane);
+    used = size;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    ws->m_used = used;
+    ws->m_size = size;
+  }
+  __syncwarp();
+}
+
 // Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
 // victim digest term and the query record (trial sums are added in query order
 // by the accounting step).
-template <typename Idx, bool kGlobal, int kTag>
+template <typename Idx, bool kGlobal, int kTag, bool kExt>
 __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, uint32_t w, bool tree,
                                           bool use_list, bool lbgr_or_static, kvr_query_record* rec,
                                           uint64_t* vlog) {
@@ -915,7 +983,13 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   R.cap_mask = p.aux.log_cap - 1;
   const uint32_t tmask = p.lay.T - 1;
   const uint64_t* H = reinterpret_cast<const uint64_t*>(stage + (size_t)ws->buf * p.stage_bytes + 32);
-  H += (reinterpret_cast<const QueryHdr*>(stage + (size_t)ws->buf * p.stage_bytes)->block_off & 1);
+  const uint64_t boff = reinterpret_cast<const QueryHdr*>(stage + (size_t)ws->buf * p.stage_bytes)->block_off;
+  H += (boff & 1);
+  // phase ledger of this trial (extended instantiation only; pointers in the control block)
+  uint32_t* led = kExt ? ctrl->led : nullptr;
+  const uint32_t* ph = kExt ? ctrl->lph : nullptr;
+  const uint32_t* nx = kExt ? ctrl->lnx : nullptr;
+  uint32_t* lastacc = led ? last_access(p, w) : nullptr;
   const uint32_t n = ws->n, kf = ws->kf, M = ws->M, nev = ws->nev, wq = ws->wq, ltail0 = ws->ltail0;
   const uint32_t nfree = M - nev;
   const uint64_t vc = ws->vc;
@@ -932,6 +1006,22 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     const bool my_ev = (sv >> 31) != 0;
     const uint64_t t = act ? H[kf + qq] : 0ull;
     uint32_t cleared = 0;
+    if (led && act) {
+      // phase ledger (A39): this miss, and whether the victim was cached when
+      // this phase began and is first requested again in it (not clean then)
+      const uint64_t o = boff + kf + qq;
+      const uint32_t pw = ph[o], v = pw & 0x7fffffffu;
+      atomicAdd(&led[4 * v + 1], 1u);
+      if (pw >> 31) atomicAdd(&led[4 * v + 2], 1u);
+      if (my_ev) {
+        const uint32_t nxo = nx[lastacc[my_slot]];
+        if (nxo != 0xFFFFFFFFu) {
+          const uint32_t pn = ph[nxo];
+          if ((pn >> 31) && (pn & 0x7fffffffu) == v) atomicAdd(&led[4 * v + 3], 1u);
+        }
+      }
+      lastacc[my_slot] = (uint32_t)o;
+    }
     if (act && my_ev) {
       const uint64_t vkey = S.key[my_slot];
       cleared = tbl_erase<Idx>(S, tmask, vkey, (Idx)my_slot);
@@ -1081,6 +1171,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     uint64_t* vlog = (recorded && p.victims) ? p.victims + (size_t)trial * p.victims_per_trial : nullptr;
     // deferred apply needs the overlay (register victim bitmap): B <= 1024
     const bool defer = regbits;
+    const uint32_t lag = kExt ? pol.tracker_lag : 0u;   // stale tracker (A29): k events
+    uint32_t* led = (kExt && p.ledger) ? p.ledger + (size_t)trial * p.ledger_stride : nullptr;
 
 #ifdef KVR_PHASE_PROFILE
     const unsigned long long t_trial0 = clock64();
@@ -1093,6 +1185,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     }
     if (use_list)
       for (uint32_t i = lane; i < B; i += 32) R.stamp[i] = 0;
+    if (lag) {   // the tracker's mirror starts empty too
+      const WorkerView<Idx> MV = mirror_view<Idx>(p, w);
+      for (uint32_t i = lane; i < L.T; i += 32) MV.table[i] = NIL;
+    }
+    if (led)
+      for (uint32_t i = tid; i < p.ledger_stride; i += blockDim.x) led[i] = 0u;
     // The worker's scalar cache state (size, |T|, log cursors, e_i, counters) lives in
     // its shared-memory block ws->x; the chosen warp works on a register copy for
     // the duration of its update (nothing of it stays live across the query loop).
@@ -1102,6 +1200,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       w0.c_ins = 0; w0.c_evict = 0; w0.c_draws = 0; w0.c_resets = 0; w0.c_fb = 0;
       ws->x = w0;
       ws->x_ri = 32;   // next unused draw of the batch (none yet)
+      ws->m_used = 0;
+      ws->m_size = 0;
+      ws->m_cur = 0;
     }
     uint32_t fh = 0, fn = 0;
     double P = 0.0, F = 0.0, Pt = 0.0;
@@ -1130,6 +1231,11 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       ctrl->status = 0;
       ctrl->fifo_bump = 0;
       for (int c = 0; c < 10; ++c) ctrl->cnt[c] = 0;
+      if (kExt) {
+        ctrl->led = led;
+        ctrl->lph = tr.ph;
+        ctrl->lnx = tr.nx;
+      }
     }
     for (uint32_t b = tid; b < p.bins; b += blockDim.x) ctrl->hist[b] = 0;
     // (bt*k)/1000.0 computed once per trial with the same IEEE division (A9)
@@ -1138,7 +1244,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // a per-trial policy from device memory is validated here (host validated the default)
     const bool pol_ok = policy_valid(pol) &&
                         (!opt || (W == 1 && (tr.nu != nullptr || N == 0))) &&
-                        (!pol.tracker_lag || defer) &&
+                        (kExt ? (!p.ledger || (W == 1 && tr.ph != nullptr)) : p.ledger == nullptr) &&
                         (kExt || (pol.eviction <= KVR_EVICT_RLT && pol.router <= KVR_ROUTE_RANDOM &&
                                   pol.tracker_lag == 0 && pol.tracker_grain == 1));
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
@@ -1298,14 +1404,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       KVR_ACC(1, tl);
 
-      // 2. longest cached prefix over the input (ballot of 32 probes).  With the
-      // tracker lag (App. E, reading A29) a second pass over the old table alone
-      // (before this worker's pending update) gives the router's view.
-      uint32_t mm = 0, mv = 0;
-#pragma unroll 1
-      for (uint32_t pass = 0; pass < 2; ++pass) {
-        const bool ovl = pass == 0 && minus_victims;
-        const uint32_t npp = pass == 0 ? np : 0u;
+      // 2. longest cached prefix over the input (ballot of 32 probes) on the worker's
+      // cache, and with the stale tracker (App. E, reading A29) the router's view: the
+      // same match on the mirror of the cache after query j-1-k
+      auto match_on = [&](const WorkerView<Idx> V, bool ovl, uint32_t npp) -> uint32_t {
         uint32_t mx = 0;
 #pragma unroll 1
         for (uint32_t base = 0; base < nq_in; base += 32) {
@@ -1317,7 +1419,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             if (d < npp && Hp[d] == hh) {
               hit = true;
             } else {
-              const Idx s = tbl_find<Idx>(S, tmask, hh);
+              const Idx s = tbl_find<Idx>(V, tmask, hh);
               hit = s != NIL;
               check = ovl && hit;
               sidx = (uint32_t)s;
@@ -1335,15 +1437,11 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           mx = base + (__ffs(~bal) - 1);
           break;
         }
-        if (mx > nq_in) mx = nq_in;
-        if (pass == 1) {
-          mv = mx;
-          break;
-        }
-        mm = mx;
-        mv = mx;
-        if (!(kExt && pol.tracker_lag && minus_victims)) break;
-      }
+        return mx > nq_in ? nq_in : mx;
+      };
+      const uint32_t mm = match_on(S, minus_victims, np);
+      uint32_t mv = mm;
+      if (kExt && lag) mv = match_on(mirror_view<Idx>(p, w), false, 0u);
       if (kExt && pol.tracker_grain > 1) mv = pol.tracker_grain * (mv / pol.tracker_grain);
       KVR_ACC(2, tl);
 
@@ -1400,6 +1498,17 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
              (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
         np = ws->n;
       }
+      if (kExt && lag && j >= lag) {
+        // the tracker catches up to the caches after query j-1-k: this worker's updates
+        // of queries < j-k, in query order (ring entries live kLagRing > k+1 queries)
+        const uint32_t upto = j - lag;
+        uint32_t cur = ws->m_cur;
+#pragma unroll 1
+        for (; cur < upto; ++cur)
+          if (lag_entry(p, cur)->worker == w) mirror_apply<Idx, kMaxThreads>(p, tr.hash, w, lane, cur);
+        __syncwarp();
+        if (lane == 0) ws->m_cur = cur;
+      }
       uint32_t m, mview;
       double score, Chat, f0, f1, f2;
       score_query(H, a, n_in, q, Hp, np, overlay, m, mview, score, Chat, f0, f1, f2);
@@ -1407,6 +1516,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ctrl->score[par][w] = score;
         ctrl->mhit[par][w] = mview;   // the router's view (THRESHOLD)
         ctrl->npend[par][w] = fn;
+        ctrl->csize[par][w] = ws->x.size;   // cached blocks (CACHE_AWARE, A38)
         ws->c_probes += min(m + 1, n_in);
       }
       KVR_RESET(tp);
@@ -1459,6 +1569,22 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           const uint32_t mmax = __reduce_max_sync(kFull, mh);
           best = __ffs(__ballot_sync(kFull, lane < W && mh == mmax)) - 1;
         }
+      } else if (kExt && router == KVR_ROUTE_CACHE_AWARE) {   // A38
+        const uint32_t npd = lane < W ? ctrl->npend[par][lane] : 0u;
+        const uint32_t mx = __reduce_max_sync(kFull, npd);
+        const uint32_t mn = __reduce_min_sync(kFull, lane < W ? npd : 0xffffffffu);
+        if (((double)(mx - mn) > pol.ca_balance_abs) && ((double)mx > pol.ca_balance_rel * (double)mn)) {
+          best = __ffs(__ballot_sync(kFull, lane < W && npd == mn)) - 1;
+        } else {
+          const uint32_t mh = lane < W ? ctrl->mhit[par][lane] : 0u;
+          const uint32_t mmax = __reduce_max_sync(kFull, mh);
+          best = __ffs(__ballot_sync(kFull, lane < W && mh == mmax)) - 1;
+          if (!((double)(bt * mmax) / (double)q > pol.ca_cache_threshold)) {
+            const uint32_t cs = lane < W ? ctrl->csize[par][lane] : 0xffffffffu;
+            const uint32_t cmin = __reduce_min_sync(kFull, cs);
+            best = __ffs(__ballot_sync(kFull, lane < W && cs == cmin)) - 1;
+          }
+        }
       } else if (router == KVR_ROUTE_ROUND_ROBIN) {
         best = j % W;
       } else {
@@ -1468,7 +1594,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 
       // deferred apply of this warp's previous update (overlaps others' decisions)
       if (ws->active) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
 #ifdef KVR_PHASE_PROFILE
@@ -1569,6 +1695,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           R.log[(ltail0 + (n - 1 - d)) & R.cap_mask] = ((uint64_t)wr.wq << 32) | (uint32_t)s;
         }
         if (opt && act) opt_keys(p, w)[s] = opt_key(tr.nu[hd.block_off + d], d + 1, (uint32_t)s);
+        if (led && act) last_access(p, w)[s] = (uint32_t)(hd.block_off + d);   // phase ledger
         if (rlt) {
           const bool um = act && !((S.mark[(uint32_t)s >> 5] >> ((uint32_t)s & 31)) & 1u);
           const uint32_t u = __ballot_sync(kFull, um);
@@ -1742,6 +1869,18 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       if (lane == 0) ws->x.c_ins += M;
       __syncwarp();
+      if (kExt && lag) {   // this update, for the trackers of the next queries (A29)
+        LagHdr* le = lag_entry(p, j);
+        uint32_t* lsl = reinterpret_cast<uint32_t*>(le + 1);
+        for (uint32_t qq = lane; qq < M; qq += 32) lsl[qq] = slots[qq];
+        if (lane == 0) {
+          le->block_off = hd.block_off;
+          le->j = j;
+          le->worker = w;
+          le->kf = kf;
+          le->M = M;
+        }
+      }
       KVR_ACC(8, tp);
 
       if (defer) {   // overlay bitmap of this update's victims -> registers
@@ -1766,7 +1905,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       __syncwarp();
       if (!defer) {
-        apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
     }
@@ -1774,7 +1913,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // ---- end of trial ----
     __syncthreads();   // all warps are past their last query before the final applies
     if (ws->active) {
-      apply_update<Idx, kGlobal, kMaxThreads>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+      apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
       vbits = 0;
     }
     __syncthreads();
@@ -1834,6 +1973,13 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     if (p.hist)
       for (uint32_t b = tid; b < p.bins; b += blockDim.x)
         p.hist[(size_t)trial * p.bins + b] = ctrl->hist[b];
+    if (led && Nrun) {   // distinct per phase; clean = first-appearance misses - not clean
+      __threadfence_block();
+      for (uint32_t v = tid; v < tr.n_phases; v += blockDim.x) {
+        led[4 * v] = tr.distinct[v];
+        led[4 * v + 3] = led[4 * v + 2] - led[4 * v + 3];
+      }
+    }
     __syncthreads();
   }
 }

@@ -25,6 +25,9 @@ EVICT_LRU, EVICT_RLT, EVICT_OPT = 0, 1, 2   # OPT: offline Belady, W = 1 (needs 
 RLT_EARLY_RESET, RLT_UNIFORM_LEAF, RLT_LRU_MARKED = 0, 1, 2
 ROUTE_LBGR, ROUTE_STATIC_LINEAR, ROUTE_THRESHOLD, ROUTE_ROUND_ROBIN, ROUTE_RANDOM = 0, 1, 2, 3, 4
 ROUTE_LBGR_RLS = 5   # LBGR, RLS reading of the 0.992 update (A8b)
+ROUTE_CACHE_AWARE = 6   # SGLang-style cache-aware rule (A38)
+MAX_TRACKER_LAG = 32
+LEDGER_FIELDS = ("distinct", "misses", "first_misses", "clean")
 TRIAL_OK, TRIAL_RING_OVERFLOW, TRIAL_VICTIM_LOG_FULL, TRIAL_BAD_POLICY = 0, 1, 2, 3
 TRIAL_ADMISSION, TRIAL_BAD_TRACE = 4, 5
 ERR_HASH_COLLISION = 4
@@ -35,7 +38,8 @@ EXPORTS = ("kvr_last_error", "kvr_abi_version", "kvr_build_id", "kvr_trace_packe
            "kvr_trace_next_use_bytes", "kvr_trace_build_next_use", "kvr_trace_collision_bytes",
            "kvr_trace_check_collisions", "kvr_sim_create",
            "kvr_sim_destroy", "kvr_sim_plan", "kvr_sim_workspace_bytes",
-           "kvr_sim_workspace_bytes_multi", "kvr_sim_run", "kvr_sim_run_multi")
+           "kvr_sim_workspace_bytes_multi", "kvr_sim_run", "kvr_sim_run_multi",
+           "kvr_trace_phase_bytes", "kvr_trace_build_phases", "kvr_sim_run_ledger")
 
 
 class KvrError(RuntimeError):
@@ -64,7 +68,9 @@ class kvr_policy(C.Structure):
                 ("rho", C.c_double), ("delta_t_ms", C.c_double), ("mu", C.c_double),
                 ("theta0", C.c_double * 4), ("tau", C.c_double),
                 ("w_hit", C.c_double), ("w_load", C.c_double), ("rls_p0", C.c_double),
-                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32)]
+                ("tracker_lag", C.c_uint32), ("tracker_grain", C.c_uint32),
+                ("ca_balance_abs", C.c_double), ("ca_balance_rel", C.c_double),
+                ("ca_cache_threshold", C.c_double), ("_pad2", C.c_uint64)]
 
 
 class kvr_sim_config(C.Structure):
@@ -80,7 +86,9 @@ POLICY_DTYPE = np.dtype([("eviction", "<u4"), ("rlt_fallback", "<u4"), ("router"
                          ("est_alpha_miss_ms", "<f8"), ("rho", "<f8"), ("delta_t_ms", "<f8"),
                          ("mu", "<f8"), ("theta0", "<f8", (4,)), ("tau", "<f8"),
                          ("w_hit", "<f8"), ("w_load", "<f8"), ("rls_p0", "<f8"),
-                         ("tracker_lag", "<u4"), ("tracker_grain", "<u4")])
+                         ("tracker_lag", "<u4"), ("tracker_grain", "<u4"),
+                         ("ca_balance_abs", "<f8"), ("ca_balance_rel", "<f8"),
+                         ("ca_cache_threshold", "<f8"), ("_pad2", "<u8")])
 RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
     "queries", "hit_tokens", "input_tokens", "probes", "inserted_blocks", "evictions",
     "rlt_draws", "rlt_resets", "rlt_fallbacks", "max_pending", "decision_digest")] +
@@ -90,7 +98,7 @@ RESULT_DTYPE = np.dtype([(n, "<u8") for n in (
 RECORD_DTYPE = np.dtype([("worker", "<u4"), ("hit_tokens", "<u4"), ("n_victims", "<u4"),
                          ("_pad", "<u4"), ("ttft_ms", "<f8"), ("latency_ms", "<f8"),
                          ("score", "<f8"), ("victim_offset", "<u8")])
-assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 128
+assert POLICY_DTYPE.itemsize == C.sizeof(kvr_policy) == 160
 assert RESULT_DTYPE.itemsize == 144 and RECORD_DTYPE.itemsize == 48
 
 _lib = None
@@ -118,6 +126,9 @@ def lib():
             "kvr_trace_collision_bytes": [vp, vp],
             "kvr_trace_check_collisions": [vp, vp, vp, C.c_size_t, vp, vp],
             "kvr_trace_build_next_use": [vp, vp, C.c_size_t, vp, C.c_size_t, vp, vp],
+            "kvr_trace_phase_bytes": [vp, vp, vp],
+            "kvr_trace_build_phases": [vp, u32, vp, C.c_size_t, vp, C.c_size_t, vp, vp, vp],
+            "kvr_sim_run_ledger": [vp, vp, u32, vp, vp, vp, vp, vp, C.c_size_t, vp],
             "kvr_sim_create": [vp, vp],
             "kvr_sim_destroy": [vp],
             "kvr_sim_plan": [vp, u32, vp, vp, vp],
@@ -225,6 +236,30 @@ def kvr_trace_build_next_use(handle: int, nu, scratch, stream=None) -> int:
     return h.value
 
 
+def kvr_trace_phase_bytes(handle: int):
+    a, b = C.c_size_t(0), C.c_size_t(0)
+    _check(lib().kvr_trace_phase_bytes(handle, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def kvr_trace_build_phases(handle: int, B: int, phase, scratch, stream=None):
+    """Returns (new handle, n_phases)."""
+    h = C.c_void_p(0)
+    n = C.c_uint32(0)
+    _check(lib().kvr_trace_build_phases(handle, B, _ptr(phase), phase.numel() * phase.element_size(),
+                                        _ptr(scratch), scratch.numel(), _stream_ptr(stream),
+                                        C.byref(n), C.byref(h)))
+    return h.value, n.value
+
+
+def kvr_sim_run_ledger(handle: int, trace: int, n_trials: int, keys, policies, results, ledger,
+                       workspace, stream=None):
+    _check(lib().kvr_sim_run_ledger(
+        handle, trace, n_trials, _ptr(keys), _ptr(policies), _ptr(results), _ptr(ledger),
+        _ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+
+
 def kvr_sim_create(cfg: kvr_sim_config) -> int:
     h = C.c_void_p(0)
     _check(lib().kvr_sim_create(C.byref(cfg), C.byref(h)))
@@ -293,8 +328,11 @@ class Policy:
     w_hit: float = 1.0
     w_load: float = 1.0
     rls_p0: float = 1000.0     # LBGR_RLS initial covariance P = rls_p0 * I
-    tracker_lag: int = 0       # A29: router's h~ lags the previous query's update
+    tracker_lag: int = 0       # A29: router's h~ lags the last k queries' updates (k <= 32)
     tracker_grain: int = 1     # A29: router sees whole grains of matched blocks
+    ca_balance_abs: float = 32.0        # A38 (ROUTE_CACHE_AWARE): imbalance iff max-min > abs
+    ca_balance_rel: float = 1.0001      #   and max > rel * min (pending queries)
+    ca_cache_threshold: float = 0.5     #   highest match if h~/|q| > threshold
 
     def mu_value(self) -> float:
         if self.mu is not None:
@@ -307,7 +345,7 @@ class Policy:
     def c(self) -> kvr_policy:
         p = kvr_policy()
         for f, _ in kvr_policy._fields_:
-            if f == "_pad":
+            if f in ("_pad", "_pad2"):
                 continue
             if f == "theta0":
                 for k in range(4):
@@ -319,15 +357,16 @@ class Policy:
     def row(self) -> np.ndarray:
         r = np.zeros((), dtype=POLICY_DTYPE)
         for f in POLICY_DTYPE.names:
-            if f != "_pad":
+            if f not in ("_pad", "_pad2"):
                 r[f] = self._get(f)
         return r
 
 
 def policies_extended(arr: np.ndarray) -> bool:
-    """True if any policy needs the extended kernel (OPT, LBGR_RLS, tracker bias)."""
+    """True if any policy needs the extended kernel (OPT, LBGR_RLS, CACHE_AWARE, tracker bias)."""
     a = np.asarray(arr).view(POLICY_DTYPE)
     return bool(np.any((a["eviction"] == EVICT_OPT) | (a["router"] == ROUTE_LBGR_RLS) |
+                       (a["router"] == ROUTE_CACHE_AWARE) |
                        (a["tracker_lag"] != 0) | (a["tracker_grain"] != 1)))
 
 
@@ -432,6 +471,27 @@ class DeviceTrace:
         torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
         t._parent = self        # keeps the packed buffer alive
         return t
+
+    def with_phases(self, B: int, stream=None) -> "DeviceTrace":
+        """A trace handle that also carries the phase index of the phase ledger:
+        phases of B distinct identities, first-appearance bits and next occurrences, built
+        on the device by kvr_trace_build_phases (keeps this handle's next-use index)."""
+        import copy
+        import torch
+        pb, sb = kvr_trace_phase_bytes(self.handle)
+        t = copy.copy(self)
+        t.phase = torch.empty(max(1, pb // 4), dtype=torch.int32, device=self.device)
+        scratch = torch.empty(max(1, sb), dtype=torch.uint8, device=self.device)
+        t.handle, t.n_phases = kvr_trace_build_phases(self.handle, B, t.phase, scratch, stream)
+        t.phase_B = B
+        t._parent = self
+        return t
+
+    def phase_index(self):
+        """(ph, nx, distinct) copies: phase | first-appearance bit, next occurrence, per phase."""
+        n = self.n_blocks_total
+        a = self.phase.cpu().numpy().view(np.uint32)
+        return a[:n].copy(), a[n:2 * n].copy(), a[2 * n: 2 * n + self.n_phases].copy()
 
     def next_use(self) -> np.ndarray:
         """Copy of the device next-use index (u32 per block occurrence, CSR order)."""
@@ -558,6 +618,32 @@ class Simulator:
         hist = b["hist"].cpu().numpy().view(np.uint32).reshape(n, -1).copy() \
             if b["hist"] is not None else None
         return RunOutput(res, rec, vic, hist)
+
+    def run_ledger(self, trace: DeviceTrace, keys, policies: Optional[np.ndarray] = None,
+                   stream=None):
+        """kvr_sim_run_ledger (W = 1, trace.with_phases(B)): returns (results, ledger)
+        with ledger u32 [n_trials, n_phases, 4] = LEDGER_FIELDS per phase."""
+        import torch
+        dev = trace.device
+        n = len(keys)
+        if not self.cfg.extended_policies:
+            self.cfg.extended_policies = 1
+            old = self.handle
+            self.handle = kvr_sim_create(self.cfg)
+            kvr_sim_destroy(old)
+        nph = getattr(trace, "n_phases", 0)   # 0: no phase index (the C ABI refuses it)
+        npz = max(1, nph)
+        kt = torch.from_numpy(np.asarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
+        pt = (torch.from_numpy(np.ascontiguousarray(policies).view(np.uint8)).to(dev)
+              if policies is not None else None)
+        res = torch.empty(max(1, n) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        led = torch.zeros(max(1, n * npz * 4), dtype=torch.int32, device=dev)
+        ws = self.workspace([trace], n, dev)
+        kvr_sim_run_ledger(self.handle, trace.handle, n, kt, pt, res, led, ws, stream)
+        torch.cuda.synchronize()
+        r = res.cpu().numpy().view(RESULT_DTYPE)[:n].copy()
+        lg = led.cpu().numpy().view(np.uint32)[: n * nph * 4]
+        return r, lg.reshape(n, nph, 4).copy()
 
     def close(self):
         if getattr(self, "handle", None):

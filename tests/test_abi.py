@@ -35,7 +35,7 @@ def test_header_declares_the_north_star_entry_points():
 def test_library_exports_every_declared_symbol(libkvr):
     for name in _declared():
         assert hasattr(libkvr, name), name
-    assert libkvr.kvr_abi_version() == 7
+    assert libkvr.kvr_abi_version() == 8
 
 
 def test_library_is_built_from_these_sources(libkvr):
@@ -46,9 +46,9 @@ def test_library_is_built_from_these_sources(libkvr):
 
 def test_struct_sizes_match_header(libkvr):
     from paper_2601_18999_b200 import kvr
-    assert C.sizeof(kvr.kvr_policy) == 128
+    assert C.sizeof(kvr.kvr_policy) == 160
     assert C.sizeof(kvr.kvr_trace_desc) == 72
-    assert C.sizeof(kvr.kvr_sim_config) == 4 + 4 + 24 + 128 + 16 + 8
+    assert C.sizeof(kvr.kvr_sim_config) == 4 + 4 + 24 + 160 + 16 + 8
     assert kvr.RESULT_DTYPE.itemsize == 144 and kvr.RECORD_DTYPE.itemsize == 48
 
 

@@ -69,16 +69,21 @@ def test_tracker_lag_hand_example(kvr, oracle_mod):
     assert list(out.records[0]["worker"][:2]) == [0, 0] and list(out.records[1]["worker"][:2]) == [0, 1]
 
 
-def test_tracker_validation(kvr):
-    with pytest.raises(kvr.KvrError):   # the lag reads the deferred-apply overlay (B <= 1024)
-        kvr.Simulator(1, 2048, policy=kvr.Policy(tracker_lag=1))
+def test_tracker_validation(kvr, oracle_mod):
+    """A lag above KVR_MAX_TRACKER_LAG (32) is refused (host: KvrError; per trial: status
+    3); a lag at a large capacity (B = 2048, the global-memory tier) runs and matches."""
+    with pytest.raises(kvr.KvrError):
+        kvr.Simulator(2, 64, policy=kvr.Policy(tracker_lag=33))
     with pytest.raises(kvr.KvrError):
         kvr.Simulator(2, 64, policy=kvr.Policy(tracker_grain=0))
     tr = wl.adv(2048, 4, 1, seed=2)
     sim = kvr.Simulator(1, 2048)
     out = sim.run(kvr.DeviceTrace(tr), np.array([1, 2], np.uint64),
-                  kvr.policies_array([kvr.Policy(tracker_lag=1), kvr.Policy()]))
+                  kvr.policies_array([kvr.Policy(tracker_lag=33), kvr.Policy()]))
     assert int(out.results[0]["status"]) == 3 and int(out.results[1]["status"]) == 0
+    tr = wl.gsp(10, 8, 0.5, seed=7, W=2, lengths=(128, 256))
+    compare(oracle_mod, kvr, tr, 2, 2048, [kvr.Policy(tracker_lag=3, eviction=e) for e in (0, 1)],
+            [1, 2], record=True)
 
 
 def test_lean_kernel_refuses_extended_policies(kvr):
