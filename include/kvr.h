@@ -245,7 +245,10 @@ typedef struct {
                                       workspace of ~64 B x N per resident CTA */
   uint32_t record_trials;          /* the first R trials emit per-query records + victim logs */
   uint32_t latency_hist_bins;      /* 0, or 1..256 log-bucket bins (4 per octave, bin 0 = <1 ms) */
-  uint32_t force_tier;             /* 0 auto, 1 shared-memory tables, 2 global-memory tables */
+  uint32_t force_tier;             /* 0 auto, 1 shared-memory tables, 2 global-memory tables,
+                                      3 split (W >= 2: identities + tables in global memory,
+                                      tree arrays / bitmaps / stamps in shared memory, two
+                                      workers per warp; beta = 1 engine only) */
   uint32_t extended_policies;      /* 1: per-trial policies may use OPT / LBGR_RLS / tracker bias
                                       (runs the kernel instantiation that carries them; implied
                                       when default_policy uses one).  0: such a per-trial policy
@@ -284,7 +287,9 @@ typedef struct { uint32_t worker, hit_tokens, n_victims, _pad; double ttft_ms, l
                  uint64_t victim_offset; } kvr_query_record;
 
 /* Tier and launch shape chosen for (sim, trace): tier 1 = per-worker tables in
- * shared memory, 2 = in global memory (L2-resident); dynamic smem per CTA. */
+ * shared memory, 2 = in global memory (L2-resident), 3 = split (identities + tables
+ * global, the rest shared; chosen automatically for W > 16 when tier 1 does not fit);
+ * dynamic smem per CTA. */
 kvr_status kvr_sim_plan(const kvr_sim* sim, uint32_t max_path_blocks, uint32_t* tier,
                         size_t* smem_bytes, uint32_t* ctas_per_sm);
 /* Workspace bytes for a run of n_trials whose longest path is max_path_blocks. */

@@ -99,7 +99,7 @@ struct Plan {
   kvr::AuxLayout aux;
   kvr::FifoLayout fifo;
   kvr::BatchLayout blay;
-  size_t ws_aux, ws_fifo, ws_lag, ws_state, ws_total;
+  size_t ws_aux, ws_fifo, ws_lag, ws_div, ws_state, ws_total;
 };
 
 // continuous batching (kvr_batch.cu): per-worker state in shared memory when W
@@ -114,6 +114,7 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   const size_t smem1 = ctrl + (size_t)c.W * l16.bytes;
   const bool fit1 = c.capacity_blocks <= 65535 && smem1 <= (size_t)optin;   // 0xFFFF = NONE
   const uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
+  if (tier == 3) return fail(KVR_ERR_UNSUPPORTED, "batching: no split tier (force_tier 0..2)");
   if (tier == 1 && !fit1)
     return fail(KVR_ERR_UNSUPPORTED, "batching: shared-memory tier needs %zu B > %d B", smem1, optin);
   pl->tier = tier;
@@ -128,6 +129,7 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   pl->ws_aux = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * sizeof(kvr::BFlight));
   pl->ws_fifo = 0;
   pl->ws_lag = 0;
+  pl->ws_div = 0;
   pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->blay.bytes : 0;
   pl->ws_total = 256 + pl->ws_aux + pl->ws_state;
   return KVR_OK;
@@ -141,20 +143,29 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t max_N, uint32_
   const size_t base = kvr::smem_base_bytes(c.W, max_n);
   const kvr::WorkerLayout l16 = kvr::make_layout(c.capacity_blocks, 2);
   const kvr::WorkerLayout l32 = kvr::make_layout(c.capacity_blocks, 4);
-  const size_t smem1 = base + (size_t)c.W * l16.bytes;
+  const kvr::WorkerLayout lsp = kvr::make_layout(c.capacity_blocks, 2, true);
+  // W > 16 runs two workers per warp, whose idle one's scalars wait in a save area
+  const size_t wsv = c.W > 16 ? sizeof(kvr::WSave) : 0;
+  const size_t smem1 = base + (size_t)c.W * (l16.bytes + wsv);
+  const size_t smem3 = base + (size_t)c.W * (lsp.sbytes + sizeof(kvr::WSave));
   const bool fit1 = c.capacity_blocks <= 65533 && smem1 <= (size_t)optin;   // 0xFFFE/F = tomb/empty
-  uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : 2u);
+  // split tier (identities + tables global, tree arrays / bitmaps / stamps shared): W > 16
+  const bool fit3 = c.W >= 2 && c.capacity_blocks <= 65533 && smem3 <= (size_t)optin;
+  uint32_t tier = c.force_tier ? c.force_tier : (fit1 ? 1u : ((fit3 && c.W > 16) ? 3u : 2u));
   if (tier == 1 && !fit1)
     return fail(KVR_ERR_UNSUPPORTED, "shared-memory tier needs %zu B > %d B (W=%u, B=%u)", smem1,
                 optin, c.W, c.capacity_blocks);
+  if (tier == 3 && !fit3)
+    return fail(KVR_ERR_UNSUPPORTED, "split tier needs W >= 2 and %zu B <= %d B of shared memory",
+                smem3, optin);
   if (tier == 2 && base > (size_t)optin)
     return fail(KVR_ERR_UNSUPPORTED, "query staging needs %zu B of shared memory", base);
   pl->tier = tier;
-  // global tier with W > 16 (1,024 threads): u16 slot ids halve the L1/L2 footprint of the
-  // tables (kernel tier 3); below that the u32 kernel keeps its registers
-  pl->ktier = (tier == 2 && c.W > 16 && c.capacity_blocks <= 65533) ? 3u : tier;
-  pl->lay = (tier == 1 || pl->ktier == 3) ? l16 : l32;
-  pl->smem = tier == 1 ? smem1 : base;
+  // kernel tier: 1 shared, 2 global (u32 ids), 3 global with u16 ids (W > 16: halves the
+  // L1/L2 footprint of the tables), 4 split
+  pl->ktier = tier == 3 ? 4u : ((tier == 2 && c.W > 16 && c.capacity_blocks <= 65533) ? 3u : tier);
+  pl->lay = tier == 3 ? lsp : ((tier == 1 || pl->ktier == 3) ? l16 : l32);
+  pl->smem = tier == 1 ? smem1 : (tier == 3 ? smem3 : base);
   cudaError_t e = kvr::replay_attrs(pl->ktier, pl->smem, &pl->ctas_per_sm, c.W, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
@@ -166,8 +177,9 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t max_N, uint32_
   pl->fifo = kvr::make_fifo(c.W, c.pending_ring, max_N);
   pl->ws_fifo = (size_t)pl->grid * pl->fifo.bytes;
   pl->ws_lag = ext ? (size_t)pl->grid * kvr::kLagRing * kvr::lag_entry_bytes(max_n) : 0;
-  pl->ws_state = tier == 2 ? (size_t)pl->grid * c.W * pl->lay.bytes : 0;
-  pl->ws_total = 256 + pl->ws_aux + pl->ws_fifo + pl->ws_lag + pl->ws_state;
+  pl->ws_div = kvr::align16((size_t)pl->grid * 8 * ((size_t)max_n + 1));
+  pl->ws_state = tier >= 2 ? (size_t)pl->grid * c.W * pl->lay.gbytes : 0;
+  pl->ws_total = 256 + pl->ws_aux + pl->ws_fifo + pl->ws_lag + pl->ws_div + pl->ws_state;
   return KVR_OK;
 }
 
@@ -354,7 +366,7 @@ kvr_status kvr_sim_create(const kvr_sim_config* cfg, kvr_sim** out) {
   if (cfg->pending_ring < 1) return fail(KVR_ERR_INVALID_ARG, "pending_ring must be >= 1");
   if (cfg->latency_hist_bins > kvr::kMaxHistBins)
     return fail(KVR_ERR_INVALID_ARG, "latency_hist_bins must be <= 256");
-  if (cfg->force_tier > 2) return fail(KVR_ERR_INVALID_ARG, "force_tier must be 0, 1 or 2");
+  if (cfg->force_tier > 3) return fail(KVR_ERR_INVALID_ARG, "force_tier must be 0, 1, 2 or 3");
   if (cfg->extended_policies > 1) return fail(KVR_ERR_INVALID_ARG, "extended_policies must be 0 or 1");
   const kvr_service_model& t = cfg->truth;
   if (!std::isfinite(t.alpha_cached_ms) || !std::isfinite(t.alpha_miss_ms) ||
@@ -484,6 +496,7 @@ kvr_status run_impl(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* tra
   p.bins = d_hist ? c.latency_hist_bins : 0;
   p.stage_bytes = (uint32_t)kvr::stage_bytes(max_n);
   p.scratch_bytes = (uint32_t)kvr::scratch_bytes(max_n);
+  p.slotbuf_bytes = (uint32_t)kvr::slotbuf_bytes(max_n);
   p.max_n = max_n;
   p.aux = pl.aux;
   p.fifo = pl.fifo;
@@ -503,7 +516,8 @@ kvr_status run_impl(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* tra
   p.fifo_base = ws + 256 + pl.ws_aux;
   p.lag_base = pl.ws_lag ? ws + 256 + pl.ws_aux + pl.ws_fifo : nullptr;
   p.lag_entry = (uint32_t)kvr::lag_entry_bytes(max_n);
-  p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux + pl.ws_fifo + pl.ws_lag : nullptr;
+  p.divtab_base = reinterpret_cast<double*>(ws + 256 + pl.ws_aux + pl.ws_fifo + pl.ws_lag);
+  p.gstate = pl.tier >= 2 ? ws + 256 + pl.ws_aux + pl.ws_fifo + pl.ws_lag + pl.ws_div : nullptr;
   if (d_ledger) {
     p.ledger = d_ledger;
     p.ledger_stride = 4 * traces[0]->n_phases;

@@ -74,9 +74,13 @@ __host__ __device__ inline bool policy_valid(const kvr_policy& p) {
 struct WorkerLayout {
   uint32_t B, T, nwords, idx_bytes;
   size_t off_key, off_parent, off_nchild, off_table, off_leaf, off_mark, off_stamp, bytes;
+  // split layout (kernel tier 4): identity + table in global memory (gbytes per worker,
+  // offsets from the global base), tree arrays / bitmaps / stamps in shared memory
+  // (sbytes per worker, offsets from the shared base); unsplit: gbytes = sbytes = bytes
+  size_t gbytes, sbytes;
 };
 
-inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
+inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes, bool split = false) {
   WorkerLayout L{};
   L.B = B;
   uint32_t T = 4;
@@ -84,6 +88,20 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   L.T = T;
   L.nwords = (B + 31) / 32;
   L.idx_bytes = idx_bytes;
+  if (split) {
+    size_t g = 0, o = 0;
+    L.off_key = g;    g = align16(g + (size_t)B * 8);
+    L.off_table = g;  g = align16(g + (size_t)T * idx_bytes);
+    L.off_parent = o; o = align16(o + (size_t)B * idx_bytes);
+    L.off_nchild = o; o = align16(o + (size_t)B * idx_bytes);
+    L.off_leaf = o;   o = align16(o + (size_t)L.nwords * 4);
+    L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);
+    L.off_stamp = o;  o = align16(o + (size_t)B * 2);
+    L.gbytes = g;
+    L.sbytes = o;
+    L.bytes = g + o;
+    return L;
+  }
   size_t o = 0;
   L.off_key = o;    o = align16(o + (size_t)B * 8);
   L.off_parent = o; o = align16(o + (size_t)B * idx_bytes);
@@ -93,6 +111,8 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes) {
   L.off_mark = o;   o = align16(o + (size_t)L.nwords * 4);
   L.off_stamp = o;  o = align16(o + (size_t)B * 2);     // Leaf-LRU recency stamps (u16)
   L.bytes = o;
+  L.gbytes = o;
+  L.sbytes = o;
   return L;
 }
 
@@ -172,7 +192,6 @@ struct __align__(16) Ctrl {
   uint32_t* led;                       // phase ledger of this trial (extended policies) or null
   const uint32_t* lph;                 // its trace's phase index (ph, nx)
   const uint32_t* lnx;
-  uint32_t hist[kMaxHistBins];
 };
 
 inline size_t ctrl_bytes() { return align16(sizeof(Ctrl)); }
@@ -185,7 +204,7 @@ struct WorkerRegs {
 };
 
 // Per-warp shared-memory block: the pending (deferred) apply of this worker's
-// last update, its per-miss slots, Leaf-LRU victims, the overlay victim bitmap
+// last update, its per-miss slots (Leaf-LRU takes its victims in place), the overlay victim bitmap
 // staging area, and the worker's trial counters.
 struct __align__(16) WarpSm {
   double ttft, lat, score;
@@ -198,11 +217,23 @@ struct __align__(16) WarpSm {
   uint32_t x_ri;                   // next unused draw of x_rbuf
   uint32_t m_used, m_size, m_cur;  // stale-tracker mirror: table fill, slots, next ring entry
   unsigned long long x_rbuf[32];   // RLT: 32 counter-based draws, one per lane
-  uint32_t slot[4];                // [max_n] slots | [max_n] victims | [32] bitmap
 };
-inline size_t scratch_bytes(uint32_t max_n) {
-  return align16(sizeof(WarpSm) + 4 * (2 * (size_t)max_n + 32));
-}
+inline size_t scratch_bytes(uint32_t) { return align16(sizeof(WarpSm)); }
+// Per-miss slot buffers of an update ([max_n] slot | evicted << 31, then the [32] victim
+// bitmap staging of the overlay): at most two updates are live at once (the one being
+// decided, and the previous query's pending apply), so a CTA holds two, by query parity.
+inline size_t slotbuf_bytes(uint32_t max_n) { return align16(4 * ((size_t)max_n + 32)); }
+
+// Save area of one worker's query-loop scalars when a warp serves two workers (split
+// tier): uniform doubles (P, F, P~, theta, front completion time), tick count, FIFO
+// head / count, the front record (lanes 0..7) and the overlay victim bitmap (per lane).
+struct __align__(16) WSave {
+  double u[8];
+  unsigned long long k;
+  uint32_t fh, fn;
+  double fr[8];
+  uint32_t vb[32];
+};
 
 // ---- continuous batching (kvr_batch.cu; readings A30-A36) ----
 // one assigned query: waiting in the FIFO ring, then in a batch slot (c set at dequeue)
@@ -256,7 +287,7 @@ struct ReplayParams {
   const uint32_t* trial_trace;   // [n_trials] or null
   uint32_t n_traces, n_trials, W, B;
   uint32_t ring, record_trials, rec_stride, bins;
-  uint32_t stage_bytes, scratch_bytes;
+  uint32_t stage_bytes, scratch_bytes, slotbuf_bytes;
   uint32_t max_n, _pad1;
   WorkerLayout lay;
   AuxLayout aux;
@@ -265,6 +296,7 @@ struct ReplayParams {
   uint8_t* lag_base;             // [grid][kLagRing][lag_entry] update rings (extended policies)
   uint32_t lag_entry, ledger_stride;   // bytes per ring entry; u32 per trial of the ledger
   uint32_t* ledger;              // phase ledger [n_trials][ledger_stride] or null
+  double* divtab_base;           // [grid][max_n + 1] exact (bt * k) / 1000 per CTA (global, L1)
   kvr_service_model truth;
   kvr_policy defpol;
   const kvr_policy* policies;
@@ -287,13 +319,15 @@ inline size_t divtab_bytes(uint32_t max_n) { return align16(8 * ((size_t)max_n +
 
 inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
   return ctrl_bytes() + kNumStages * stage_bytes(max_n) + (size_t)W * scratch_bytes(max_n) +
-         divtab_bytes(max_n);
+         2 * slotbuf_bytes(max_n);
 }
 
 // launchers (kvr_pack.cu / kvr_kernel.cu)
 cudaError_t launch_pack(const kvr_trace_desc& d, QueryHdr* hdr, uint64_t* hash, uint32_t* scratch,
                         cudaStream_t s);
-// tier 1 = tables in shared memory (u16 slot ids), 2 = tables in global memory (u32 slot ids)
+// tier 1 = tables in shared memory (u16 slot ids), 2 = tables in global memory (u32 slot ids),
+// 3 = global memory with u16 ids (W > 16), 4 = split: identities + tables in global memory,
+// tree arrays / bitmaps / stamps in shared memory (u16 ids, W > 16)
 // ext: the instantiation with the extended policies (OPT, LBGR_RLS, tracker bias)
 cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W, bool ext);
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,

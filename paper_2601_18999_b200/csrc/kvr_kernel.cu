@@ -80,33 +80,49 @@ struct WorkerView {
   uint32_t* mark;
 };
 
+// gbase: identities + table; sbase: tree arrays, bitmaps (and stamps) -- the same base
+// except in the split tier (kMem == 2)
 template <typename Idx>
-__device__ __forceinline__ WorkerView<Idx> make_view(uint8_t* base, const WorkerLayout& L) {
+__device__ __forceinline__ WorkerView<Idx> make_view(uint8_t* gbase, uint8_t* sbase,
+                                                     const WorkerLayout& L) {
   WorkerView<Idx> v;
-  v.key = reinterpret_cast<uint64_t*>(base + L.off_key);
-  v.parent = reinterpret_cast<Idx*>(base + L.off_parent);
-  v.nchild = reinterpret_cast<Idx*>(base + L.off_nchild);
-  v.table = reinterpret_cast<Idx*>(base + L.off_table);
-  v.leaf = reinterpret_cast<uint32_t*>(base + L.off_leaf);
-  v.mark = reinterpret_cast<uint32_t*>(base + L.off_mark);
+  v.key = reinterpret_cast<uint64_t*>(gbase + L.off_key);
+  v.parent = reinterpret_cast<Idx*>(sbase + L.off_parent);
+  v.nchild = reinterpret_cast<Idx*>(sbase + L.off_nchild);
+  v.table = reinterpret_cast<Idx*>(gbase + L.off_table);
+  v.leaf = reinterpret_cast<uint32_t*>(sbase + L.off_leaf);
+  v.mark = reinterpret_cast<uint32_t*>(sbase + L.off_mark);
   return v;
 }
 
-// dynamic shared memory map: [Ctrl][stages][WarpSm x W][divtab][workers x W] (tier 1)
+// dynamic shared memory map: [Ctrl][stages][WarpSm x W][slot buffers x 2][workers x W] (tier 1)
 __device__ __forceinline__ size_t stage_off() { return align16(sizeof(Ctrl)); }
 __device__ __forceinline__ size_t warps_off(const ReplayParams& p) {
   return stage_off() + (size_t)kNumStages * p.stage_bytes;
 }
-__device__ __forceinline__ size_t divtab_off(const ReplayParams& p) {
+__device__ __forceinline__ size_t slotbuf_off(const ReplayParams& p) {
   return warps_off(p) + (size_t)p.W * p.scratch_bytes;
 }
 __device__ __forceinline__ size_t workers_off(const ReplayParams& p) {
-  return divtab_off(p) + align16(8 * ((size_t)p.max_n + 1));
+  return slotbuf_off(p) + 2 * (size_t)p.slotbuf_bytes;
 }
-template <bool kGlobal>
-__device__ __forceinline__ uint8_t* worker_base(const ReplayParams& p, uint32_t w) {
-  if constexpr (kGlobal) return p.gstate + ((size_t)blockIdx.x * p.W + w) * p.lay.bytes;
+// the per-miss slots (and, after max_n of them, the overlay bitmap staging) of the update
+// of query j: buffer j mod 2
+__device__ __forceinline__ uint32_t* slot_buf(const ReplayParams& p, uint32_t j) {
+  return reinterpret_cast<uint32_t*>(kvr_dsmem + slotbuf_off(p) + (size_t)(j & 1) * p.slotbuf_bytes);
+}
+// kMem: 0 = worker state in shared memory, 1 = in global memory, 2 = split (identities and
+// tables global, the rest shared), 3 = shared memory like 0; kMem >= 2 runs two workers
+// per warp (W > 16)
+template <int kMem>
+__device__ __forceinline__ uint8_t* worker_gbase(const ReplayParams& p, uint32_t w) {
+  if constexpr (kMem == 1 || kMem == 2) return p.gstate + ((size_t)blockIdx.x * p.W + w) * p.lay.gbytes;
   else return kvr_dsmem + workers_off(p) + (size_t)w * p.lay.bytes;
+}
+template <int kMem>
+__device__ __forceinline__ uint8_t* worker_sbase(const ReplayParams& p, uint32_t w) {
+  if constexpr (kMem == 2) return kvr_dsmem + workers_off(p) + (size_t)w * p.lay.sbytes;
+  else return worker_gbase<kMem>(p, w);
 }
 __device__ __forceinline__ WarpSm* warp_sm(const ReplayParams& p, uint32_t w) {
   return reinterpret_cast<WarpSm*>(kvr_dsmem + warps_off(p) + (size_t)w * p.scratch_bytes);
@@ -543,24 +559,25 @@ __device__ __forceinline__ uint32_t pick32(uint32_t lo, uint32_t hi, uint32_t t)
 // rem)); U loses the victim (its slot is refilled by the new, marked leaf) and
 // gains the victim's parent iff that became an unmarked leaf.  Resets and the
 // U = {} fallbacks (A5) recount from lw/mw.
-template <typename Idx, bool kGlobal, int kTag>
+template <typename Idx, int kMem, int kTag>
 __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, Idx p0,
                                             uint32_t fallback, uint64_t K, uint32_t worker,
-                                            uint32_t lane, bool use_list) {
+                                            uint32_t lane, bool use_list, uint32_t jq) {
   const Idx NIL = Nil<Idx>::empty;
   const uint32_t B = p_.B, nwords = p_.lay.nwords;
-  uint8_t* wb = worker_base<kGlobal>(p_, worker);
-  const WorkerView<Idx> S = make_view<Idx>(wb, p_.lay);
+  uint8_t* wb = worker_gbase<kMem>(p_, worker);
+  uint8_t* sb = worker_sbase<kMem>(p_, worker);
+  const WorkerView<Idx> S = make_view<Idx>(wb, sb, p_.lay);
   RecencyLog R;
   R.log = reinterpret_cast<uint64_t*>(p_.aux_base + ((size_t)blockIdx.x * p_.W + worker) * p_.aux.bytes +
                                       p_.aux.off_log);
-  R.stamp = reinterpret_cast<uint16_t*>(wb + p_.lay.off_stamp);
+  R.stamp = reinterpret_cast<uint16_t*>(sb + p_.lay.off_stamp);
   R.cap_mask = p_.aux.log_cap - 1;
   // state in and out through the warp's shared-memory block (no by-reference
   // arguments: they would put the caller's registers in local memory)
   WarpSm* ws = warp_sm(p_, worker);
-  uint32_t* slots = ws->slot;
-  uint32_t* vmap = ws->slot + 2 * p_.max_n;
+  uint32_t* slots = slot_buf(p_, jq);
+  uint32_t* vmap = slots + p_.max_n;
   // registers: size, |T| and e_i only; counters are bumped in shared memory (draws
   // = the change of e_i, evictions are counted by the caller), the log cursors and
   // recency stamp are read there on the rare paths that need them
@@ -821,16 +838,18 @@ __device__ __forceinline__ uint64_t* opt_keys(const ReplayParams& p, uint32_t w)
                                      p.aux.off_log);
 }
 
-template <typename Idx, bool kGlobal, int kTag>
+template <typename Idx, int kMem, int kTag>
 __device__ __noinline__ void opt_decide(const ReplayParams& p_, uint32_t M, uint32_t kf, Idx p0,
-                                        const uint32_t* nu_q, uint32_t worker, uint32_t lane) {
+                                        const uint32_t* nu_q, uint32_t worker, uint32_t lane,
+                                        uint32_t jq) {
   const Idx NIL = Nil<Idx>::empty;
   const uint32_t B = p_.B;
-  uint8_t* wb = worker_base<kGlobal>(p_, worker);
-  const WorkerView<Idx> S = make_view<Idx>(wb, p_.lay);
+  uint8_t* wb = worker_gbase<kMem>(p_, worker);
+  uint8_t* sb = worker_sbase<kMem>(p_, worker);
+  const WorkerView<Idx> S = make_view<Idx>(wb, sb, p_.lay);
   uint64_t* okey = opt_keys(p_, worker);
   WarpSm* ws = warp_sm(p_, worker);
-  uint32_t* slots = ws->slot;
+  uint32_t* slots = slot_buf(p_, jq);
   MemBits mb;
   mb.leaf = S.leaf;
   mb.mark = S.mark;
@@ -892,7 +911,7 @@ __device__ __noinline__ void opt_decide(const ReplayParams& p_, uint32_t M, uint
     __syncwarp();
   }
   if (lane == 0) ws->x.size = size;
-  (ws->slot + 2 * p_.max_n)[lane] = vbits;   // victims -> overlay bitmap (read back by the caller)
+  (slots + p_.max_n)[lane] = vbits;   // victims -> overlay bitmap (read back by the caller)
   __syncwarp();
 }
 
@@ -967,19 +986,20 @@ __device__ __noinline__ void mirror_apply(const ReplayParams& p, const uint64_t*
 // Deferred apply of one update: table deletes/inserts, slot arrays, log entries,
 // victim digest term and the query record (trial sums are added in query order
 // by the accounting step).
-template <typename Idx, bool kGlobal, int kTag, bool kExt>
+template <typename Idx, int kMem, int kTag, bool kExt>
 __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, uint32_t w, bool tree,
                                           bool use_list, bool lbgr_or_static, kvr_query_record* rec,
                                           uint64_t* vlog) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(kvr_dsmem);
   WarpSm* ws = warp_sm(p, w);
   const uint8_t* stage = kvr_dsmem + stage_off();
-  uint8_t* wb = worker_base<kGlobal>(p, w);
-  const WorkerView<Idx> S = make_view<Idx>(wb, p.lay);
+  uint8_t* wb = worker_gbase<kMem>(p, w);
+  uint8_t* sb = worker_sbase<kMem>(p, w);
+  const WorkerView<Idx> S = make_view<Idx>(wb, sb, p.lay);
   RecencyLog R;
   R.log = reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
                                       p.aux.off_log);
-  R.stamp = reinterpret_cast<uint16_t*>(wb + p.lay.off_stamp);
+  R.stamp = reinterpret_cast<uint16_t*>(sb + p.lay.off_stamp);
   R.cap_mask = p.aux.log_cap - 1;
   const uint32_t tmask = p.lay.T - 1;
   const uint64_t* H = reinterpret_cast<const uint64_t*>(stage + (size_t)ws->buf * p.stage_bytes + 32);
@@ -991,6 +1011,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   const uint32_t* nx = kExt ? ctrl->lnx : nullptr;
   uint32_t* lastacc = led ? last_access(p, w) : nullptr;
   const uint32_t n = ws->n, kf = ws->kf, M = ws->M, nev = ws->nev, wq = ws->wq, ltail0 = ws->ltail0;
+  const uint32_t* wslots = slot_buf(p, ws->j);
   const uint32_t nfree = M - nev;
   const uint64_t vc = ws->vc;
   uint64_t V = 0;
@@ -1001,7 +1022,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     const uint32_t cnt = min(32u, M - cb);
     const uint32_t qq = cb + lane;
     const bool act = lane < cnt;
-    const uint32_t sv = act ? ws->slot[qq] : 0u;
+    const uint32_t sv = act ? wslots[qq] : 0u;
     const uint32_t my_slot = sv & 0x7fffffffu;
     const bool my_ev = (sv >> 31) != 0;
     const uint64_t t = act ? H[kf + qq] : 0ull;
@@ -1092,6 +1113,20 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   KVR_ACC(23, t_ap);   // digest term, record
 }
 
+// Scalar state of one worker in the query loop (see the kernel): FIFO head / count,
+// Eq. 2 load P, last completion F, LBGR's decayed load P~ and theta, the tick count,
+// the FIFO front record (lane f < 8 holds field f; fr_c uniform) and the overlay victim
+// bitmap of a pending update (lane l: word l).
+struct WSt {
+  double P, F, Pt, th0, th1, th2, th3, fr, fr_c;
+  uint64_t k;
+  uint32_t fh, fn, vbits;
+};
+// its shared-memory save area (split tier: two workers per warp), after the workers
+__device__ __forceinline__ WSave* wsave(const ReplayParams& p, uint32_t v) {
+  return reinterpret_cast<WSave*>(kvr_dsmem + workers_off(p) + (size_t)p.W * p.lay.sbytes) + v;
+}
+
 // occupancy targets (shared memory allows ~4 CTAs/SM at W<=4 and 2 at W<=8):
 // 128 threads -> 4 CTAs/SM (128 regs), 256 -> 2 (128 regs), else 1
 template <int kMaxThreads>
@@ -1100,39 +1135,75 @@ struct MinBlocks { static constexpr int value = kMaxThreads <= 128 ? 4 : (kMaxTh
 // kExt: the extended policies (offline OPT, LBGR_RLS, tracker bias) are
 // compiled in.  The lean instantiation runs the paper's default policies without
 // paying for them in registers and code layout (measured 2.6 %).
-template <typename Idx, bool kGlobal, int kMaxThreads, bool kExt>
+template <typename Idx, int kMem, int kMaxThreads, bool kExt>
 __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     replay_kernel(const __grid_constant__ ReplayParams p) {
   uint8_t* smem = kvr_dsmem;
   const Idx NIL = Nil<Idx>::empty;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // workers per warp: the split tier (W > 16) runs W/2 warps of two workers each, so that
+  // every thread keeps 128 registers (1,024 threads would cap them at 64 and spill)
+  constexpr uint32_t kV = kMem >= 2 ? 2u : 1u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
   const uint32_t W = p.W, B = p.B;
   const WorkerLayout& L = p.lay;
   const uint32_t tmask = L.T - 1, nwords = L.nwords;
 
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem);
   uint8_t* stage = smem + align16(sizeof(Ctrl));
-  WarpSm* ws = reinterpret_cast<WarpSm*>(stage + (size_t)kNumStages * p.stage_bytes +
-                                         (size_t)w * p.scratch_bytes);
-  uint32_t* slots = ws->slot;              // [max_n] slot | evicted << 31 per miss
-  uint32_t* victims = slots + p.max_n;     // [max_n] Leaf-LRU victims of one query
-  uint32_t* vmap = victims + p.max_n;      // [32] victim bitmap staging (overlay)
-  double* divtab = reinterpret_cast<double*>(stage + (size_t)kNumStages * p.stage_bytes +
-                                             (size_t)W * p.scratch_bytes);
-  uint8_t* sbase = reinterpret_cast<uint8_t*>(divtab) + align16(8 * ((size_t)p.max_n + 1));
-  uint8_t* wbase = kGlobal ? p.gstate + ((size_t)blockIdx.x * W + w) * L.bytes
-                           : sbase + (size_t)w * L.bytes;
-  const WorkerView<Idx> S = make_view<Idx>(wbase, L);
-  uint8_t* abase = p.aux_base + ((size_t)blockIdx.x * W + w) * p.aux.bytes;
+  // exact (bt*k)/1000 for k = 0..max_n (A9), per CTA in global memory (L1-resident)
+  double* divtab = p.divtab_base + (size_t)blockIdx.x * (p.max_n + 1);
   // this CTA's pending-FIFO pool: chunk links, then 32-record chunks (FifoLayout)
   uint32_t* flink = reinterpret_cast<uint32_t*>(p.fifo_base + (size_t)blockIdx.x * p.fifo.bytes);
   double* fifo = reinterpret_cast<double*>(p.fifo_base + (size_t)blockIdx.x * p.fifo.bytes +
                                            p.fifo.off_rec);
-  RecencyLog R;
-  R.log = reinterpret_cast<uint64_t*>(abase + p.aux.off_log);
-  R.stamp = reinterpret_cast<uint16_t*>(wbase + L.off_stamp);
-  R.cap_mask = p.aux.log_cap - 1;
   const bool regbits = nwords <= 32;
+  // per-worker scalar state of the query loop: registers (kV == 1) or, with two workers
+  // per warp, saved in shared memory between uses (only one set live at a time)
+  WSt st0{};
+  auto st_load = [&](uint32_t v) -> WSt {
+    const WSave* sv = wsave(p, v);
+    WSt X;
+    X.P = sv->u[0]; X.F = sv->u[1]; X.Pt = sv->u[2]; X.th0 = sv->u[3]; X.th1 = sv->u[4];
+    X.th2 = sv->u[5]; X.th3 = sv->u[6]; X.fr_c = sv->u[7]; X.k = sv->k; X.fh = sv->fh; X.fn = sv->fn;
+    X.fr = lane < 8 ? sv->fr[lane] : 0.0;
+    X.vbits = sv->vb[lane];
+    return X;
+  };
+  auto st_store = [&](uint32_t v, const WSt& X) {
+    WSave* sv = wsave(p, v);
+    __syncwarp();
+    if (lane == 0) {
+      sv->u[0] = X.P; sv->u[1] = X.F; sv->u[2] = X.Pt; sv->u[3] = X.th0; sv->u[4] = X.th1;
+      sv->u[5] = X.th2; sv->u[6] = X.th3; sv->u[7] = X.fr_c; sv->k = X.k; sv->fh = X.fh; sv->fn = X.fn;
+    }
+    if (lane < 8) sv->fr[lane] = X.fr;
+    sv->vb[lane] = X.vbits;
+    __syncwarp();
+  };
+// binds the worker-local names (w, ws, S, R and the scalar state) for worker `vv`
+#define KVR_BIND_WORKER(vv)                                                          \
+  const uint32_t w = (vv);                                                           \
+  WSt Xl_;                                                                           \
+  if constexpr (kV > 1) Xl_ = st_load(w);                                            \
+  WSt& X_ = kV > 1 ? Xl_ : st0;                                                      \
+  uint32_t& fh = X_.fh; uint32_t& fn = X_.fn; uint32_t& vbits = X_.vbits;            \
+  double& P = X_.P; double& F = X_.F; double& Pt = X_.Pt; double& fr = X_.fr;        \
+  double& fr_c = X_.fr_c; double& th0 = X_.th0; double& th1 = X_.th1;              \
+  double& th2 = X_.th2; double& th3 = X_.th3; uint64_t& k = X_.k;                    \
+  WarpSm* ws = warp_sm(p, w);                                                        \
+  const WorkerView<Idx> S =                                                          \
+      make_view<Idx>(worker_gbase<kMem>(p, w), worker_sbase<kMem>(p, w), L);         \
+  RecencyLog R;                                                                      \
+  R.log = reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * W + w) *    \
+                                      p.aux.bytes + p.aux.off_log);                  \
+  R.stamp = reinterpret_cast<uint16_t*>(worker_sbase<kMem>(p, w) + L.off_stamp);     \
+  R.cap_mask = p.aux.log_cap - 1;                                                    \
+  (void)fh; (void)fn; (void)vbits; (void)P; (void)F; (void)Pt; (void)fr; (void)fr_c; \
+  (void)th0; (void)th1; (void)th2; (void)th3; (void)k; (void)S; (void)R
+#define KVR_SAVE_WORKER() \
+  do {                    \
+    if constexpr (kV > 1) st_store(w, X_); \
+  } while (0)
 
   if (tid == 0) {
     for (uint32_t b = 0; b < kNumStages; ++b) mbar_init(&ctrl->mbar[b], 1);
@@ -1178,47 +1249,60 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     const unsigned long long t_trial0 = clock64();
 #endif
     // ---- per-trial init: empty caches S_i^(0), P_i^(0) = 0 ----
-    for (uint32_t i = lane; i < L.T; i += 32) S.table[i] = NIL;
-    for (uint32_t i = lane; i < nwords; i += 32) {
-      S.leaf[i] = 0;
-      S.mark[i] = 0;
-    }
-    if (use_list)
-      for (uint32_t i = lane; i < B; i += 32) R.stamp[i] = 0;
-    if (lag) {   // the tracker's mirror starts empty too
-      const WorkerView<Idx> MV = mirror_view<Idx>(p, w);
-      for (uint32_t i = lane; i < L.T; i += 32) MV.table[i] = NIL;
-    }
     if (led)
       for (uint32_t i = tid; i < p.ledger_stride; i += blockDim.x) led[i] = 0u;
-    // The worker's scalar cache state (size, |T|, log cursors, e_i, counters) lives in
-    // its shared-memory block ws->x; the chosen warp works on a register copy for
-    // the duration of its update (nothing of it stays live across the query loop).
-    if (lane == 0) {
-      WorkerRegs w0;
-      w0.size = 0; w0.cntT = 0; w0.used = 0; w0.wq = 0; w0.lhead = 0; w0.ltail = 0; w0.e = 0;
-      w0.c_ins = 0; w0.c_evict = 0; w0.c_draws = 0; w0.c_resets = 0; w0.c_fb = 0;
-      ws->x = w0;
-      ws->x_ri = 32;   // next unused draw of the batch (none yet)
-      ws->m_used = 0;
-      ws->m_size = 0;
-      ws->m_cur = 0;
+#pragma unroll
+    for (uint32_t vi = 0; vi < kV; ++vi) {
+      if (kV > 1 && wid + vi * nwarps >= W) break;
+      KVR_BIND_WORKER(wid + vi * nwarps);
+      for (uint32_t i = lane; i < L.T; i += 32) S.table[i] = NIL;
+      for (uint32_t i = lane; i < nwords; i += 32) {
+        S.leaf[i] = 0;
+        S.mark[i] = 0;
+      }
+      if (use_list)
+        for (uint32_t i = lane; i < B; i += 32) R.stamp[i] = 0;
+      if (lag) {   // the tracker's mirror starts empty too
+        const WorkerView<Idx> MV = mirror_view<Idx>(p, w);
+        for (uint32_t i = lane; i < L.T; i += 32) MV.table[i] = NIL;
+      }
+      // The worker's scalar cache state (size, |T|, log cursors, e_i, counters) lives in
+      // its shared-memory block ws->x; the chosen warp works on a register copy for
+      // the duration of its update (nothing of it stays live across the query loop).
+      if (lane == 0) {
+        WorkerRegs w0;
+        w0.size = 0; w0.cntT = 0; w0.used = 0; w0.wq = 0; w0.lhead = 0; w0.ltail = 0; w0.e = 0;
+        w0.c_ins = 0; w0.c_evict = 0; w0.c_draws = 0; w0.c_resets = 0; w0.c_fb = 0;
+        ws->x = w0;
+        ws->x_ri = 32;   // next unused draw of the batch (none yet)
+        ws->m_used = 0;
+        ws->m_size = 0;
+        ws->m_cur = 0;
+      }
+      fh = 0;
+      fn = 0;
+      P = 0.0;
+      F = 0.0;
+      Pt = 0.0;
+      th0 = pol.theta0[0];
+      th1 = pol.theta0[1];
+      th2 = pol.theta0[2];
+      th3 = pol.theta0[3];
+      k = 0;
+      fr = 0.0;      // front record of the pending FIFO
+      fr_c = 0.0;
+      vbits = 0;     // victims of this worker's pending update
+      if (rls && lane < 16) rls_region(p, w)[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;   // P = p0 I
+      if (lane == 0) {
+        ws->active = 0;
+        ws->c_probes = 0; ws->c_hit = 0; ws->c_in = 0; ws->c_q = 0; ws->c_maxp = 0;
+        ws->ftail = 0;        // record index of the next push (chunk boundary: allocate first)
+        ws->ffree = ~0u;      // this worker's free-chunk list (empty)
+      }
+      KVR_SAVE_WORKER();
     }
-    uint32_t fh = 0, fn = 0;
-    double P = 0.0, F = 0.0, Pt = 0.0;
-    double th0 = pol.theta0[0], th1 = pol.theta0[1], th2 = pol.theta0[2], th3 = pol.theta0[3];
-    uint64_t k = 0;
-    // front record of the pending FIFO: lane f < 8 holds field f; fr_c is uniform
-    double fr = 0.0, fr_c = 0.0;
-    uint32_t vbits = 0;     // victims of this warp's pending update (lane l: word l)
-    if (rls && lane < 16) rls_region(p, w)[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;   // P = p0 I
-    if (lane == 0) {
-      ws->active = 0;
-      ws->c_probes = 0; ws->c_hit = 0; ws->c_in = 0; ws->c_q = 0; ws->c_maxp = 0;
-      ws->ftail = 0;        // record index of the next push (chunk boundary: allocate first)
-      ws->ffree = ~0u;      // this worker's free-chunk list (empty)
-    }
-    vmap[lane] = 0u;
+    for (uint32_t i = tid; i < 2 * 32; i += blockDim.x)   // overlay staging of both slot buffers
+      slot_buf(p, i >> 5)[p.max_n + (i & 31)] = 0u;
     if (tid == 0) {
       ctrl->sum_lat = 0.0;
       ctrl->sum_ttft = 0.0;
@@ -1237,7 +1321,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ctrl->lnx = tr.nx;
       }
     }
-    for (uint32_t b = tid; b < p.bins; b += blockDim.x) ctrl->hist[b] = 0;
+    uint32_t* hist = p.hist ? p.hist + (size_t)trial * p.bins : nullptr;   // global, per trial
+    if (hist)
+      for (uint32_t b = tid; b < p.bins; b += blockDim.x) hist[b] = 0;
     // (bt*k)/1000.0 computed once per trial with the same IEEE division (A9)
     for (uint32_t kk = tid; kk <= p.max_n; kk += blockDim.x) divtab[kk] = (double)(bt * kk) / 1000.0;
 
@@ -1279,198 +1365,6 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     uint32_t consumed = 0;
 
     const double pol_inv_dt = 1.0 / pol.delta_t_ms;
-    // ---- steps 1-3 of one query for this warp's worker ----
-    // Membership = the table, or the path Hp[0..np) (same position, same identity),
-    // minus the pending update's victims (register bitmap vbits) if minus_victims.
-    auto score_query = [&](const uint64_t* Hq, double aq, uint32_t nq_in, uint32_t qtok,
-                           const uint64_t* Hp, uint32_t np, bool minus_victims, uint32_t& m_o,
-                           uint32_t& mview_o,
-                           double& score_o, double& Chat_o, double& f0_o, double& f1_o,
-                           double& f2_o) {
-      KVR_T0(tl);
-      // 1. catch-up (A11: tick before completion before routing)
-      {
-        const double rho = pol.rho, dt = pol.delta_t_ms, inv_dt = pol_inv_dt;
-#pragma unroll 1
-        for (;;) {
-          if (lbgr) {
-            // every tick k' with (double)k'*dt <= min(a, c) comes first (A11); (double)k'*dt
-            // is monotone in k', so find the last such k' and apply the multiplications
-            // one by one (same rounding sequence as a per-tick loop)
-            const double lim = (fn == 0 || aq < fr_c) ? aq : fr_c;
-            const double est = lim * inv_dt;   // a guess only: the loops below make it exact
-            uint64_t kk = est < 1.8e19 ? (uint64_t)est : k;
-            if (kk < k) kk = k;
-            while ((double)(kk + 1) * dt <= lim) ++kk;
-            while (kk > k && (double)kk * dt > lim) --kk;
-            if (kk > k) {
-              if (Pt != 0.0) {
-                uint32_t nt = (uint32_t)(kk - k);
-#pragma unroll 1
-                for (; nt >= 4; nt -= 4) {
-                  Pt = rho * Pt;
-                  Pt = rho * Pt;
-                  Pt = rho * Pt;
-                  Pt = rho * Pt;
-                }
-                for (; nt; --nt) Pt = rho * Pt;
-              }
-              k = kk;
-            }
-          }
-          if (fn != 0 && fr_c <= aq) {
-            // pop the front record (its fields are in fr); an emptied chunk goes to this
-            // worker's free list and the head follows the chunk link
-            const uint32_t nh = fh + 1;
-            --fn;
-            if ((nh & (kFifoChunk - 1)) == 0) {
-              const uint32_t c0 = (nh - 1) / kFifoChunk;
-              const uint32_t nxt = fn ? flink[c0] : 0u;
-              __syncwarp();
-              if (lane == 0) {
-                flink[c0] = ws->ffree;
-                ws->ffree = c0;
-              }
-              fh = fn ? nxt * kFifoChunk : nh;
-            } else {
-              fh = nh;
-            }
-            if (lbgr) {
-              const double fa = __shfl_sync(kFull, fr, 1), fE = __shfl_sync(kFull, fr, 2);
-              const double g0 = __shfl_sync(kFull, fr, 3), g1 = __shfl_sync(kFull, fr, 4);
-              const double g2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
-              const uint64_t ka = (uint64_t)__double_as_longlong(__shfl_sync(kFull, fr, 7));
-              const double E = fr_c - fa;
-              const double res = E - fE;
-              if (rls) {
-                // OnlineUpdate, RLS reading (A8b), one weighted least-squares step in
-                // the oracle's order (rls_step): lane 4a+b holds P[a][b]; every sum is
-                // gathered by shuffles left to right.  pi = P phi, gamma = lam + phi'pi,
-                // k = pi / gamma, theta += k e, P = (P - k pi') / lam.
-                const double lam = pol.mu;
-                double* Rg = rls_region(p, w);
-                const uint32_t ra = (lane >> 2) & 3u, rb = lane & 3u;
-                const double Pab = lane < 16 ? Rg[lane] : 0.0;
-                const double phb = rb == 0 ? g0 : (rb == 1 ? g1 : (rb == 2 ? g2 : 1.0));
-                const double prod = Pab * phb;
-                double pi = __shfl_sync(kFull, prod, 4 * ra);
-                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 1);
-                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 2);
-                pi = pi + __shfl_sync(kFull, prod, 4 * ra + 3);   // pi[a] in lanes 4a..4a+3
-                double gsum = g0 * __shfl_sync(kFull, pi, 0);
-                gsum = gsum + g1 * __shfl_sync(kFull, pi, 4);
-                gsum = gsum + g2 * __shfl_sync(kFull, pi, 8);
-                gsum = gsum + 1.0 * __shfl_sync(kFull, pi, 12);
-                const double gamma = lam + gsum;
-                const double kk = pi / gamma;                       // k[a]
-                const double pib = __shfl_sync(kFull, pi, 4 * rb);  // pi[b]
-                if (lane < 16) Rg[lane] = (Pab - kk * pib) / lam;
-                th0 = th0 + __shfl_sync(kFull, kk, 0) * res;
-                th1 = th1 + __shfl_sync(kFull, kk, 4) * res;
-                th2 = th2 + __shfl_sync(kFull, kk, 8) * res;
-                th3 = th3 + __shfl_sync(kFull, kk, 12) * res;
-              } else {     // OnlineUpdate (A8): NLMS on the squared residual
-                const double g3 = 1.0;
-                double s = g0 * g0;
-                s = s + g1 * g1;
-                s = s + g2 * g2;
-                s = s + g3 * g3;
-                const double gstep = (pol.mu * res) / (1.0 + s);
-                th0 = th0 + gstep * g0;
-                th1 = th1 + gstep * g1;
-                th2 = th2 + gstep * g2;
-                th3 = th3 + gstep * g3;
-              }
-              // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
-              uint64_t kap = k - ka;
-              double pw = 1.0, bb = rho;
-#pragma unroll 1
-              while (kap) {
-                if (kap & 1) pw = pw * bb;
-                bb = bb * bb;
-                kap >>= 1;
-              }
-              Pt = Pt - fC * pw;
-              if (Pt < 0.0) Pt = 0.0;
-            }
-            if (fn) {
-              if (lane < 8) fr = fifo[(size_t)fh * 8 + lane];
-              fr_c = __shfl_sync(kFull, fr, 0);
-            }
-            continue;
-          }
-          break;
-        }
-      }
-      KVR_ACC(1, tl);
-
-      // 2. longest cached prefix over the input (ballot of 32 probes) on the worker's
-      // cache, and with the stale tracker (App. E, reading A29) the router's view: the
-      // same match on the mirror of the cache after query j-1-k
-      auto match_on = [&](const WorkerView<Idx> V, bool ovl, uint32_t npp) -> uint32_t {
-        uint32_t mx = 0;
-#pragma unroll 1
-        for (uint32_t base = 0; base < nq_in; base += 32) {
-          const uint32_t d = base + lane;
-          bool hit = false, check = false;
-          uint32_t sidx = 0;
-          if (d < nq_in) {
-            const uint64_t hh = Hq[d];
-            if (d < npp && Hp[d] == hh) {
-              hit = true;
-            } else {
-              const Idx s = tbl_find<Idx>(V, tmask, hh);
-              hit = s != NIL;
-              check = ovl && hit;
-              sidx = (uint32_t)s;
-            }
-          }
-          if (ovl) {   // found in the old table but evicted by the pending update?
-            const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
-            if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
-          }
-          const uint32_t bal = __ballot_sync(kFull, hit);
-          if (bal == kFull) {
-            mx = base + 32;
-            continue;
-          }
-          mx = base + (__ffs(~bal) - 1);
-          break;
-        }
-        return mx > nq_in ? nq_in : mx;
-      };
-      const uint32_t mm = match_on(S, minus_victims, np);
-      uint32_t mv = mm;
-      if (kExt && lag) mv = match_on(mirror_view<Idx>(p, w), false, 0u);
-      if (kExt && pol.tracker_grain > 1) mv = pol.tracker_grain * (mv / pol.tracker_grain);
-      KVR_ACC(2, tl);
-
-      // 3. score (Eq. 4-5, A9) on the tracker's view h~ = bt*mv (= h by default)
-      const double x = (double)(bt * mv), y = (double)(qtok - bt * mv);
-      double sc = 0.0, Ch = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0;
-      if (lbgr) {
-        Ch = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
-        h0 = divtab[mv];            // == x / 1000.0 (x = bt*m~)
-        h1 = divtab[nq_in - mv];    // == y / 1000.0 (y = bt*(n_in-m~))
-        h2 = Pt / 1000.0;
-        const double h3 = 1.0;
-        double dd = th0 * h0;
-        dd = dd + th1 * h1;
-        dd = dd + th2 * h2;
-        dd = dd + th3 * h3;
-        sc = (Ch + Pt) + dd;
-      } else if (router == KVR_ROUTE_STATIC_LINEAR) {
-        sc = (pol.w_load * (double)fn) - (pol.w_hit * (x / (double)qtok));
-      }
-      KVR_ACC(3, tl);
-      m_o = mm;
-      mview_o = mv;
-      score_o = sc;
-      Chat_o = Ch;
-      f0_o = h0;
-      f1_o = h1;
-      f2_o = h2;
-    };
 #pragma unroll 1
     for (uint32_t j = 0; j < Nrun; ++j) {
       const uint64_t g = gq + j;
@@ -1487,37 +1381,237 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       const uint32_t n_in = hd.n_in, n = hd.n_in + hd.n_out;
       const uint32_t q = bt * n_in;
 
-      // with a pending deferred apply, membership = path of that query or the old
-      // table minus that update's victims
-      const bool overlay = defer && ws->active;
-      const uint64_t* Hp = nullptr;
-      uint32_t np = 0;
-      if (overlay) {
-        const uint8_t* sp = stage + (size_t)ws->buf * p.stage_bytes;
-        Hp = reinterpret_cast<const uint64_t*>(sp + 32) +
-             (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
-        np = ws->n;
-      }
-      if (kExt && lag && j >= lag) {
-        // the tracker catches up to the caches after query j-1-k: this worker's updates
-        // of queries < j-k, in query order (ring entries live kLagRing > k+1 queries)
-        const uint32_t upto = j - lag;
-        uint32_t cur = ws->m_cur;
+      // steps 1-3 for each of this warp's workers; the chooser reuses its worker's values
+      uint32_t m_v[kV] = {}, mview_v[kV] = {};
+      double score_v[kV] = {}, Chat_v[kV] = {}, f0_v[kV] = {}, f1_v[kV] = {}, f2_v[kV] = {};
+#pragma unroll
+      for (uint32_t vi = 0; vi < kV; ++vi) {
+        if (kV > 1 && wid + vi * nwarps >= W) break;
+        KVR_BIND_WORKER(wid + vi * nwarps);
+        // ---- steps 1-3 of one query for this warp's worker ----
+        // Membership = the table, or the path Hp[0..np) (same position, same identity),
+        // minus the pending update's victims (register bitmap vbits) if minus_victims.
+        auto score_query = [&](const uint64_t* Hq, double aq, uint32_t nq_in, uint32_t qtok,
+                               const uint64_t* Hp, uint32_t np, bool minus_victims, uint32_t& m_o,
+                               uint32_t& mview_o,
+                               double& score_o, double& Chat_o, double& f0_o, double& f1_o,
+                               double& f2_o) {
+          KVR_T0(tl);
+          // 1. catch-up (A11: tick before completion before routing)
+          {
+            const double rho = pol.rho, dt = pol.delta_t_ms, inv_dt = pol_inv_dt;
+    #pragma unroll 1
+            for (;;) {
+              if (lbgr) {
+                // every tick k' with (double)k'*dt <= min(a, c) comes first (A11); (double)k'*dt
+                // is monotone in k', so find the last such k' and apply the multiplications
+                // one by one (same rounding sequence as a per-tick loop)
+                const double lim = (fn == 0 || aq < fr_c) ? aq : fr_c;
+                const double est = lim * inv_dt;   // a guess only: the loops below make it exact
+                uint64_t kk = est < 1.8e19 ? (uint64_t)est : k;
+                if (kk < k) kk = k;
+                while ((double)(kk + 1) * dt <= lim) ++kk;
+                while (kk > k && (double)kk * dt > lim) --kk;
+                if (kk > k) {
+                  if (Pt != 0.0) {
+                    uint32_t nt = (uint32_t)(kk - k);
+    #pragma unroll 1
+                    for (; nt >= 4; nt -= 4) {
+                      Pt = rho * Pt;
+                      Pt = rho * Pt;
+                      Pt = rho * Pt;
+                      Pt = rho * Pt;
+                    }
+                    for (; nt; --nt) Pt = rho * Pt;
+                  }
+                  k = kk;
+                }
+              }
+              if (fn != 0 && fr_c <= aq) {
+                // pop the front record (its fields are in fr); an emptied chunk goes to this
+                // worker's free list and the head follows the chunk link
+                const uint32_t nh = fh + 1;
+                --fn;
+                if ((nh & (kFifoChunk - 1)) == 0) {
+                  const uint32_t c0 = (nh - 1) / kFifoChunk;
+                  const uint32_t nxt = fn ? flink[c0] : 0u;
+                  __syncwarp();
+                  if (lane == 0) {
+                    flink[c0] = ws->ffree;
+                    ws->ffree = c0;
+                  }
+                  fh = fn ? nxt * kFifoChunk : nh;
+                } else {
+                  fh = nh;
+                }
+                if (lbgr) {
+                  const double fa = __shfl_sync(kFull, fr, 1), fE = __shfl_sync(kFull, fr, 2);
+                  const double g0 = __shfl_sync(kFull, fr, 3), g1 = __shfl_sync(kFull, fr, 4);
+                  const double g2 = __shfl_sync(kFull, fr, 5), fC = __shfl_sync(kFull, fr, 6);
+                  const uint64_t ka = (uint64_t)__double_as_longlong(__shfl_sync(kFull, fr, 7));
+                  const double E = fr_c - fa;
+                  const double res = E - fE;
+                  if (rls) {
+                    // OnlineUpdate, RLS reading (A8b), one weighted least-squares step in
+                    // the oracle's order (rls_step): lane 4a+b holds P[a][b]; every sum is
+                    // gathered by shuffles left to right.  pi = P phi, gamma = lam + phi'pi,
+                    // k = pi / gamma, theta += k e, P = (P - k pi') / lam.
+                    const double lam = pol.mu;
+                    double* Rg = rls_region(p, w);
+                    const uint32_t ra = (lane >> 2) & 3u, rb = lane & 3u;
+                    const double Pab = lane < 16 ? Rg[lane] : 0.0;
+                    const double phb = rb == 0 ? g0 : (rb == 1 ? g1 : (rb == 2 ? g2 : 1.0));
+                    const double prod = Pab * phb;
+                    double pi = __shfl_sync(kFull, prod, 4 * ra);
+                    pi = pi + __shfl_sync(kFull, prod, 4 * ra + 1);
+                    pi = pi + __shfl_sync(kFull, prod, 4 * ra + 2);
+                    pi = pi + __shfl_sync(kFull, prod, 4 * ra + 3);   // pi[a] in lanes 4a..4a+3
+                    double gsum = g0 * __shfl_sync(kFull, pi, 0);
+                    gsum = gsum + g1 * __shfl_sync(kFull, pi, 4);
+                    gsum = gsum + g2 * __shfl_sync(kFull, pi, 8);
+                    gsum = gsum + 1.0 * __shfl_sync(kFull, pi, 12);
+                    const double gamma = lam + gsum;
+                    const double kk = pi / gamma;                       // k[a]
+                    const double pib = __shfl_sync(kFull, pi, 4 * rb);  // pi[b]
+                    if (lane < 16) Rg[lane] = (Pab - kk * pib) / lam;
+                    th0 = th0 + __shfl_sync(kFull, kk, 0) * res;
+                    th1 = th1 + __shfl_sync(kFull, kk, 4) * res;
+                    th2 = th2 + __shfl_sync(kFull, kk, 8) * res;
+                    th3 = th3 + __shfl_sync(kFull, kk, 12) * res;
+                  } else {     // OnlineUpdate (A8): NLMS on the squared residual
+                    const double g3 = 1.0;
+                    double s = g0 * g0;
+                    s = s + g1 * g1;
+                    s = s + g2 * g2;
+                    s = s + g3 * g3;
+                    const double gstep = (pol.mu * res) / (1.0 + s);
+                    th0 = th0 + gstep * g0;
+                    th1 = th1 + gstep * g1;
+                    th2 = th2 + gstep * g2;
+                    th3 = th3 + gstep * g3;
+                  }
+                  // ReleaseLoad (A10): P~ <- max(0, P~ - C^ rho^kappa)
+                  uint64_t kap = k - ka;
+                  double pw = 1.0, bb = rho;
+    #pragma unroll 1
+                  while (kap) {
+                    if (kap & 1) pw = pw * bb;
+                    bb = bb * bb;
+                    kap >>= 1;
+                  }
+                  Pt = Pt - fC * pw;
+                  if (Pt < 0.0) Pt = 0.0;
+                }
+                if (fn) {
+                  if (lane < 8) fr = fifo[(size_t)fh * 8 + lane];
+                  fr_c = __shfl_sync(kFull, fr, 0);
+                }
+                continue;
+              }
+              break;
+            }
+          }
+          KVR_ACC(1, tl);
+
+          // 2. longest cached prefix over the input (ballot of 32 probes) on the worker's
+          // cache, and with the stale tracker (App. E, reading A29) the router's view: the
+          // same match on the mirror of the cache after query j-1-k
+          auto match_on = [&](const WorkerView<Idx> V, bool ovl, uint32_t npp) -> uint32_t {
+            uint32_t mx = 0;
+    #pragma unroll 1
+            for (uint32_t base = 0; base < nq_in; base += 32) {
+              const uint32_t d = base + lane;
+              bool hit = false, check = false;
+              uint32_t sidx = 0;
+              if (d < nq_in) {
+                const uint64_t hh = Hq[d];
+                if (d < npp && Hp[d] == hh) {
+                  hit = true;
+                } else {
+                  const Idx s = tbl_find<Idx>(V, tmask, hh);
+                  hit = s != NIL;
+                  check = ovl && hit;
+                  sidx = (uint32_t)s;
+                }
+              }
+              if (ovl) {   // found in the old table but evicted by the pending update?
+                const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
+                if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
+              }
+              const uint32_t bal = __ballot_sync(kFull, hit);
+              if (bal == kFull) {
+                mx = base + 32;
+                continue;
+              }
+              mx = base + (__ffs(~bal) - 1);
+              break;
+            }
+            return mx > nq_in ? nq_in : mx;
+          };
+          const uint32_t mm = match_on(S, minus_victims, np);
+          uint32_t mv = mm;
+          if (kExt && lag) mv = match_on(mirror_view<Idx>(p, w), false, 0u);
+          if (kExt && pol.tracker_grain > 1) mv = pol.tracker_grain * (mv / pol.tracker_grain);
+          KVR_ACC(2, tl);
+
+          // 3. score (Eq. 4-5, A9) on the tracker's view h~ = bt*mv (= h by default)
+          const double x = (double)(bt * mv), y = (double)(qtok - bt * mv);
+          double sc = 0.0, Ch = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0;
+          if (lbgr) {
+            Ch = (pol.est_alpha_cached_ms * x) + (pol.est_alpha_miss_ms * y);
+            h0 = divtab[mv];            // == x / 1000.0 (x = bt*m~)
+            h1 = divtab[nq_in - mv];    // == y / 1000.0 (y = bt*(n_in-m~))
+            h2 = Pt / 1000.0;
+            const double h3 = 1.0;
+            double dd = th0 * h0;
+            dd = dd + th1 * h1;
+            dd = dd + th2 * h2;
+            dd = dd + th3 * h3;
+            sc = (Ch + Pt) + dd;
+          } else if (router == KVR_ROUTE_STATIC_LINEAR) {
+            sc = (pol.w_load * (double)fn) - (pol.w_hit * (x / (double)qtok));
+          }
+          KVR_ACC(3, tl);
+          m_o = mm;
+          mview_o = mv;
+          score_o = sc;
+          Chat_o = Ch;
+          f0_o = h0;
+          f1_o = h1;
+          f2_o = h2;
+        };
+        // with a pending deferred apply, membership = path of that query or the old
+        // table minus that update's victims
+        const bool overlay = defer && ws->active;
+        const uint64_t* Hp = nullptr;
+        uint32_t np = 0;
+        if (overlay) {
+          const uint8_t* sp = stage + (size_t)ws->buf * p.stage_bytes;
+          Hp = reinterpret_cast<const uint64_t*>(sp + 32) +
+               (reinterpret_cast<const QueryHdr*>(sp)->block_off & 1);
+          np = ws->n;
+        }
+        if (kExt && lag && j >= lag) {
+          // the tracker catches up to the caches after query j-1-k: this worker's updates
+          // of queries < j-k, in query order (ring entries live kLagRing > k+1 queries)
+          const uint32_t upto = j - lag;
+          uint32_t cur = ws->m_cur;
 #pragma unroll 1
-        for (; cur < upto; ++cur)
-          if (lag_entry(p, cur)->worker == w) mirror_apply<Idx, kMaxThreads>(p, tr.hash, w, lane, cur);
-        __syncwarp();
-        if (lane == 0) ws->m_cur = cur;
-      }
-      uint32_t m, mview;
-      double score, Chat, f0, f1, f2;
-      score_query(H, a, n_in, q, Hp, np, overlay, m, mview, score, Chat, f0, f1, f2);
-      if (lane == 0) {
-        ctrl->score[par][w] = score;
-        ctrl->mhit[par][w] = mview;   // the router's view (THRESHOLD)
-        ctrl->npend[par][w] = fn;
-        ctrl->csize[par][w] = ws->x.size;   // cached blocks (CACHE_AWARE, A38)
-        ws->c_probes += min(m + 1, n_in);
+          for (; cur < upto; ++cur)
+            if (lag_entry(p, cur)->worker == w) mirror_apply<Idx, kMaxThreads>(p, tr.hash, w, lane, cur);
+          __syncwarp();
+          if (lane == 0) ws->m_cur = cur;
+        }
+        score_query(H, a, n_in, q, Hp, np, overlay, m_v[vi], mview_v[vi], score_v[vi], Chat_v[vi],
+                    f0_v[vi], f1_v[vi], f2_v[vi]);
+        if (lane == 0) {
+          ctrl->score[par][w] = score_v[vi];
+          ctrl->mhit[par][w] = mview_v[vi];   // the router's view (THRESHOLD)
+          ctrl->npend[par][w] = fn;
+          ctrl->csize[par][w] = ws->x.size;   // cached blocks (CACHE_AWARE, A38)
+          ws->c_probes += min(m_v[vi] + 1, n_in);
+        }
+        KVR_SAVE_WORKER();
       }
       KVR_RESET(tp);
       __syncthreads();
@@ -1593,21 +1687,40 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       KVR_ACC(5, tp);
 
       // deferred apply of this warp's previous update (overlaps others' decisions)
-      if (ws->active) {
-        apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
-        vbits = 0;
+#pragma unroll
+      for (uint32_t vi = 0; vi < kV; ++vi) {
+        if (kV > 1 && wid + vi * nwarps >= W) break;
+        const uint32_t w = wid + vi * nwarps;
+        WarpSm* ws = warp_sm(p, w);
+        if (ws->active) {
+          apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+          if constexpr (kV > 1) wsave(p, w)->vb[lane] = 0u;
+          else st0.vbits = 0;
+        }
       }
 #ifdef KVR_PHASE_PROFILE
-      if (w == best && clock64() - tp > 200) {   // an apply on the critical path
+      if (best % nwarps == wid && clock64() - tp > 200) {   // an apply on the critical path
         KVR_CNT(16, clock64() - tp);
         KVR_CNT(17, 1);
       }
 #endif
       KVR_ACC(6, tp);
 
-      if (w != best) continue;
+      if (best % nwarps != wid) continue;
 
       // ================= warp i* : UpdateCache decisions + accounting =================
+      const uint32_t vib = best / nwarps;   // which of this warp's workers (0 unless kV == 2)
+      const uint32_t m = (kV > 1 && vib) ? m_v[kV - 1] : m_v[0];
+      const double score = (kV > 1 && vib) ? score_v[kV - 1] : score_v[0];
+      const double Chat = (kV > 1 && vib) ? Chat_v[kV - 1] : Chat_v[0];
+      const double f0 = (kV > 1 && vib) ? f0_v[kV - 1] : f0_v[0];
+      const double f1 = (kV > 1 && vib) ? f1_v[kV - 1] : f1_v[0];
+      const double f2 = (kV > 1 && vib) ? f2_v[kV - 1] : f2_v[0];
+#pragma unroll 1
+      for (uint32_t once = 0; once < 1; ++once) {   // (break = leave the update early)
+      KVR_BIND_WORKER(best);
+      uint32_t* slots = slot_buf(p, j);        // [max_n] slot | evicted << 31 per miss
+      uint32_t* vmap = slots + p.max_n;        // [32] victim bitmap staging (overlay)
       __syncwarp();
       // register copy of the scalars this update changes (written back at the end);
       // counters and e_i are bumped in shared memory
@@ -1624,7 +1737,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           ctrl->status = KVR_TRIAL_RING_OVERFLOW;
           ctrl->abortf[par ^ 1] = 1;
         }
-        continue;
+        break;
       }
       // FIFO push position: the tail chunk's next record, or a new chunk (own free list
       // first, else the pool's bump counter) linked behind the tail
@@ -1639,7 +1752,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             ctrl->status = KVR_TRIAL_RING_OVERFLOW;
             ctrl->abortf[par ^ 1] = 1;
           }
-          continue;
+          break;
         }
         __syncwarp();
         if (lane == 0) {
@@ -1772,7 +1885,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         ctrl->sum_lat = ctrl->sum_lat + lat;
         ctrl->sum_ttft = ctrl->sum_ttft + ttft;
         if (lat > ctrl->max_lat) ctrl->max_lat = lat;
-        if (p.bins) ctrl->hist[hist_bin(lat, p.bins)] += 1;
+        if (hist) atomicAdd(&hist[hist_bin(lat, p.bins)], 1u);
         if (fn > ws->c_maxp) ws->c_maxp = fn;   // before any catch-up for j+1
         vc = ctrl->vcursor;
         ctrl->vcursor = vc + nev;
@@ -1796,7 +1909,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
               ws->x.ltail = wr.ltail;
             }
             __syncwarp();
-            rlt_decide_reg<Idx, kGlobal, kMaxThreads>(p, M, p0, fallback, K, w, lane, use_list);
+            rlt_decide_reg<Idx, kMem, kMaxThreads>(p, M, p0, fallback, K, w, lane, use_list, j);
             wr.size = ws->x.size;
             wr.cntT = ws->x.cntT;
             if (lane == 0) ws->x.c_evict += nev;
@@ -1833,7 +1946,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           __syncwarp();
           if (lane == 0) ws->x.size = wr.size;
           __syncwarp();
-          opt_decide<Idx, kGlobal, kMaxThreads>(p, M, kf, p0, tr.nu + hd.block_off, w, lane);
+          opt_decide<Idx, kMem, kMaxThreads>(p, M, kf, p0, tr.nu + hd.block_off, w, lane, j);
           wr.size = ws->x.size;
           if (lane == 0) ws->x.c_evict += nev;
         }
@@ -1848,7 +1961,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           // registers to hold them across the hits and accounting: slower overall)
           uint64_t lpre[kLogDepth];
           log_preload(R, wr.lhead, ltail0, lane, lpre);
-          wr.lhead = log_take(R, wr.lhead, ltail0, nev, victims, lane, lpre);
+          // the victims land in place, in slots[nfree .. M) (flagged below)
+          wr.lhead = log_take(R, wr.lhead, ltail0, nev, slots + nfree, lane, lpre);
           KVR_ACC(11, tt);
           KVR_CNT(12, wr.lhead - h0);
         }
@@ -1858,7 +1972,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           if (qq < nfree) {
             sv = size0 + qq;
           } else {
-            const uint32_t v = victims[qq - nfree];
+            const uint32_t v = slots[qq];
             sv = v | 0x80000000u;
             if (defer) atomicOr(&vmap[v >> 5], 1u << (v & 31));   // overlay bitmap
           }
@@ -1905,16 +2019,25 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       __syncwarp();
       if (!defer) {
-        apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+        apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
         vbits = 0;
       }
+      KVR_SAVE_WORKER();
+      }   // once
     }
 
     // ---- end of trial ----
     __syncthreads();   // all warps are past their last query before the final applies
-    if (ws->active) {
-      apply_update<Idx, kGlobal, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
-      vbits = 0;
+#pragma unroll
+    for (uint32_t vi = 0; vi < kV; ++vi) {
+      if (kV > 1 && wid + vi * nwarps >= W) break;
+      const uint32_t w = wid + vi * nwarps;
+      WarpSm* ws = warp_sm(p, w);
+      if (ws->active) {
+        apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
+        if constexpr (kV > 1) wsave(p, w)->vb[lane] = 0u;
+        else st0.vbits = 0;
+      }
     }
     __syncthreads();
     // drain staged-but-unconsumed queries (only after an abort)
@@ -1923,6 +2046,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       mbar_wait(&ctrl->mbar[g % kNumStages], (uint32_t)((g / kNumStages) & 1));
     }
     gq += issued;
+#pragma unroll
+    for (uint32_t vi = 0; vi < kV; ++vi) {
+      if (kV > 1 && wid + vi * nwarps >= W) break;
+      KVR_BIND_WORKER(wid + vi * nwarps);
     if (lane == 0) {
       atomicAdd(&ctrl->cnt[0], ws->c_probes);
       atomicAdd(&ctrl->cnt[1], (unsigned long long)ws->x.c_ins);
@@ -1936,6 +2063,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       atomicMax(&ctrl->cnt[9], (unsigned long long)ws->c_maxp);
       ctrl->P[w] = P;
       ctrl->F[w] = F;
+    }
     }
     __syncthreads();
     if (tid == 0) {
@@ -1970,9 +2098,6 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (trial < 4096) g_trial_cycles[trial] = clock64() - t_trial0;
 #endif
     }
-    if (p.hist)
-      for (uint32_t b = tid; b < p.bins; b += blockDim.x)
-        p.hist[(size_t)trial * p.bins + b] = ctrl->hist[b];
     if (led && Nrun) {   // distinct per phase; clean = first-appearance misses - not clean
       __threadfence_block();
       for (uint32_t v = tid; v < tr.n_phases; v += blockDim.x) {
@@ -1987,33 +2112,40 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 template <bool kExt>
 static const void* kernel_for_t(uint32_t tier, uint32_t W) {
   if (tier == 1) {
-    if (W <= 4) return (const void*)replay_kernel<uint16_t, false, 128, kExt>;
-    if (W <= 8) return (const void*)replay_kernel<uint16_t, false, 256, kExt>;
-    if (W <= 16) return (const void*)replay_kernel<uint16_t, false, 512, kExt>;
-    return (const void*)replay_kernel<uint16_t, false, 1024, kExt>;
+    if (W <= 4) return (const void*)replay_kernel<uint16_t, 0, 128, kExt>;
+    if (W <= 8) return (const void*)replay_kernel<uint16_t, 0, 256, kExt>;
+    if (W <= 16) return (const void*)replay_kernel<uint16_t, 0, 512, kExt>;
+    return (const void*)replay_kernel<uint16_t, 3, 512, kExt>;   // W > 16: two workers per warp
   }
-  if (W <= 4) return (const void*)replay_kernel<uint32_t, true, 128, kExt>;
-  if (W <= 8) return (const void*)replay_kernel<uint32_t, true, 256, kExt>;
-  if (W <= 16) return (const void*)replay_kernel<uint32_t, true, 512, kExt>;
-  if (tier == 3) return (const void*)replay_kernel<uint16_t, true, 1024, kExt>;
-  return (const void*)replay_kernel<uint32_t, true, 1024, kExt>;
+  if (tier == 4) return (const void*)replay_kernel<uint16_t, 2, 512, kExt>;   // W > 16, 2 per warp
+  if (W <= 4) return (const void*)replay_kernel<uint32_t, 1, 128, kExt>;
+  if (W <= 8) return (const void*)replay_kernel<uint32_t, 1, 256, kExt>;
+  if (W <= 16) return (const void*)replay_kernel<uint32_t, 1, 512, kExt>;
+  if (tier == 3) return (const void*)replay_kernel<uint16_t, 1, 1024, kExt>;
+  return (const void*)replay_kernel<uint32_t, 1, 1024, kExt>;
 }
 
 static const void* kernel_for(uint32_t tier, uint32_t W, bool ext) {
   return ext ? kernel_for_t<true>(tier, W) : kernel_for_t<false>(tier, W);
 }
 
+// threads per CTA: one warp per worker, two workers per warp in the split tier
+static uint32_t replay_threads(uint32_t tier, uint32_t W) {
+  return (tier == 4 || (tier == 1 && W > 16)) ? 32 * ((W + 1) / 2) : 32 * W;
+}
+
 cudaError_t replay_attrs(uint32_t tier, size_t smem, int* ctas_per_sm, uint32_t W, bool ext) {
   const void* k = kernel_for(tier, W, ext);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, 32 * W, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, replay_threads(tier, W), smem);
 }
 
 cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, size_t smem,
                           cudaStream_t s, bool ext) {
   void* args[] = {const_cast<ReplayParams*>(&p)};
-  return cudaLaunchKernel(kernel_for(tier, p.W, ext), dim3(grid), dim3(32 * p.W), args, smem, s);
+  return cudaLaunchKernel(kernel_for(tier, p.W, ext), dim3(grid), dim3(replay_threads(tier, p.W)),
+                          args, smem, s);
 }
 
 cudaError_t phase_cycles(unsigned long long* out16, int reset) {

@@ -169,3 +169,23 @@ def test_phase_ledger_validation(kvr):
         sim.run_ledger(dt.with_phases(32), np.array([1], np.uint64))
     with pytest.raises(kvr.KvrError):           # W must be 1
         kvr.Simulator(2, 64, extended_policies=True).run_ledger(dt.with_phases(64), np.array([1], np.uint64))
+
+
+# -------------------------------------------------- split tier, two workers per warp
+@pytest.mark.parametrize("W", [17, 24, 31, 32])
+def test_split_tier_two_workers_per_warp(kvr, oracle_mod, W):
+    """W > 16 runs ceil(W/2) warps of two workers (odd W leaves one warp with a single
+    worker), in the shared-memory tier when it fits (W = 17 here) and otherwise the split
+    tier (identities + tables in global memory, tree arrays / bitmaps / stamps in shared
+    memory).  Every field, record and victim equals the oracle's, lean and extended
+    policies, for the automatic tier, the forced split tier and the all-global tier 2."""
+    tr = wl.gsp(24, 10, 0.5, seed=0xE0 + W, W=W, util=1.5, lengths=(128, 256, 512))
+    sim = kvr.Simulator(W, 512)
+    assert sim.plan(tr.max_blocks)[0] == (1 if W == 17 else 3)
+    pols = [kvr.Policy(eviction=e, router=r) for e in (0, 1) for r in (0, 1, 2)]
+    keys = list(range(60, 60 + len(pols)))
+    for tier in (0, 2, 3):
+        compare(oracle_mod, kvr, tr, W, 512, pols, keys, force_tier=tier, ring=tr.n_queries)
+    ext = [kvr.Policy(eviction=1, router=6), kvr.Policy(eviction=0, tracker_lag=3),
+           kvr.Policy(eviction=1, router=5), kvr.Policy(eviction=1, rlt_fallback=2)]
+    compare(oracle_mod, kvr, tr, W, 512, ext, [70, 71, 72, 73], ring=tr.n_queries)
