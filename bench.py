@@ -41,6 +41,7 @@ METRIC = "simulated queries/sec (all replays)"
 UNIT = "query-replays/s"
 B_BLOCKS = 512
 UTIL = 0.8                                     # all-miss utilisation of the Poisson arrivals
+BATCH_SLOTS = [0]                              # --batch-slots (the oracle baseline follows it)
 
 # ---- config 5 ----
 C5_WS = (4, 8, 16, 32)
@@ -170,6 +171,7 @@ def config_json(args):
     return {"workload": "config2: W=8, B=512 blocks, 3 GSP traces (125 groups x 800 queries, "
                         "128-2048 tokens, prefix ratio 0.3/0.5/0.9), LBGR (mu=0.008) x {RLT, L-LRU}",
             "replays_per_gpu": args.trials or C2_TRIALS, "queries_per_trace": args.queries or C2_QUERIES,
+            "batch_slots": args.batch_slots,
             "block_tokens": 16, "util": UTIL, "parallelism": f"replica-sharded x{args.gpus}",
             "l2": "inputs larger than L2 (3 packed traces ~250 MB) + 256 MB L2 flush between steps"}
 
@@ -312,7 +314,8 @@ def run_oracle_sample(sample, threads):
 
     def one(s):
         W, tr, ev, key, ring = s
-        cfg = oracle.OracleConfig(W=W, capacity_blocks=B_BLOCKS, pending_ring=ring)
+        cfg = oracle.OracleConfig(W=W, capacity_blocks=B_BLOCKS, pending_ring=ring,
+                                  batch_slots=BATCH_SLOTS[0])
         r = oracle.run(cfg, tr, oracle.OraclePolicy(eviction=ev), key)
         return r.result["queries"]
 
@@ -381,6 +384,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kvr", choices=["kvr", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c5", "c2"])
+    ap.add_argument("--batch-slots", type=int, default=0,
+                    help="continuous batching (beta concurrent queries per worker; config 2 only: "
+                         "beta * L_max <= B)")
     ap.add_argument("--ref-queries", type=int, default=15000,
                     help="config 2 only: queries per oracle trial in the CPU sample")
     ap.add_argument("--ref-trials-per-thread", type=int, default=1)
@@ -392,6 +398,9 @@ def main():
     ap.add_argument("--ncu", action="store_true",
                     help="profiling run: one step, no warm-up / e2e / cpu baseline")
     args = ap.parse_args()
+    if args.batch_slots and args.workload != "c2":
+        ap.error("--batch-slots needs --workload c2 (config 5's 292-block paths exceed B / beta)")
+    BATCH_SLOTS[0] = args.batch_slots
     if args.ncu:
         args.warmup, args.steps, args.no_e2e, args.no_cpu_baseline = 0, 1, True, True
     else:
@@ -434,7 +443,7 @@ def main():
     trace_hash = 0
     for L in launches:
         dts = [DeviceTrace(t, device=dev) for t in L.traces]
-        sim = Simulator(L.W, B_BLOCKS, pending_ring=L.ring)
+        sim = Simulator(L.W, B_BLOCKS, pending_ring=L.ring, batch_slots=args.batch_slots)
         n = len(L)
         buf = sim.alloc(dts, max(1, n), 0, dev)
         if n:
@@ -614,7 +623,7 @@ def e2e_measure(launches, dev, stream, args):  # noqa: C901
     per = []
     h2d, d2h = 0, 0
     for L in launches:
-        sim = Simulator(L.W, B_BLOCKS, pending_ring=L.ring)
+        sim = Simulator(L.W, B_BLOCKS, pending_ring=L.ring, batch_slots=args.batch_slots)
         host = [DeviceTrace.pin(t) for t in L.traces]                 # pinned, outside timing
         n = len(L)
         hk = torch.from_numpy(L.keys.view(np.int64)).pin_memory()

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -127,6 +128,8 @@ kvr_status make_batch_plan(const kvr_sim* sim, uint32_t max_n, uint32_t n_trials
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
   pl->ws_aux = kvr::align16((size_t)pl->grid * c.W * c.pending_ring * sizeof(kvr::BFlight));
+  // + the Leaf-LRU recency logs (after the FIFO rings)
+  pl->ws_aux += kvr::align16((size_t)pl->grid * c.W * kvr::batch_log_cap(c.capacity_blocks, mx) * 8);
   pl->ws_fifo = 0;
   pl->ws_lag = 0;
   pl->ws_div = 0;
@@ -169,6 +172,9 @@ kvr_status make_plan(const kvr_sim* sim, uint32_t max_n, uint32_t max_N, uint32_
   cudaError_t e = kvr::replay_attrs(pl->ktier, pl->smem, &pl->ctas_per_sm, c.W, sim_extended(c));
   if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
   if (pl->ctas_per_sm < 1) return fail(KVR_ERR_UNSUPPORTED, "replay kernel cannot be resident");
+  // experiment knob (scripts only): cap the resident trials per SM
+  if (const char* cap = getenv("KVR_MAX_CTAS_PER_SM"))
+    if (atoi(cap) > 0) pl->ctas_per_sm = std::min(pl->ctas_per_sm, atoi(cap));
   const uint64_t slots = (uint64_t)pl->ctas_per_sm * (uint64_t)num_sms();
   pl->grid = (uint32_t)std::min<uint64_t>(std::max<uint32_t>(n_trials, 1), slots);
   const bool ext = sim_extended(c);
@@ -530,6 +536,9 @@ kvr_status run_impl(kvr_sim* sim, uint32_t n_traces, const kvr_trace* const* tra
     p.beta = c.batch_slots;
     p.blay = pl.blay;
     p.bglobal = pl.tier == 2 ? 1u : 0u;
+    p.blog_cap = kvr::batch_log_cap(c.capacity_blocks, std::max<uint32_t>(max_n, 1));
+    p.blog_base = reinterpret_cast<uint64_t*>(
+        ws + 256 + kvr::align16((size_t)pl.grid * c.W * c.pending_ring * sizeof(kvr::BFlight)));
     p.gstate = pl.tier == 2 ? ws + 256 + pl.ws_aux : nullptr;
     e = kvr::launch_batch(p, pl.grid, pl.smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "batching replay launch");

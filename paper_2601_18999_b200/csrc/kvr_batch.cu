@@ -183,6 +183,7 @@ struct __align__(16) BCtrl {
 // Per-warp (worker) scalar state: warp-uniform registers.
 struct BW {
   uint32_t size, cntT, nfl, wh, wn;
+  uint32_t lhead, ltail;   // Leaf-LRU recency log cursors (first maybe-valid entry, end)
   uint64_t e, k, vcur;
   double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
   // counters, u32 in registers and flushed into the worker's u64 accumulators in shared
@@ -208,7 +209,28 @@ struct BTrial {
   BFlight* ring;
   uint32_t ringcap;
   BCtrl* ctrl;
+  uint64_t* log;      // this worker's recency log (Leaf-LRU trials)
+  uint32_t lmask;
 };
+
+// in-place order-preserving compaction of the recency log [head, tail): keeps the
+// entries whose stamp is still the node's (pinned or not); returns the new tail
+template <typename Idx>
+__device__ __forceinline__ uint32_t blog_compact(const BTrial& T, const BView<Idx>& S, uint32_t head,
+                                                 uint32_t tail) {
+  uint32_t w = head;
+  for (uint32_t r = head; r < tail; r += 32) {
+    const uint32_t idx = r + T.lane;
+    const uint64_t e = idx < tail ? T.log[idx & T.lmask] : 0ull;
+    const bool v = idx < tail && S.stamp[(uint32_t)e] == (uint32_t)(e >> 32);
+    const uint32_t bal = __ballot_sync(kFull, v);
+    __syncwarp();   // every read of this window precedes the writes (they land below r + 32)
+    if (v) T.log[(w + __popc(bal & ((1u << T.lane) - 1u))) & T.lmask] = e;
+    w += __popc(bal);
+    __syncwarp();
+  }
+  return w;
+}
 
 __device__ __forceinline__ bool bit_test(const uint32_t* bm, uint32_t s) {
   return (bm[s >> 5] >> (s & 31)) & 1u;
@@ -264,6 +286,43 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   bool hitrun = true;   // hits are a prefix of Gamma (prefix closure)
   uint32_t nv = 0;
   uint64_t V = 0;
+  const bool lru = !T.rlt;
+  if (lru && x.ltail - x.lhead + n > T.lmask + 1) x.ltail = blog_compact(T, S, x.lhead, x.ltail);
+  // Leaf-LRU victims (A33) = the unpinned nodes in recency-log order (stamp, -depth)
+  // from the head: the minimum over the unpinned nodes is always a leaf, and the
+  // nodes this update loads are pinned, so the e victims of a miss run are the e
+  // first unpinned valid entries.  The head only moves past entries
+  // that are no longer valid.
+  uint32_t lpos = x.lhead, cm = 0;
+  uint64_t le = 0;
+  bool lwin = false, headfix = false;
+  auto lru_take = [&]() -> uint32_t {
+    for (;;) {
+      if (cm == 0) {
+        if (lwin) lpos += 32;
+        if (lpos >= x.ltail) return kNone;
+        const uint32_t idx = lpos + lane;
+        le = idx < x.ltail ? T.log[idx & T.lmask] : 0ull;
+        const uint32_t sl = (uint32_t)le;
+        const bool valid = idx < x.ltail && S.stamp[sl] == (uint32_t)(le >> 32);
+        const uint32_t vb = __ballot_sync(kFull, valid);
+        cm = __ballot_sync(kFull, valid && S.pin[sl] == 0);
+        if (!headfix) {
+          if (vb) {
+            x.lhead = lpos + (__ffs(vb) - 1);
+            headfix = true;
+          } else {
+            x.lhead = min(lpos + 32, x.ltail);
+          }
+        }
+        lwin = true;
+        continue;
+      }
+      const uint32_t L = __ffs(cm) - 1;
+      cm &= cm - 1;
+      return __shfl_sync(kFull, (uint32_t)le, L);
+    }
+  };
   // Lane-parallel hit run: 32 blocks per step, each lane looks up its own block; the
   // leading hits are refreshed, pinned and (RLT) marked at once when no |T| = B+1
   // reset can fall inside the step, else the step is left to the serial loop below.
@@ -282,6 +341,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     }
     if (hit) {
       S.stamp[sl] = j;
+      S.gam[q] = sl;   // block q's slot (recency log)
       const uint32_t pv = S.pin[sl];
       S.pin[sl] = (uint8_t)(pv + 1);
       if (pv == 0) atomicAnd(&S.leafu[sl >> 5], ~(1u << (sl & 31)));
@@ -305,6 +365,10 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   const uint32_t d_miss0 = hitrun ? n : d;   // first block known to miss (if any)
   uint32_t d_ins0 = n;                       // first block whose insert is deferred
   int32_t nU_known = -1;                     // |U| when known, -1 = recount
+  // B <= 1024: U's words in registers (lane l: word l) with their inclusive prefix
+  // counts, valid whenever nU_known >= 0 (reloaded at every recount)
+  const bool regu = T.nwords <= 32;
+  uint32_t uw = 0, uincl = 0;
   uint64_t rbatch = 0, rbase = 0;            // draws for counters rbase .. rbase+31
   bool rvalid = false;
   for (; d < n; ++d) {
@@ -329,8 +393,10 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       }
     }
     if (s != kNone) {   // hit (Alg. 1 l.10-11): refresh, pin (an unpinned leaf stops being a candidate)
+      __syncwarp();
       if (lane == 0) {
         S.stamp[s] = j;
+        S.gam[d] = s;
         const uint32_t pv = S.pin[s];
         S.pin[s] = (uint8_t)(pv + 1);
         if (pv == 0) S.leafu[s >> 5] &= ~(1u << (s & 31));
@@ -345,11 +411,30 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     if (x.size == B) {
       // choose the victim among unpinned leaves (A30, A33): LEAFU bitmap
       uint32_t v = kNone;
-      bool use_lru = !T.rlt;
+      bool use_lru = false;    // the LRU_MARKED fallback of RLT (A5): least unpinned leaf
       bool via_u = false;      // v drawn from U = LEAFU \ T (the incremental count applies)
+      if (lru) v = lru_take();
       if (T.rlt) {
         bool mark_ok = true;
-        uint32_t nU = nU_known >= 0 ? (uint32_t)nU_known : cand_count(S, T, true);
+        uint32_t nU;
+        if (nU_known >= 0) {
+          nU = (uint32_t)nU_known;
+        } else if (regu) {   // (re)load U = LEAFU & ~MARK into registers, word l on lane l
+          uw = lane < T.nwords ? (S.leafu[lane] & ~S.markb[lane]) : 0u;
+          const uint32_t c = __popc(uw);
+          const uint32_t le = lane == 31 ? kFull : (2u << lane) - 1u;
+          uint32_t tot = 0, inc = 0;
+#pragma unroll
+          for (int b = 0; b < 6; ++b) {   // bit-sliced prefix sums of the per-lane counts
+            const uint32_t bal = __ballot_sync(kFull, (c >> b) & 1u);
+            tot += (uint32_t)__popc(bal) << b;
+            inc += (uint32_t)__popc(bal & le) << b;
+          }
+          uincl = inc;
+          nU = tot;
+        } else {
+          nU = cand_count(S, T, true);
+        }
         if (nU == 0) {   // A5: U empty
           x.c[5]++;
           mark_ok = false;
@@ -374,7 +459,19 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
           const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
           x.e++;
           x.c[3]++;
-          v = cand_select(S, T, mark_ok, (uint32_t)pick_index(r, nU));
+          const uint32_t idx = (uint32_t)pick_index(r, nU);
+          if (mark_ok && regu) {
+            // owner word: first lane whose inclusive count exceeds idx; the bit inside
+            // it: the first lane l with popc(word & lanes <= l) > rem
+            const uint32_t owner = __reduce_min_sync(kFull, uincl > idx ? lane : 32u);
+            const uint32_t ou = __shfl_sync(kFull, uw, owner);
+            const uint32_t rem = idx - (__shfl_sync(kFull, uincl, owner) - (uint32_t)__popc(ou));
+            const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;
+            const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
+            v = owner * 32 + bit;
+          } else {
+            v = cand_select(S, T, mark_ok, idx);
+          }
           via_u = mark_ok;
           if (mark_ok) nU_known = (int32_t)nU;
         }
@@ -402,7 +499,20 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       const bool has_pa = pa != BView<Idx>::NIL;
       const uint32_t nc = has_pa ? S.nchild[pa] - 1u : 1u;
       const bool pa_leafu = has_pa && nc == 0 && S.pin[pa] == 0;   // parent joins LEAFU
-      if (via_u) nU_known = nU_known - 1 + ((pa_leafu && !bit_test(S.markb, pa)) ? 1 : 0);
+      if (via_u) {
+        const bool join = pa_leafu && !bit_test(S.markb, pa);   // the parent joins U
+        nU_known = nU_known - 1 + (join ? 1 : 0);
+        if (regu) {   // U loses v, maybe gains pa
+          const uint32_t vw = v >> 5;
+          if (lane == vw) uw &= ~(1u << (v & 31));
+          if (lane >= vw) --uincl;
+          if (join) {
+            const uint32_t pw = pa >> 5;
+            if (lane == pw) uw |= 1u << (pa & 31);
+            if (lane >= pw) ++uincl;
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) {
         t_erase(S, hv, v);
@@ -452,6 +562,12 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     t_insert_cas(S, S.key[slot], slot);
   }
   __syncwarp();
+  if (lru) {   // the path, deepest first, at stamp j (it was compacted to fit)
+    for (uint32_t q = lane; q < n; q += 32)
+      T.log[(x.ltail + (n - 1 - q)) & T.lmask] = ((uint64_t)j << 32) | (uint32_t)S.gam[q];
+    x.ltail += n;
+    __syncwarp();
+  }
   *nvict = nv;
   *Vout = V;
   return m;
@@ -700,6 +816,8 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     T.ringcap = p.ring;
     T.ring = reinterpret_cast<BFlight*>(p.aux_base) + (size_t)blockIdx.x * W * p.ring;
     T.ctrl = ctrl;
+    T.log = p.blog_base + ((size_t)blockIdx.x * W + w) * p.blog_cap;
+    T.lmask = p.blog_cap - 1;
     const uint32_t N = T.tr.N;
 
     // a per-trial policy from device memory is validated here (A36)
@@ -716,6 +834,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     __syncwarp();
     BW x;
     x.size = 0; x.cntT = 0; x.nfl = 0; x.wh = 0; x.wn = 0;
+    x.lhead = 0; x.ltail = 0;
     x.e = 0; x.k = 0; x.vcur = 0;
     x.Pt = 0.0; x.P = 0.0; x.F = 0.0; x.slat = 0.0; x.sttft = 0.0; x.mlat = 0.0;
     x.th0 = pol.theta0[0]; x.th1 = pol.theta0[1]; x.th2 = pol.theta0[2]; x.th3 = pol.theta0[3];

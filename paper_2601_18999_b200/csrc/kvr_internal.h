@@ -73,8 +73,9 @@ __host__ __device__ inline bool policy_valid(const kvr_policy& p) {
 // LEAF / MARK bitmaps (RLT's marking set T is exactly the MARK bits, T in S).
 struct WorkerLayout {
   uint32_t B, T, nwords, idx_bytes;
+  uint32_t rebuild_at, _pad;   // rebuild the table when live + tombstones exceed this
   size_t off_key, off_parent, off_nchild, off_table, off_leaf, off_mark, off_stamp, bytes;
-  // split layout (kernel tier 4): identity + table in global memory (gbytes per worker,
+  // split layout (kernel tier 4): identities + table in global memory (gbytes per worker,
   // offsets from the global base), tree arrays / bitmaps / stamps in shared memory
   // (sbytes per worker, offsets from the shared base); unsplit: gbytes = sbytes = bytes
   size_t gbytes, sbytes;
@@ -88,7 +89,11 @@ inline WorkerLayout make_layout(uint32_t B, uint32_t idx_bytes, bool split = fal
   L.T = T;
   L.nwords = (B + 31) / 32;
   L.idx_bytes = idx_bytes;
+  L.rebuild_at = T >> 1;
   if (split) {
+    // (measured: the table on chip at half the size, T = 2B rebuilt at 3T/4, costs more
+    // in longer probe chains against the L2-resident identities than it saves: 10.5 ->
+    // 8.1 M query-replays/s at W = 32, so it stays in global memory at T = 4B)
     size_t g = 0, o = 0;
     L.off_key = g;    g = align16(g + (size_t)B * 8);
     L.off_table = g;  g = align16(g + (size_t)T * idx_bytes);
@@ -312,10 +317,20 @@ struct ReplayParams {
   // batching kernel only (kvr_batch.cu)
   uint32_t beta, bglobal;        // batch slots; per-worker state in gstate (1) or smem (0)
   BatchLayout blay;              // aux_base = [grid][W][ring] BFlight waiting FIFOs
+  uint64_t* blog_base;           // [grid][W][blog_cap] Leaf-LRU recency logs (stamp << 32 | slot)
+  uint32_t blog_cap, _pad3;
 };
 
 // exact table (bt * k) / 1000.0 for k = 0..max_n (the A9 feature scaling of integer token counts)
 inline size_t divtab_bytes(uint32_t max_n) { return align16(8 * ((size_t)max_n + 1)); }
+
+// Leaf-LRU recency log of the batching engine: one valid entry per cached node, 2x
+// headroom (compacted in place when full)
+inline uint32_t batch_log_cap(uint32_t B, uint32_t max_n) {
+  uint32_t C = 64;
+  while (C < 2 * (B + max_n + 32)) C <<= 1;
+  return C;
+}
 
 inline size_t smem_base_bytes(uint32_t W, uint32_t max_n) {
   return ctrl_bytes() + kNumStages * stage_bytes(max_n) + (size_t)W * scratch_bytes(max_n) +

@@ -971,7 +971,7 @@ __device__ __noinline__ void mirror_apply(const ReplayParams& p, const uint64_t*
   }
   uint32_t used = ws->m_used + add - sub;
   const uint32_t size = ws->m_size + fresh;
-  if (used > (p.lay.T >> 1)) {
+  if (used > p.lay.rebuild_at) {
     tbl_rebuild<Idx>(V, p.lay.T, size, lane);
     used = size;
   }
@@ -1077,7 +1077,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     KVR_ACC(31, t_ap);   // table inserts
   }
   uint32_t used = ws->x.used + used_add - used_sub;   // live + tombstone table entries
-  if (used > (p.lay.T >> 1)) {
+  if (used > p.lay.rebuild_at) {
     tbl_rebuild<Idx>(S, p.lay.T, ws->x.size, lane);
     used = ws->x.size;
   }
