@@ -1363,6 +1363,13 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     __syncthreads();
 
     uint32_t consumed = 0;
+    // two workers per warp: the warp that updated the previous query's chosen worker scores
+    // only that worker for the next query; its other workers move to the following warps
+    // (one each), so the chooser's critical path carries one worker's catch-up / match /
+    // score, not two.  pb / pcw: the previous chosen worker and the warp that updated it
+    // (identical in every warp)
+    constexpr uint32_t kL = kV > 1 ? 3u : 1u;   // workers a warp may score in one query
+    uint32_t pb = 0xffffffffu, pcw = 0xffffffffu;
 
     const double pol_inv_dt = 1.0 / pol.delta_t_ms;
 #pragma unroll 1
@@ -1381,13 +1388,42 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       const uint32_t n_in = hd.n_in, n = hd.n_in + hd.n_out;
       const uint32_t q = bt * n_in;
 
-      // steps 1-3 for each of this warp's workers; the chooser reuses its worker's values
-      uint32_t m_v[kV] = {}, mview_v[kV] = {};
-      double score_v[kV] = {}, Chat_v[kV] = {}, f0_v[kV] = {}, f1_v[kV] = {}, f2_v[kV] = {};
+      // this query's workers of this warp (kV == 1: its own; kV == 2: see pb / pcw)
+      uint32_t wl[kL];
+      if constexpr (kV == 1) {
+        wl[0] = wid;
+      } else {
+        const uint32_t NONE = 0xffffffffu;
 #pragma unroll
-      for (uint32_t vi = 0; vi < kV; ++vi) {
-        if (kV > 1 && wid + vi * nwarps >= W) break;
-        KVR_BIND_WORKER(wid + vi * nwarps);
+        for (uint32_t li = 0; li < kL; ++li) wl[li] = NONE;
+        if (pb == NONE) {
+          wl[0] = wid;
+          wl[1] = wid + nwarps < W ? wid + nwarps : NONE;
+        } else if (wid == pcw) {
+          wl[0] = pb;
+        } else {
+          const uint32_t o0 = wid, o1 = wid + nwarps;
+          wl[0] = o0 == pb ? NONE : o0;
+          wl[1] = (o1 >= W || o1 == pb) ? NONE : o1;
+          // pcw's own workers other than pb, the k-th one to warp pcw + 1 + k
+          uint32_t k = 0;
+#pragma unroll
+          for (uint32_t r = 0; r < 2; ++r) {
+            const uint32_t x = pcw + r * nwarps;
+            if (x < W && x != pb) {
+              if ((pcw + 1 + k) % nwarps == wid) wl[2] = x;
+              ++k;
+            }
+          }
+        }
+      }
+      // steps 1-3 for each of those workers; the chooser reuses its worker's values
+      uint32_t m_v[kL] = {}, mview_v[kL] = {};
+      double score_v[kL] = {}, Chat_v[kL] = {}, f0_v[kL] = {}, f1_v[kL] = {}, f2_v[kL] = {};
+#pragma unroll
+      for (uint32_t vi = 0; vi < kL; ++vi) {
+        if (kV > 1 && wl[vi] == 0xffffffffu) continue;
+        KVR_BIND_WORKER(wl[vi]);
         // ---- steps 1-3 of one query for this warp's worker ----
         // Membership = the table, or the path Hp[0..np) (same position, same identity),
         // minus the pending update's victims (register bitmap vbits) if minus_victims.
@@ -1686,11 +1722,12 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       }
       KVR_ACC(5, tp);
 
-      // deferred apply of this warp's previous update (overlaps others' decisions)
+      // deferred apply of the previous update of a worker this warp scored (overlaps the
+      // other warps' decisions)
 #pragma unroll
-      for (uint32_t vi = 0; vi < kV; ++vi) {
-        if (kV > 1 && wid + vi * nwarps >= W) break;
-        const uint32_t w = wid + vi * nwarps;
+      for (uint32_t vi = 0; vi < kL; ++vi) {
+        if (kV > 1 && wl[vi] == 0xffffffffu) continue;
+        const uint32_t w = wl[vi];
         WarpSm* ws = warp_sm(p, w);
         if (ws->active) {
           apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
@@ -1698,24 +1735,54 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           else st0.vbits = 0;
         }
       }
+      uint32_t vib = 0xffffffffu;   // position of the chosen worker in this warp's list
+#pragma unroll
+      for (uint32_t vi = 0; vi < kL; ++vi)
+        if (wl[vi] == best) vib = vi;
+      if constexpr (kV > 1) {   // every warp tracks who updates the chosen worker
+        uint32_t cw = 0xffffffffu;
+        if (pb == 0xffffffffu) {
+          cw = best % nwarps;
+        } else if (best == pb) {
+          cw = pcw;
+        } else if (best % nwarps != pcw) {
+          cw = best % nwarps;
+        } else {   // a worker of pcw moved to the following warps
+          uint32_t k = 0;
+          for (uint32_t r = 0; r < 2; ++r) {
+            const uint32_t x = pcw + r * nwarps;
+            if (x < W && x != pb) {
+              if (x == best) cw = (pcw + 1 + k) % nwarps;
+              ++k;
+            }
+          }
+        }
+        pb = best;
+        pcw = cw;
+      }
 #ifdef KVR_PHASE_PROFILE
-      if (best % nwarps == wid && clock64() - tp > 200) {   // an apply on the critical path
+      if (vib != 0xffffffffu && clock64() - tp > 200) {   // an apply on the critical path
         KVR_CNT(16, clock64() - tp);
         KVR_CNT(17, 1);
       }
 #endif
       KVR_ACC(6, tp);
 
-      if (best % nwarps != wid) continue;
+      if (vib == 0xffffffffu) continue;
 
       // ================= warp i* : UpdateCache decisions + accounting =================
-      const uint32_t vib = best / nwarps;   // which of this warp's workers (0 unless kV == 2)
-      const uint32_t m = (kV > 1 && vib) ? m_v[kV - 1] : m_v[0];
-      const double score = (kV > 1 && vib) ? score_v[kV - 1] : score_v[0];
-      const double Chat = (kV > 1 && vib) ? Chat_v[kV - 1] : Chat_v[0];
-      const double f0 = (kV > 1 && vib) ? f0_v[kV - 1] : f0_v[0];
-      const double f1 = (kV > 1 && vib) ? f1_v[kV - 1] : f1_v[0];
-      const double f2 = (kV > 1 && vib) ? f2_v[kV - 1] : f2_v[0];
+      uint32_t m = m_v[0];
+      double score = score_v[0], Chat = Chat_v[0], f0 = f0_v[0], f1 = f1_v[0], f2 = f2_v[0];
+#pragma unroll
+      for (uint32_t vi = 1; vi < kL; ++vi)
+        if (vib == vi) {
+          m = m_v[vi];
+          score = score_v[vi];
+          Chat = Chat_v[vi];
+          f0 = f0_v[vi];
+          f1 = f1_v[vi];
+          f2 = f2_v[vi];
+        }
 #pragma unroll 1
       for (uint32_t once = 0; once < 1; ++once) {   // (break = leave the update early)
       KVR_BIND_WORKER(best);
