@@ -369,6 +369,66 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   // counts, valid whenever nU_known >= 0 (reloaded at every recount)
   const bool regu = T.nwords <= 32;
   uint32_t uw = 0, uincl = 0;
+  if (lru && !hitrun && d < n) {
+    // Leaf-LRU miss run, 32 misses per step: the first B - size take free slots, the rest
+    // the next unpinned entries of the recency log (in order, one per evicting lane);
+    // victims' table entries are erased by lane 0 (backward shift is serial), every other
+    // write is lane-parallel.  Leaf-LRU keeps no tree (parents, child counts and the
+    // LEAFU / MARK bitmaps serve RLT only).
+    const uint32_t M = n - d, nfree = min(M, B - x.size);
+    d_ins0 = d;
+    for (uint32_t cb = 0; cb < M; cb += 32) {
+      const uint32_t q = cb + lane;
+      const bool act = q < M;
+      const bool ev = act && q >= nfree;
+      const uint32_t evb = __ballot_sync(kFull, ev);
+      uint32_t v = kNone;
+      for (uint32_t rest = evb; rest; rest &= rest - 1) {
+        const uint32_t t = lru_take();
+        if (t == kNone) return kNone;   // every node is in flight
+        if (lane == (uint32_t)(__ffs(rest) - 1)) v = t;
+      }
+      const uint32_t slot = ev ? v : x.size + q;
+      uint64_t hv = 0;
+      if (ev) {
+        hv = S.key[v];
+        const uint64_t k = nv + (q - max(cb, nfree));   // index of this victim in the update
+        V ^= fmix64(hv ^ ((k + 1) * kPosMul));
+        if (T.vlog) {
+          if (x.vcur + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + x.vcur + k] = hv;
+          else x.c[11] = 1;
+        }
+      }
+      __syncwarp();
+      // victims leave the table first (their slots are reloaded just below)
+      for (uint32_t rest = evb; rest; rest &= rest - 1) {
+        const uint32_t L = __ffs(rest) - 1;
+        const uint64_t h = __shfl_sync(kFull, hv, L);
+        const uint32_t vv = __shfl_sync(kFull, v, L);
+        if (lane == 0) t_erase(S, h, vv);
+      }
+      __syncwarp();
+      if (act) {   // Load(S, t): pinned, stamped at j; the table insert is deferred
+        const uint32_t dd = d + q;
+        S.key[slot] = S.gam[dd];
+        S.stamp[slot] = j;
+        S.depth[slot] = (Idx)(dd + 1);
+        S.pin[slot] = 1;
+        S.gam[dd] = slot;
+      }
+      const uint32_t ne = __popc(evb);
+      nv += ne;
+      __syncwarp();
+    }
+    x.c[11] = __reduce_or_sync(kFull, x.c[11]);
+    x.c[1] += M;
+    x.c[2] += nv;
+    x.vcur += nv;
+    x.size += nfree;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+    d = n;   // the serial loop below has nothing left
+  }
   uint64_t rbatch = 0, rbase = 0;            // draws for counters rbase .. rbase+31
   bool rvalid = false;
   for (; d < n; ++d) {
