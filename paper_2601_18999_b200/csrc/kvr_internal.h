@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <algorithm>
 #include <stdint.h>
 
 #include "kvr.h"
@@ -140,7 +141,8 @@ inline AuxLayout make_aux(uint32_t B, uint32_t max_n, uint32_t T, bool ext) {
   A.log_cap = C;
   A.T = T;
   size_t o = 0;
-  A.off_log = o;   o = align16(o + (size_t)C * 8);
+  // u32 entries (stamp << 16 | slot); OPT reuses the region for its u64 per-slot keys
+  A.off_log = o;   o = align16(o + std::max((size_t)C * 4, (size_t)B * 8));
   A.off_rls = o;   o = align16(o + 16 * 8);
   A.off_mkey = o;  o = align16(o + (ext ? (size_t)B * 8 : 0));
   A.off_mtab = o;  o = align16(o + (ext ? (size_t)T * 4 : 0));

@@ -229,7 +229,7 @@ __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
 constexpr int kLogDepth = 4;   // log windows (32 entries each) kept in flight
 
 struct RecencyLog {
-  uint64_t* log;
+  uint32_t* log;     // entries stamp << 16 | slot (u16 stamps, slots < 65536)
   uint16_t* stamp;   // per slot, in the worker state (shared memory in tier 1)
   uint32_t cap_mask;
 };
@@ -239,18 +239,18 @@ struct RecencyLog {
 // the first kLogDepth windows from `head` (entries are validated against the stamps
 // at take time)
 __device__ __forceinline__ void log_preload(const RecencyLog& R, uint32_t head, uint32_t tail,
-                                            uint32_t lane, uint64_t (&e)[kLogDepth]) {
+                                            uint32_t lane, uint32_t (&e)[kLogDepth]) {
 #pragma unroll
   for (int i = 0; i < kLogDepth; ++i) {
     const uint32_t idx = head + 32u * i + lane;
-    e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
+    e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0u;
   }
 }
 
 // e: log_preload(R, head, tail, ...) (the log between head and tail unchanged since)
 __device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head, uint32_t tail,
                                           uint32_t need, uint32_t* out, uint32_t lane,
-                                          uint64_t (&e)[kLogDepth]) {
+                                          uint32_t (&e)[kLogDepth]) {
   uint32_t k = 0, pos = head;
   // software pipeline: kLogDepth windows of entries are in flight while one is filtered
 #pragma unroll 1
@@ -262,8 +262,8 @@ __device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head,
         return pos;
       }
       const bool act = pos + lane < tail;
-      const uint32_t slot = (uint32_t)e[i];
-      const bool valid = act && R.stamp[slot] == (uint16_t)(e[i] >> 32);
+      const uint32_t slot = e[i] & 0xffffu;
+      const bool valid = act && R.stamp[slot] == (uint16_t)(e[i] >> 16);
       const uint32_t bal = __ballot_sync(kFull, valid);
       const uint32_t take = min((uint32_t)__popc(bal), need - k);
       const uint32_t rank = __popc(bal & lanemask_lt(lane));
@@ -273,7 +273,7 @@ __device__ __forceinline__ uint32_t log_take(const RecencyLog& R, uint32_t head,
         pos += select_bit(bal, take - 1) + 1u;   // through the last victim
       } else {
         const uint32_t idx = pos + 32u * kLogDepth + lane;
-        e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
+        e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0u;
         pos += 32u;
       }
     }
@@ -287,10 +287,10 @@ __device__ __forceinline__ uint32_t log_first_valid(const RecencyLog& R, uint32_
   for (;; head += 32) {
     const uint32_t idx = head + lane;
     const bool act = idx < tail;
-    const uint64_t ent = act ? R.log[idx & R.cap_mask] : 0ull;
-    const bool valid = act && R.stamp[(uint32_t)ent] == (uint16_t)(ent >> 32);
+    const uint32_t ent = act ? R.log[idx & R.cap_mask] : 0u;
+    const bool valid = act && R.stamp[ent & 0xffffu] == (uint16_t)(ent >> 16);
     const uint32_t bal = __ballot_sync(kFull, valid);
-    if (bal) return (uint32_t)__shfl_sync(kFull, (uint32_t)ent, __ffs(bal) - 1);
+    if (bal) return __shfl_sync(kFull, ent, __ffs(bal) - 1) & 0xffffu;
   }
 }
 
@@ -303,16 +303,16 @@ __device__ __forceinline__ uint32_t log_compact(const RecencyLog& R, uint32_t he
   uint32_t w = head;
 #pragma unroll 1
   for (uint32_t r = head; r < tail; r += 32u * kLogDepth) {
-    uint64_t e[kLogDepth];
+    uint32_t e[kLogDepth];
     bool v[kLogDepth];
 #pragma unroll
     for (int i = 0; i < kLogDepth; ++i) {
       const uint32_t idx = r + 32u * i + lane;
-      e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0ull;
+      e[i] = idx < tail ? R.log[idx & R.cap_mask] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kLogDepth; ++i)
-      v[i] = (r + 32u * i + lane < tail) && R.stamp[(uint32_t)e[i]] == (uint16_t)(e[i] >> 32);
+      v[i] = (r + 32u * i + lane < tail) && R.stamp[e[i] & 0xffffu] == (uint16_t)(e[i] >> 16);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < kLogDepth; ++i) {
@@ -569,7 +569,7 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
   uint8_t* sb = worker_sbase<kMem>(p_, worker);
   const WorkerView<Idx> S = make_view<Idx>(wb, sb, p_.lay);
   RecencyLog R;
-  R.log = reinterpret_cast<uint64_t*>(p_.aux_base + ((size_t)blockIdx.x * p_.W + worker) * p_.aux.bytes +
+  R.log = reinterpret_cast<uint32_t*>(p_.aux_base + ((size_t)blockIdx.x * p_.W + worker) * p_.aux.bytes +
                                       p_.aux.off_log);
   R.stamp = reinterpret_cast<uint16_t*>(sb + p_.lay.off_stamp);
   R.cap_mask = p_.aux.log_cap - 1;
@@ -592,6 +592,25 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
   const uint64_t rb_in = ws->x_rbuf[lane];
   uint32_t rlo = (uint32_t)rb_in, rhi = (uint32_t)(rb_in >> 32);
   uint32_t ri = ws->x_ri, vbits = 0, p = (uint32_t)p0;
+  // The next batch of 32 draws (counters base + 32 + lane), computed at entry where the
+  // Philox rounds overlap the bitmap loads and the first recount, when this update may
+  // run past the current batch (at most M draws); a batch exhausted in the fast segment
+  // is then replaced without leaving it.  (ri == 32: no current batch; it is computed
+  // the same way.)  The counters are those a refill would use, so results are unchanged.
+  uint32_t nlo = 0, nhi = 0;
+  bool nready = false;
+  if (wr.size + M > B && M > 32u - ri) {
+    const uint64_t r = philox_r64(K, (wr.e - (ri == 32 ? 0u : ri)) + (ri == 32 ? 0u : 32u) + lane, worker, 1u);
+    if (ri == 32) {
+      rlo = (uint32_t)r;
+      rhi = (uint32_t)(r >> 32);
+      ri = 0;
+    } else {
+      nlo = (uint32_t)r;
+      nhi = (uint32_t)(r >> 32);
+      nready = true;
+    }
+  }
   RegBits rb;
   rb.load(S.leaf, S.mark, nwords, lane);
   const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;   // lanes <= lane
@@ -604,7 +623,7 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
     // (victims are old nodes, so their parents are never the excluded p; the new
     // node's parent p is the previous new node, marked, hence outside U)
     if (q > 0 && wr.size == B && !dirty && wr.cntT < B && total > 0 && ri < 32) {
-      const uint32_t lim = min(M, min(q + (B - wr.cntT), q + (32u - ri)));
+      const uint32_t lim = min(M, min(q + (B - wr.cntT), q + (32u - ri) + (nready ? 32u : 0u)));
       KVR_T0(tfast);
       KVR_CNT(26, 0u - q);
       uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
@@ -613,6 +632,12 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
         ++wr.cntT;
         ++ri;
         const uint32_t idx = pick32(dlo, dhi, total);
+        if (ri == 32 && nready) {   // the prefetched batch takes over
+          rlo = nlo;
+          rhi = nhi;
+          ri = 0;
+          nready = false;
+        }
         // the next draw's broadcast is off the chain (lane 0 when this was the last)
         dlo = __shfl_sync(kFull, rlo, ri & 31);
         dhi = __shfl_sync(kFull, rhi, ri & 31);
@@ -704,9 +729,15 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
       uint32_t v;
       if (!generic) {
         if (ri == 32) {   // 32 counter-based draws e .. e+31, one per lane
-          const uint64_t r = philox_refill(K, wr.e + lane, worker);
-          rlo = (uint32_t)r;
-          rhi = (uint32_t)(r >> 32);
+          if (nready) {
+            rlo = nlo;
+            rhi = nhi;
+            nready = false;
+          } else {
+            const uint64_t r = philox_refill(K, wr.e + lane, worker);
+            rlo = (uint32_t)r;
+            rhi = (uint32_t)(r >> 32);
+          }
           ri = 0;
         }
         const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
@@ -748,9 +779,15 @@ __device__ __noinline__ void rlt_decide_reg(const ReplayParams& p_, uint32_t M, 
         bool vmarked;
         if (fallback == KVR_RLT_UNIFORM_LEAF) {   // uniform over leaves != p, marks ignored
           if (ri == 32) {
-            const uint64_t r = philox_refill(K, wr.e + lane, worker);
-            rlo = (uint32_t)r;
-            rhi = (uint32_t)(r >> 32);
+            if (nready) {
+              rlo = nlo;
+              rhi = nhi;
+              nready = false;
+            } else {
+              const uint64_t r = philox_refill(K, wr.e + lane, worker);
+              rlo = (uint32_t)r;
+              rhi = (uint32_t)(r >> 32);
+            }
             ri = 0;
           }
           const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
@@ -997,7 +1034,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   uint8_t* sb = worker_sbase<kMem>(p, w);
   const WorkerView<Idx> S = make_view<Idx>(wb, sb, p.lay);
   RecencyLog R;
-  R.log = reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
+  R.log = reinterpret_cast<uint32_t*>(p.aux_base + ((size_t)blockIdx.x * p.W + w) * p.aux.bytes +
                                       p.aux.off_log);
   R.stamp = reinterpret_cast<uint16_t*>(sb + p.lay.off_stamp);
   R.cap_mask = p.aux.log_cap - 1;
@@ -1064,7 +1101,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
       }
       if (use_list) {
         if (!tree) R.stamp[my_slot] = wq;
-        R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] = ((uint64_t)wq << 32) | my_slot;
+        R.log[(ltail0 + (n - 1 - (kf + qq))) & R.cap_mask] = (wq << 16) | my_slot;
       }
     }
     __syncwarp();
@@ -1194,7 +1231,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
   const WorkerView<Idx> S =                                                          \
       make_view<Idx>(worker_gbase<kMem>(p, w), worker_sbase<kMem>(p, w), L);         \
   RecencyLog R;                                                                      \
-  R.log = reinterpret_cast<uint64_t*>(p.aux_base + ((size_t)blockIdx.x * W + w) *    \
+  R.log = reinterpret_cast<uint32_t*>(p.aux_base + ((size_t)blockIdx.x * W + w) *    \
                                       p.aux.bytes + p.aux.off_log);                  \
   R.stamp = reinterpret_cast<uint16_t*>(worker_sbase<kMem>(p, w) + L.off_stamp);     \
   R.cap_mask = p.aux.log_cap - 1;                                                    \
@@ -1872,7 +1909,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         const Idx s = act ? tbl_find<Idx>(S, tmask, H[d]) : NIL;
         if (act && use_list) {
           R.stamp[s] = wr.wq;
-          R.log[(ltail0 + (n - 1 - d)) & R.cap_mask] = ((uint64_t)wr.wq << 32) | (uint32_t)s;
+          R.log[(ltail0 + (n - 1 - d)) & R.cap_mask] = ((wr.wq & 0xffffu) << 16) | (uint32_t)s;
         }
         if (opt && act) opt_keys(p, w)[s] = opt_key(tr.nu[hd.block_off + d], d + 1, (uint32_t)s);
         if (led && act) last_access(p, w)[s] = (uint32_t)(hd.block_off + d);   // phase ledger
@@ -2026,7 +2063,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
 #endif
           // (loading the head windows earlier hides their latency but costs the
           // registers to hold them across the hits and accounting: slower overall)
-          uint64_t lpre[kLogDepth];
+          uint32_t lpre[kLogDepth];
           log_preload(R, wr.lhead, ltail0, lane, lpre);
           // the victims land in place, in slots[nfree .. M) (flagged below)
           wr.lhead = log_take(R, wr.lhead, ltail0, nev, slots + nfree, lane, lpre);

@@ -21,7 +21,7 @@ for L in bench.c5_plan(0, world):
     if L.W not in Ws:
         continue
     dts = [DeviceTrace(t) for t in L.traces]
-    for tier in (0, 1, 2, 3):
+    for tier in [int(t) for t in os.environ.get("KVR_AB_TIERS", "0,1,2,3").split(",")]:
         try:
             sim = Simulator(L.W, bench.B_BLOCKS, pending_ring=L.ring, force_tier=tier)
             plan = sim.plan(max(t.max_blocks for t in L.traces))

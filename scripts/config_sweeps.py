@@ -92,7 +92,9 @@ if 3 in which:
         plan.append(by_router[r][k % len(by_router[r])])
     mine = list(range(0, 4096, RANKS))
     pols = policies_array([Policy(eviction=1, **plan[t]) for t in mine])
-    sim = Simulator(16, 512, pending_ring=RING)
+    # pending FIFO up to the trace length (pooled chunks, ABI v7): no trial stops at a ring
+    # overflow, even the collapsing NLMS cells (mu = 0.992) whose queues grow without bound
+    sim = Simulator(16, 512, pending_ring=tr.n_queries)
     res, ms = timed_launch(sim, [dt], np.array([t + 1 for t in mine], np.uint64), pols)
     rows.append(summarize("config3: DRIFT 1M queries, W=16, B=512, RLT, LBGR/STATIC/THRESHOLD grid",
                           [(res, ms)], dict(share=f"trials t = 0 mod {RANKS} of 4,096",
@@ -119,43 +121,20 @@ if 4 in which:
                           dict(share=f"trials t = 0 mod {RANKS} of 16,384 (one launch per B)")))
 
 if 5 in which:
-    # RLT on even keys, L-LRU on odd: with keys t + 1 strided over an even
-    # number of ranks, even ranks hold only L-LRU trials and odd ranks only RLT trials, so
-    # the shares of rank 0 and rank 1 are both timed (an 8-GPU job waits for the slower).
-    settings = ((0.3, 2), (0.5, 8), (0.9, 32))
-    cell_of = (np.arange(65536) * 48) // 65536
-    for rank in (0, 1):
-        parts = []
-        for W in (4, 8, 16, 32):
-            trs = []
-            for si, (r, qd) in enumerate(settings):
-                seed = 0xC7 + 16 * si + W
-                trs.append(wl.gsp(128, 32, r, seed=seed, W=W))
-                trs.append(wl.mt(128, r, seed=seed + 1, W=W, name="mt-sharegpt"))
-                trs.append(wl.mt(128, r, seed=seed + 2, W=W, name="mt-ultrachat"))
-                trs.append(wl.ld(512, qd, seed=seed + 3, W=W))
-            dts = [DeviceTrace(t) for t in trs]
-            # 48 cells (12 traces x 4 W) of 1,365/1,366 trials over 65,536; this W's cells
-            wi = (4, 8, 16, 32).index(W)
-            mine = [t for t in range(65536) if cell_of[t] // 12 == wi and t % RANKS == rank]
-            # longest trials first (LPT list scheduling onto the persistent CTAs): the
-            # kernel hands trials out in index order, and LD-high trials are 25x longer
-            # than MT ones; per-trial results do not depend on the order
-            nq = np.array([t.n_queries for t in trs])
-            mine.sort(key=lambda t: (-int(nq[cell_of[t] % 12]), t))
-            tt = np.array([cell_of[t] % 12 for t in mine], np.uint32)
-            pols = policies_array([Policy(eviction=1 if (t + 1) % 2 == 0 else 0) for t in mine])
-            ev = "RLT" if (rank + 1) % 2 == 0 else "L-LRU"
-            sim = Simulator(W, 512, pending_ring=RING)
-            res, ms = timed_launch(sim, dts, np.array([t + 1 for t in mine], np.uint64), pols,
-                                   trial_trace=tt)
-            parts.append((res, ms))
-            rows.append(summarize(f"config5 rank {rank} ({ev}) W={W}: 4 benchmarks x 3 settings, B=512, LBGR",
-                                  [(res, ms)], dict(share=f"trials t = {rank} mod {RANKS} of 65,536",
-                                                    tier=sim.plan(max(t.max_blocks for t in trs))[0])))
-            sim.close()
-        rows.append(summarize(f"config5 rank {rank} all W (sum of the four launches)", parts,
-                              dict(share=f"trials t = {rank} mod {RANKS} of 65,536")))
+    # the bench's fixed 65,536-trial list, this script's share = rank 0 of RANKS under the
+    # bench's (t div 2) mod N sharding (RLT and Leaf-LRU mixed), one launch per W
+    parts = []
+    for L in bench.c5_plan(0, RANKS):
+        dts = [DeviceTrace(t) for t in L.traces]
+        sim = Simulator(L.W, bench.B_BLOCKS, pending_ring=L.ring)
+        res, ms = timed_launch(sim, dts, L.keys, L.policies(), trial_trace=L.trial_trace)
+        parts.append((res, ms))
+        rows.append(summarize(f"config5 W={L.W}: 4 benchmarks x 3 settings, B=512, LBGR, RLT/L-LRU mixed",
+                              [(res, ms)], dict(share=f"(t div 2) mod {RANKS} == 0 of 65,536",
+                                                tier=sim.plan(max(t.max_blocks for t in L.traces))[0])))
+        sim.close()
+    rows.append(summarize("config5 all W (sum of the four launches)", parts,
+                          dict(share=f"(t div 2) mod {RANKS} == 0 of 65,536")))
 
 if out_path:
     with open(out_path, "w") as f:
