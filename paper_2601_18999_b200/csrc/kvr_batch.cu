@@ -17,14 +17,16 @@
 // double-buffered by query parity so one barrier per query suffices.
 //
 // Per-worker state (tree slots, open-addressed identity -> slot table with
-// backward-shift deletion, pin counts, RLT marks, in-flight records, staged
-// path) lives in shared memory when W of them fit, else in the workspace
-// (L2-resident); the waiting FIFO is a ring in the workspace.  Victim
-// selection is a warp-parallel scan over the B slots (Leaf-LRU: warp min of
-// (stamp, -depth) over the set bits of the unpinned-leaf bitmap LEAFU; RLT:
-// popc of LEAFU & ~MARK per word, a Philox draw, a warp scan + bit select).
-// LEAFU is maintained incrementally: hits/loads pin (clear), unpins of a
-// childless node and evictions that empty an unpinned parent set it.
+// tombstones, pin counts, RLT marks, in-flight records, staged path) lives in shared
+// memory when W of them fit, else in the workspace (L2-resident); the waiting FIFO is a
+// ring in the workspace.  Victim selection: Leaf-LRU takes the first unpinned valid
+// entries of a per-worker recency log, 32 per ballot; RLT (B <= 1024) keeps LEAFU, MARK
+// and U = LEAFU & ~MARK in registers (lane l: word l) with U's prefix counts and selects
+// each victim with two CREDUX reductions, fetching the victim's parent / child count /
+// pin speculatively; its table erases, digest terms and the loaded slots' arrays are
+// written in one lane-parallel pass after the decisions.  LEAFU is maintained
+// incrementally: hits/loads pin (clear), unpins of a childless node and evictions that
+// empty an unpinned parent set it.
 #include <math.h>
 
 #include "kvr_device.cuh"
@@ -34,14 +36,38 @@ namespace kvr {
 
 extern __shared__ __align__(16) uint8_t kvr_bsmem[];
 
+#ifdef KVR_PHASE_PROFILE
+// phase profiler of the batching kernel (profiling build only): cycles summed by lane 0
+__device__ unsigned long long g_bphase[32];
+#define BP_T0(v) unsigned long long v = clock64()
+#define BP_ACC(ph, v)                                                        \
+  do {                                                                       \
+    const unsigned long long _n = clock64();                                 \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_bphase[ph], _n - (v));         \
+    v = _n;                                                                  \
+  } while (0)
+#define BP_CNT(ph, cnt)                                                                 \
+  do {                                                                                  \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_bphase[ph], (unsigned long long)(cnt));   \
+  } while (0)
+#else
+#define BP_T0(v) (void)0
+#define BP_ACC(ph, v) (void)0
+#define BP_CNT(ph, cnt) (void)0
+#endif
+
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
+#ifndef KVR_BATCH_REBUILD_NUM
+#define KVR_BATCH_REBUILD_NUM 6u   // rebuild the table when live + tombstones > (num / 8) T
+#endif
 
 // Idx = u16 (shared-memory tier) or u32 (global tier) slot ids; all-ones = NONE
 template <typename Idx>
 struct BView {
   static constexpr uint32_t NIL = (uint32_t)(Idx)~(Idx)0;
+  static constexpr uint32_t TOMB = NIL - 1u;
   uint64_t* key;
   uint32_t* stamp;
   Idx *parent, *nchild, *depth, *table;
@@ -94,57 +120,68 @@ __device__ __forceinline__ BView<Idx> bview(uint8_t* base, const BatchLayout& Lr
   return v;
 }
 
-// ---- identity -> slot table: linear probing, backward-shift deletion ----
+// ---- identity -> slot table: linear probing, tombstones ----
+// An erased entry becomes a tombstone (probes continue past it, inserts reuse it), or
+// EMPTY when its successor is EMPTY (no probe path can run through it).  Lanes may erase
+// concurrently (distinct slots): an entry only turns EMPTY when its successor was EMPTY
+// when read, and nothing turns an EMPTY entry back during an erase pass, so no live
+// entry is ever cut off from its home.  live + tombstones is counted per worker (x.used)
+// and the table is rebuilt without tombstones when it exceeds 3T/4 (KVR_BATCH_REBUILD_NUM).
 template <typename Idx>
 __device__ __forceinline__ uint32_t t_find(const BView<Idx>& S, uint64_t t) {
   uint32_t i = (uint32_t)t & S.tmask;
   for (;;) {
     const uint32_t s = S.table[i];
     if (s == BView<Idx>::NIL) return kNone;
-    if (S.key[s] == t) return s;
+    if (s != BView<Idx>::TOMB && S.key[s] == t) return s;
     i = (i + 1) & S.tmask;
   }
 }
+// warp-cooperative insert of (t, slot) for the active lanes, no atomics: each round every
+// pending lane reads its probe position; among the lanes that found the same free entry
+// (EMPTY or tombstone) the lowest one takes it, the others move on.  Returns the number of
+// EMPTY entries used (warp-uniform).  (Measured faster than per-lane 32-bit CAS claims.)
 template <typename Idx>
-__device__ __forceinline__ void t_insert(const BView<Idx>& S, uint64_t t, uint32_t slot) {
-  uint32_t i = (uint32_t)t & S.tmask;
-  while (S.table[i] != BView<Idx>::NIL) i = (i + 1) & S.tmask;
-  S.table[i] = (Idx)slot;
-}
-// concurrent insert: lanes claim EMPTY entries with compare-and-swap
-__device__ __forceinline__ bool cas_claim(uint16_t* e, uint32_t slot) {
-  return atomicCAS(reinterpret_cast<unsigned short*>(e), (unsigned short)0xffffu,
-                   (unsigned short)slot) == (unsigned short)0xffffu;
-}
-__device__ __forceinline__ bool cas_claim(uint32_t* e, uint32_t slot) {
-  return atomicCAS(e, 0xffffffffu, slot) == 0xffffffffu;
-}
-template <typename Idx>
-__device__ __forceinline__ void t_insert_cas(const BView<Idx>& S, uint64_t t, uint32_t slot) {
-  uint32_t i = (uint32_t)t & S.tmask;
-  for (;;) {
-    if (S.table[i] == BView<Idx>::NIL && cas_claim(&S.table[i], slot)) return;
-    i = (i + 1) & S.tmask;
+__device__ __forceinline__ uint32_t t_insert_warp(const BView<Idx>& S, bool act, uint64_t t, uint32_t slot,
+                                                  uint32_t lane) {
+  uint32_t pos = (uint32_t)t & S.tmask, fresh = 0;
+  bool pending = act;
+  while (__any_sync(kFull, pending)) {
+    const uint32_t e = pending ? (uint32_t)S.table[pos] : 0u;
+    const bool fr = pending && (e == BView<Idx>::NIL || e == BView<Idx>::TOMB);
+    const uint32_t peers = __match_any_sync(kFull, fr ? pos : 0xffffffffu);
+    const bool win = fr && (uint32_t)(__ffs(peers) - 1) == lane;
+    __syncwarp();   // every read of this round precedes its writes
+    if (win) {
+      S.table[pos] = (Idx)slot;
+      pending = false;
+    } else if (pending && !fr) {
+      pos = (pos + 1) & S.tmask;
+    }
+    fresh += __popc(__ballot_sync(kFull, win && e == BView<Idx>::NIL));
   }
+  __syncwarp();
+  return fresh;
 }
+// remove slot's entry (identity t, present); returns 1 if it became EMPTY
 template <typename Idx>
-__device__ __forceinline__ void t_erase(const BView<Idx>& S, uint64_t t, uint32_t slot) {
+__device__ __forceinline__ uint32_t t_erase(const BView<Idx>& S, uint64_t t, uint32_t slot) {
   uint32_t i = (uint32_t)t & S.tmask;
   while (S.table[i] != (Idx)slot) i = (i + 1) & S.tmask;   // present (caller's contract)
-  uint32_t j = i;
-  for (;;) {
-    j = (j + 1) & S.tmask;
-    const uint32_t s = S.table[j];
-    if (s == BView<Idx>::NIL) break;
-    const uint32_t home = (uint32_t)S.key[s] & S.tmask;
-    // keep s where it is iff its home lies cyclically in (i, j]
-    const bool keep = (i <= j) ? (home > i && home <= j) : (home > i || home <= j);
-    if (!keep) {
-      S.table[i] = (Idx)s;
-      i = j;
-    }
+  const bool clear = S.table[(i + 1) & S.tmask] == BView<Idx>::NIL;
+  S.table[i] = (Idx)(clear ? BView<Idx>::NIL : BView<Idx>::TOMB);
+  return clear ? 1u : 0u;
+}
+// rebuild without tombstones (warp): slots [0, size) are the live nodes
+template <typename Idx>
+__device__ __forceinline__ void t_rebuild(const BView<Idx>& S, uint32_t size, uint32_t lane) {
+  __syncwarp();
+  for (uint32_t q = lane; q <= S.tmask; q += 32) S.table[q] = (Idx)BView<Idx>::NIL;
+  __syncwarp();
+  for (uint32_t b0 = 0; b0 < size; b0 += 32) {
+    const uint32_t q = b0 + lane;
+    t_insert_warp(S, q < size, q < size ? S.key[q] : 0ull, q, lane);
   }
-  S.table[i] = (Idx)BView<Idx>::NIL;
 }
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
@@ -183,6 +220,7 @@ struct __align__(16) BCtrl {
 // Per-warp (worker) scalar state: warp-uniform registers.
 struct BW {
   uint32_t size, cntT, nfl, wh, wn;
+  uint32_t used;           // table entries that are live or tombstones
   uint32_t lhead, ltail;   // Leaf-LRU recency log cursors (first maybe-valid entry, end)
   uint64_t e, k, vcur;
   double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
@@ -273,12 +311,243 @@ __device__ __forceinline__ uint32_t cand_select(const BView<Idx>& S, const BTria
   return kNone;
 }
 
+// Register-resident candidate words (B <= 1024, lane l holds word l): inclusive prefix
+// counts of the per-lane popcounts by six bit-sliced ballots; returns the total
+__device__ __forceinline__ uint32_t words_count(uint32_t w, uint32_t lane, uint32_t& incl) {
+  const uint32_t c = __popc(w);
+  const uint32_t le = lane == 31 ? kFull : (2u << lane) - 1u;
+  uint32_t tot = 0, inc = 0;
+#pragma unroll
+  for (int b = 0; b < 6; ++b) {
+    const uint32_t bal = __ballot_sync(kFull, (c >> b) & 1u);
+    tot += (uint32_t)__popc(bal) << b;
+    inc += (uint32_t)__popc(bal & le) << b;
+  }
+  incl = inc;
+  return tot;
+}
+// the idx-th set bit (slot order) of the words w, incl as from words_count
+__device__ __forceinline__ uint32_t words_select(uint32_t w, uint32_t incl, uint32_t idx, uint32_t lane) {
+  const uint32_t owner = __reduce_min_sync(kFull, incl > idx ? lane : 32u);
+  const uint32_t ou = __shfl_sync(kFull, w, owner);
+  const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
+  const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;
+  const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
+  return owner * 32 + bit;
+}
+
+// RLT miss decisions of an update, blocks [d0, n) (all misses; Alg. 1 l.6-17 with
+// pinning, A30-A33), B <= 1024.  LEAFU (lw), MARK (mw) and U = LEAFU & ~MARK (uw) are
+// held in registers with U's prefix counts; a draw selects its victim by two CREDUX
+// reductions, the victim's parent / child count / pin are fetched speculatively for
+// the whole owner word while the bit is selected.  Everything the decisions do not
+// read is deferred to one lane-parallel pass at the end: the victims' table erases,
+// digest terms and victim-log entries (their identities are still in place), and the
+// loaded slots' identities, parents, child counts, stamps, depths and pins.  gam[d]
+// <- slot | evicted << 32.
+template <typename Idx>
+__device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t j,
+                                             uint32_t d0, uint32_t n, uint32_t prev0, const uint64_t* Hj,
+                                             uint32_t* nvict, uint64_t* Vout) {
+  const uint32_t lane = T.lane, B = T.B, nw = T.nwords;
+  const uint32_t fallback = T.pol->rlt_fallback;
+  uint32_t lw = lane < nw ? S.leafu[lane] : 0u;
+  uint32_t mw = lane < nw ? S.markb[lane] : 0u;
+  uint32_t uw = 0, incl = 0, total = 0;
+  bool dirty = true;
+  uint64_t rbatch = 0, rbase = 0;
+  bool rvalid = false;
+  const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;
+  uint32_t nv = 0;
+  for (uint32_t d = d0; d < n; ++d) {
+    // Alg. 1 l.6-9: t is not cached, so not in T; the (B+1)-th distinct mark resets T
+    if (x.cntT + 1 == B + 1) {
+      mw = 0u;
+      x.cntT = 1;
+      x.c[4]++;
+      dirty = true;
+    } else {
+      x.cntT++;
+    }
+    uint32_t slot, ev = 0;
+    if (x.size < B) {
+      slot = x.size++;
+    } else {
+      if (dirty) {
+        uw = lw & ~mw;
+        total = words_count(uw, lane, incl);
+        dirty = false;
+      }
+      uint32_t v;
+      bool via_u = true;
+      if (total == 0) {   // U = {} (A5)
+        x.c[5]++;
+        via_u = false;
+        dirty = true;
+        bool draw = true;
+        uint32_t cw = lw, ci = 0, ct;
+        if (fallback == KVR_RLT_EARLY_RESET) {
+          mw = 0u;       // T <- {t}; t is loaded marked below
+          x.cntT = 1;
+          x.c[4]++;
+        } else if (fallback == KVR_RLT_LRU_MARKED) {   // least (stamp, -depth) unpinned leaf
+          draw = false;
+        }
+        if (draw) {
+          ct = words_count(cw, lane, ci);
+          if (ct == 0) return false;   // every leaf is in flight
+          if (!rvalid || x.e - rbase >= 32) {
+            rvalid = true;
+            rbase = x.e;
+            rbatch = philox_r64(T.K, rbase + lane, T.i, 1);
+          }
+          const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
+          x.e++;
+          x.c[3]++;
+          v = words_select(cw, ci, (uint32_t)pick_index(r, ct), lane);
+        } else {
+          uint64_t best = ~0ull;
+          uint32_t bits = lw;
+          while (bits) {
+            const uint32_t q = (lane << 5) + (__ffs(bits) - 1);
+            bits &= bits - 1;
+            const uint64_t key = ((uint64_t)S.stamp[q] << 32) |
+                                 ((uint64_t)((0x10000u - S.depth[q]) & 0xffffu) << 16) | (uint64_t)q;
+            best = key < best ? key : best;
+          }
+          best = warp_min_u64(best);
+          if (best == ~0ull) return false;
+          v = (uint32_t)(best & 0xffffu);
+        }
+        if ((__shfl_sync(kFull, mw, v >> 5) >> (v & 31)) & 1u) x.cntT--;   // a marked victim leaves T
+        const uint32_t pa = S.parent[v];
+        if (pa != BView<Idx>::NIL) {
+          const uint32_t nc = S.nchild[pa] - 1u;
+          __syncwarp();
+          S.nchild[pa] = (Idx)nc;
+          if (nc == 0 && S.pin[pa] == 0 && lane == (pa >> 5)) lw |= 1u << (pa & 31);
+        }
+      } else {
+        // Alg. 1 l.14-16: uniform over U in slot order (A6), counter e_i
+        if (!rvalid || x.e - rbase >= 32) {
+          rvalid = true;
+          rbase = x.e;
+          rbatch = philox_r64(T.K, rbase + lane, T.i, 1);
+        }
+        const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
+        x.e++;
+        x.c[3]++;
+        const uint32_t idx = (uint32_t)pick_index(r, total);
+        const uint32_t owner = __reduce_min_sync(kFull, incl > idx ? lane : 32u);
+        // speculative: lane l fetches the parent of slot owner*32+l, its child count and pin
+        const uint32_t ss = owner * 32 + lane;
+        uint32_t sp = ss < B ? (uint32_t)S.parent[ss] : BView<Idx>::NIL;
+        const bool sok = sp < B;
+        sp = sok ? sp : 0u;
+        const uint32_t snc = (uint32_t)S.nchild[sp];
+        const uint32_t spin = (uint32_t)S.pin[sp];
+        const uint32_t smw = __shfl_sync(kFull, mw, sp >> 5);
+        const uint32_t ou = __shfl_sync(kFull, uw, owner);
+        const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
+        const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
+        v = owner * 32 + bit;
+        const uint32_t pa = __shfl_sync(kFull, sp, bit);
+        const bool hasp = __shfl_sync(kFull, (uint32_t)sok, bit) != 0u;
+        const uint32_t nc = __shfl_sync(kFull, snc, bit) - 1u;
+        const uint32_t ppin = __shfl_sync(kFull, spin, bit);
+        const uint32_t pmw = __shfl_sync(kFull, smw, bit);
+        // U loses v (the slot is reloaded with t: pinned, marked), gains pa iff pa became an
+        // unpinned unmarked leaf
+        if (lane == owner) uw &= ~(1u << bit);
+        if (lane >= owner) --incl;
+        --total;
+        if (hasp) {
+          S.nchild[pa] = (Idx)nc;   // uniform store (every lane read its value above)
+          const uint32_t pw = pa >> 5, pb = 1u << (pa & 31);
+          if (nc == 0 && ppin == 0) {
+            if (lane == pw) lw |= pb;
+            if (!(pmw & pb)) {   // pa != v (v is its child): the victim's MARK bit is irrelevant
+              if (lane == pw) uw |= pb;
+              if (lane >= pw) ++incl;
+              ++total;
+            }
+          }
+        }
+      }
+      (void)via_u;
+      // v leaves LEAFU and its MARK bit is replaced by t's
+      if (lane == (v >> 5)) lw &= ~(1u << (v & 31));
+      slot = v;
+      ev = 1;
+      x.c[2]++;
+      ++nv;
+    }
+    if (lane == (slot >> 5)) mw |= 1u << (slot & 31);   // t in T (Alg. 1 l.7)
+    if (lane == 0) S.gam[d] = (uint64_t)slot | ((uint64_t)ev << 32);
+    x.c[1]++;
+  }
+  if (lane < nw) {
+    S.leafu[lane] = lw;
+    S.markb[lane] = mw;
+  }
+  __syncwarp();
+  // deferred, lane-parallel: victims' erases / digest terms / log entries (the k-th victim
+  // of the update is the k-th evicting block), then the loads
+  uint64_t V = 0;
+  uint32_t k0 = 0, cleared = 0, prev_last = prev0;
+  for (uint32_t b0 = d0; b0 < n; b0 += 32) {
+    const uint32_t q = b0 + lane;
+    const bool act = q < n;
+    const uint64_t g = act ? S.gam[q] : 0ull;
+    const uint32_t slot = (uint32_t)g;
+    const bool ev = act && (g >> 32) != 0;
+    const uint32_t evb = __ballot_sync(kFull, ev);
+    const uint32_t k = k0 + __popc(evb & ((1u << lane) - 1u));
+    uint64_t hv = 0;
+    if (ev) {
+      hv = S.key[slot];
+      cleared += t_erase(S, hv, slot);
+      V ^= fmix64(hv ^ ((uint64_t)(k + 1) * kPosMul));
+      if (T.vlog) {
+        if (x.vcur + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + x.vcur + k] = hv;
+        else x.c[11] = 1;
+      }
+    }
+    k0 += __popc(evb);
+    const uint32_t up = __shfl_up_sync(kFull, slot, 1);
+    const uint32_t par = lane == 0 ? prev_last : up;
+    const uint32_t last = min(31u, n - 1 - b0);
+    __syncwarp();   // every victim identity is read before the slots are reloaded
+    if (act) {
+      S.key[slot] = Hj[q];
+      S.parent[slot] = (Idx)par;   // kNone -> NIL (root child)
+      S.nchild[slot] = (Idx)(q + 1 < n ? 1 : 0);
+      S.stamp[slot] = j;
+      S.depth[slot] = (Idx)(q + 1);
+      S.pin[slot] = 1;
+      S.gam[q] = slot;
+    }
+    prev_last = __shfl_sync(kFull, slot, last);
+    __syncwarp();
+  }
+  if (prev0 != kNone && lane == 0) S.nchild[prev0] = (Idx)(S.nchild[prev0] + 1);   // prev0 is pinned
+  x.used -= __reduce_add_sync(kFull, cleared);
+  x.c[11] = __reduce_or_sync(kFull, x.c[11]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  x.vcur += nv;
+  __syncwarp();
+  *nvict += nv;
+  *Vout ^= V;
+  return true;
+}
+
 // UpdateCache(S_i, Gamma_j) at dequeue (Eq. 3 with Alg. 1 / Leaf-LRU, P:115-122,
 // P:225-245), pinning every block as it is accessed (A30, A33).
 // Returns the number of leading input hits m, or kNone on an admission failure.
 template <typename Idx>
 __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& S, BW& x, uint32_t j, uint32_t n,
-                             uint32_t n_in, uint32_t* nvict, uint64_t* Vout) {
+                             uint32_t n_in, const uint64_t* Hj, uint32_t* nvict, uint64_t* Vout) {
   const uint32_t lane = T.lane, B = T.B;
   const kvr_policy& pol = *T.pol;
   uint32_t prev = kNone;
@@ -288,6 +557,11 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   uint64_t V = 0;
   const bool lru = !T.rlt;
   if (lru && x.ltail - x.lhead + n > T.lmask + 1) x.ltail = blog_compact(T, S, x.lhead, x.ltail);
+  // room for this update's n inserts with an EMPTY entry left (probes must terminate)
+  if (x.used + n >= S.tmask) {
+    t_rebuild(S, x.size, lane);
+    x.used = x.size;
+  }
   // Leaf-LRU victims (A33) = the unpinned nodes in recency-log order (stamp, -depth)
   // from the head: the minimum over the unpinned nodes is always a leaf, and the
   // nodes this update loads are pinned, so the e victims of a miss run are the e
@@ -323,10 +597,50 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       return __shfl_sync(kFull, (uint32_t)le, L);
     }
   };
+  // the victims of the evicting lanes evb (the k-th set bit of evb takes the k-th victim),
+  // 32 log entries per ballot; returns false if the log runs out (every node in flight)
+  auto lru_take_batch = [&](uint32_t evb, uint32_t& v) -> bool {
+    const uint32_t need = __popc(evb);
+    const uint32_t rk = __popc(evb & ((1u << lane) - 1u));
+    const bool evl = (evb >> lane) & 1u;
+    uint32_t got = 0;
+    while (got < need) {
+      if (cm == 0) {
+        if (lwin) lpos += 32;
+        if (lpos >= x.ltail) return false;
+        const uint32_t idx = lpos + lane;
+        le = idx < x.ltail ? T.log[idx & T.lmask] : 0ull;
+        const uint32_t sl = (uint32_t)le;
+        const bool valid = idx < x.ltail && S.stamp[sl] == (uint32_t)(le >> 32);
+        const uint32_t vb = __ballot_sync(kFull, valid);
+        cm = __ballot_sync(kFull, valid && S.pin[sl] == 0);
+        if (!headfix) {
+          if (vb) {
+            x.lhead = lpos + (__ffs(vb) - 1);
+            headfix = true;
+          } else {
+            x.lhead = min(lpos + 32, x.ltail);
+          }
+        }
+        lwin = true;
+        continue;
+      }
+      const uint32_t c = __popc(cm);
+      const uint32_t take = min(c, need - got);
+      const bool mine = evl && rk >= got && rk < got + take;
+      const uint32_t src = mine ? select_bit(cm, rk - got) : 0u;
+      const uint32_t val = __shfl_sync(kFull, (uint32_t)le, src);
+      if (mine) v = val;
+      cm = take == c ? 0u : (cm & ~((2u << select_bit(cm, take - 1)) - 1u));
+      got += take;
+    }
+    return true;
+  };
   // Lane-parallel hit run: 32 blocks per step, each lane looks up its own block; the
   // leading hits are refreshed, pinned and (RLT) marked at once when no |T| = B+1
   // reset can fall inside the step, else the step is left to the serial loop below.
   uint32_t d = 0;
+  BP_T0(tu);
   while (d < n) {
     const uint32_t q = d + lane;
     const uint32_t sl = q < n ? t_find(S, S.gam[q]) : kNone;
@@ -362,6 +676,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   // loop (no lookup happens inside a miss run); gam[d] then holds block d's slot.
   // RLT keeps |U| incrementally (a victim leaves U, its parent may join) and draws
   // from a batch of 32 consecutive Philox counters computed lane-parallel.
+  BP_ACC(8, tu);   // hit run
   const uint32_t d_miss0 = hitrun ? n : d;   // first block known to miss (if any)
   uint32_t d_ins0 = n;                       // first block whose insert is deferred
   int32_t nU_known = -1;                     // |U| when known, -1 = recount
@@ -383,11 +698,9 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       const bool ev = act && q >= nfree;
       const uint32_t evb = __ballot_sync(kFull, ev);
       uint32_t v = kNone;
-      for (uint32_t rest = evb; rest; rest &= rest - 1) {
-        const uint32_t t = lru_take();
-        if (t == kNone) return kNone;   // every node is in flight
-        if (lane == (uint32_t)(__ffs(rest) - 1)) v = t;
-      }
+      BP_T0(tl);
+      if (!lru_take_batch(evb, v)) return kNone;   // every node is in flight
+      BP_ACC(9, tl);
       const uint32_t slot = ev ? v : x.size + q;
       uint64_t hv = 0;
       if (ev) {
@@ -400,14 +713,11 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
         }
       }
       __syncwarp();
-      // victims leave the table first (their slots are reloaded just below)
-      for (uint32_t rest = evb; rest; rest &= rest - 1) {
-        const uint32_t L = __ffs(rest) - 1;
-        const uint64_t h = __shfl_sync(kFull, hv, L);
-        const uint32_t vv = __shfl_sync(kFull, v, L);
-        if (lane == 0) t_erase(S, h, vv);
-      }
+      // victims leave the table first (their slots are reloaded just below), one lane each
+      const uint32_t clr = ev ? t_erase(S, hv, v) : 0u;
+      x.used -= __popc(__ballot_sync(kFull, clr != 0u));
       __syncwarp();
+      BP_ACC(10, tl);
       if (act) {   // Load(S, t): pinned, stamped at j; the table insert is deferred
         const uint32_t dd = d + q;
         S.key[slot] = S.gam[dd];
@@ -429,12 +739,14 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
     d = n;   // the serial loop below has nothing left
   }
+  BP_ACC(11, tu);   // Leaf-LRU miss run (incl. take / erase)
   uint64_t rbatch = 0, rbase = 0;            // draws for counters rbase .. rbase+31
   bool rvalid = false;
   for (; d < n; ++d) {
     const uint64_t t = S.gam[d];
     uint32_t s = (hitrun && d < d_miss0) ? t_find(S, t) : kNone;
     if (s == kNone) hitrun = false;
+    if (s == kNone && T.rlt && regu) break;   // every later block misses too: fast path below
     // Alg. 1 l.6-9: mark t; the (B+1)-th distinct mark resets T to {t}
     if (T.rlt) {
       const bool marked = s != kNone && bit_test(S.markb, s);
@@ -574,8 +886,9 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
         }
       }
       __syncwarp();
+      uint32_t clr = 0;
       if (lane == 0) {
-        t_erase(S, hv, v);
+        clr = t_erase(S, hv, v);
         if (has_pa) {
           S.nchild[pa] = (Idx)nc;
           if (pa_leafu) S.leafu[pa >> 5] |= 1u << (pa & 31);
@@ -583,6 +896,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
         S.markb[v >> 5] &= ~(1u << (v & 31));
         S.leafu[v >> 5] &= ~(1u << (v & 31));
       }
+      x.used -= __shfl_sync(kFull, clr, 0);
       __syncwarp();
       x.c[2]++;
       V ^= fmix64(hv ^ ((uint64_t)(nv + 1) * kPosMul));
@@ -616,18 +930,32 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     x.c[1]++;
     prev = slot;
   }
-  // deferred table inserts, lane-parallel (linear probing, CAS-claimed entries)
-  for (uint32_t q = d_ins0 + lane; q < n; q += 32) {
-    const uint32_t slot = (uint32_t)S.gam[q];
-    t_insert_cas(S, S.key[slot], slot);
+  if (d < n) {   // RLT misses with register-resident LEAFU / MARK words (B <= 1024)
+    d_ins0 = d;
+    if (!b_rlt_misses(T, S, x, j, d, n, prev, Hj, &nv, &V)) return kNone;
+    d = n;
   }
-  __syncwarp();
+  BP_ACC(12, tu);   // serial loop (RLT misses, hit steps around a reset)
+  // deferred table inserts, lane-parallel (linear probing, CAS-claimed entries)
+  for (uint32_t b0 = d_ins0; b0 < n; b0 += 32) {
+    const uint32_t q = b0 + lane;
+    const uint32_t slot = q < n ? (uint32_t)S.gam[q] : 0u;
+    x.used += t_insert_warp(S, q < n, q < n ? S.key[slot] : 0ull, slot, lane);
+  }
+  BP_ACC(17, tu);   // deferred inserts
+  if (x.used > KVR_BATCH_REBUILD_NUM * (S.tmask + 1u) / 8u) {   // too many tombstones: rebuild
+    t_rebuild(S, x.size, lane);
+    x.used = x.size;
+    BP_CNT(23, 1);
+  }
+  BP_ACC(18, tu);   // rebuilds
   if (lru) {   // the path, deepest first, at stamp j (it was compacted to fit)
     for (uint32_t q = lane; q < n; q += 32)
       T.log[(x.ltail + (n - 1 - q)) & T.lmask] = ((uint64_t)j << 32) | (uint32_t)S.gam[q];
     x.ltail += n;
     __syncwarp();
   }
+  BP_ACC(13, tu);   // log append append
   *nvict = nv;
   *Vout = V;
   return m;
@@ -641,12 +969,16 @@ __device__ __forceinline__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, 
   const QueryHdr& h = T.tr.hdr[j];
   const uint32_t n_in = h.n_in, n = h.n_in + h.n_out;
   const uint64_t* Hj = T.tr.hash + h.block_off;
+  BP_T0(td);
   for (uint32_t d = lane; d < n; d += 32) S.gam[d] = Hj[d];
   __syncwarp();
+  BP_ACC(14, td);   // dequeue: header + path staging
+  BP_CNT(20, 1);
   uint32_t nv = 0;
   uint64_t V = 0;
-  const uint32_t m = b_update(T, S, x, j, n, n_in, &nv, &V);
+  const uint32_t m = b_update(T, S, x, j, n, n_in, Hj, &nv, &V);
   if (m == kNone) return false;
+  BP_T0(ta);
   const kvr_service_model& tm = T.p->truth;
   const uint32_t q = T.bt * n_in;
   const uint32_t hh = T.bt * m;
@@ -691,6 +1023,7 @@ __device__ __forceinline__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, 
     }
     if (T.p->bins) atomicAdd(&T.ctrl->hist[hist_bin_b(lat, T.p->bins)], 1u);
   }
+  BP_ACC(15, ta);   // dequeue accounting
   return true;
 }
 
@@ -760,6 +1093,8 @@ __device__ __forceinline__ bool b_complete(const BTrial& T, const BView<Idx>& S,
     if (x.Pt < 0.0) x.Pt = 0.0;
   }
   // release_path: lane-parallel lookups, distinct slots
+  BP_T0(tr_);
+  BP_CNT(21, 1);
   const QueryHdr& h = T.tr.hdr[r.j];
   const uint32_t n = h.n_in + h.n_out;
   const uint64_t* Hj = T.tr.hash + h.block_off;
@@ -776,6 +1111,7 @@ __device__ __forceinline__ bool b_complete(const BTrial& T, const BView<Idx>& S,
   }
   if (__any_sync(kFull, bad)) return false;
   __syncwarp();
+  BP_ACC(16, tr_);   // release path (unpin)
   if (x.wn > 0) {
     const BFlight hq = T.ring[(size_t)T.i * T.ringcap + x.wh];
     x.wh = x.wh + 1 == T.ringcap ? 0 : x.wh + 1;
@@ -893,7 +1229,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     if (T.rls && lane < 16) S.rlsP[lane] = (lane % 5 == 0) ? pol.rls_p0 : 0.0;
     __syncwarp();
     BW x;
-    x.size = 0; x.cntT = 0; x.nfl = 0; x.wh = 0; x.wn = 0;
+    x.size = 0; x.cntT = 0; x.nfl = 0; x.wh = 0; x.wn = 0; x.used = 0;
     x.lhead = 0; x.ltail = 0;
     x.e = 0; x.k = 0; x.vcur = 0;
     x.Pt = 0.0; x.P = 0.0; x.F = 0.0; x.slat = 0.0; x.sttft = 0.0; x.mlat = 0.0;
@@ -914,6 +1250,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
 #pragma unroll 1
     for (uint32_t j = 0; j < Nrun; ++j) {
       const uint32_t par = j & 1;
+      BP_T0(tp);
       const QueryHdr& hq = T.tr.hdr[j];
       const double t = hq.arrival_ms;
       const uint32_t n_in = hq.n_in;
@@ -946,6 +1283,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
           ctrl->abortf[par] = 1;
         }
       }
+      BP_ACC(0, tp);   // header + catch-up (completions, dequeues)
       // 2. longest cached prefix at a_j (A32): lane-parallel probes, first miss by ballot
       const uint64_t* Hj = T.tr.hash + hq.block_off;
       uint32_t m = 0;
@@ -986,7 +1324,9 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
         ctrl->pend[par][w] = pend;
         ctrl->csize[par][w] = x.size;
       }
+      BP_ACC(1, tp);   // match + score
       __syncthreads();
+      BP_ACC(2, tp);   // barrier
       if (ctrl->abortf[par]) {
         aborted = true;
         break;
@@ -1035,8 +1375,10 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       } else {
         best = (uint32_t)pick_index(philox_r64(T.K, j, 0xFFFFFFFFu, 2), W);
       }
+      BP_ACC(3, tp);   // argmin
       // 4. assignment on the chosen worker (Eq. 6 at assignment, A32)
       if (w == best) {
+        BP_CNT(22, 1);
         const uint32_t np = par ^ 1;   // flags written now are read after the next barrier
         if (x.wn >= p.ring) {
           if (lane == 0) {
@@ -1078,6 +1420,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
           const uint32_t pe = x.nfl + x.wn;
           if (pe > x.c[9]) x.c[9] = pe;
         }
+        BP_ACC(4, tp);   // assignment (incl. a dequeue into a free slot)
       }
     }
     if (!aborted) {
@@ -1161,6 +1504,21 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
 }  // namespace
 
 size_t batch_ctrl_bytes() { return align16(sizeof(BCtrl)); }
+
+cudaError_t batch_phase_cycles(unsigned long long* out32, int reset) {
+#ifdef KVR_PHASE_PROFILE
+  cudaError_t e = cudaMemcpyFromSymbol(out32, g_bphase, 32 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[32] = {0};
+    e = cudaMemcpyToSymbol(g_bphase, z, sizeof(z));
+  }
+  return e;
+#else
+  (void)out32;
+  (void)reset;
+  return cudaErrorNotSupported;
+#endif
+}
 
 template <typename Idx, int kFixedB>
 static const void* batch_kernel_t(uint32_t W) {

@@ -369,5 +369,6 @@ cudaError_t build_phases(const uint64_t* hash, uint64_t n, uint32_t B, uint32_t*
                          size_t scratch_bytes, cudaStream_t s, uint32_t* h_n_phases);
 // phase profiler (profiling build, -DKVR_PHASE_PROFILE); cudaErrorNotSupported otherwise
 cudaError_t phase_cycles(unsigned long long* out16, int reset);
+cudaError_t batch_phase_cycles(unsigned long long* out32, int reset);   // batching kernel
 
 }  // namespace kvr
