@@ -213,7 +213,11 @@ struct __align__(16) BCtrl {
   kvr_policy pol;
   // per-worker partials, combined in worker order at the end of the trial (A34)
   double P[kMaxW], F[kMaxW], slat[kMaxW], sttft[kMaxW], mlat[kMaxW];
+  // per-worker counters, accumulated by lane 0 of the worker's warp: probes, inserted,
+  // evictions, draws, resets, fallbacks, hit blocks, input blocks, queries, max pending,
+  // digest sum, victim-log overflow
   unsigned long long cnt[kMaxW][12];
+  unsigned long long vcur[kMaxW];   // next victim-log entry of the worker
   uint32_t hist[kMaxHistBins];
 };
 
@@ -222,17 +226,12 @@ struct BW {
   uint32_t size, cntT, nfl, wh, wn;
   uint32_t used;           // table entries that are live or tombstones
   uint32_t lhead, ltail;   // Leaf-LRU recency log cursors (first maybe-valid entry, end)
-  uint64_t e, k, vcur;
-  double Pt, th0, th1, th2, th3, P, F, slat, sttft, mlat;
-  // counters, u32 in registers and flushed into the worker's u64 accumulators in shared
-  // memory as soon as one of the sums reaches 2^31 (checked after every arrival and
-  // every completion; one event adds at most 65,536 to a counter, so none wraps):
-  // probes, inserted, evictions, draws, resets, fallbacks, hit blocks, input blocks,
-  // queries, max pending, (unused), victim-log overflow
-  uint32_t c[12];
-  uint64_t dsum;
+  uint64_t e, k;
+  double Pt, th0, th1, th2, th3;
   bool dead;   // admission failure / violation: stop this worker
 };
+// (the Eq. 2 load, last completion, latency / TTFT partial sums, counters and the
+// victim-log cursor live in the control block, updated by lane 0: fewer registers)
 
 struct BTrial {
   const ReplayParams* p;
@@ -247,9 +246,15 @@ struct BTrial {
   BFlight* ring;
   uint32_t ringcap;
   BCtrl* ctrl;
+  unsigned long long* cnt;   // ctrl->cnt[i]
   uint64_t* log;      // this worker's recency log (Leaf-LRU trials)
   uint32_t lmask;
 };
+
+// counter k of this worker += v (lane 0; call from warp-uniform code)
+__device__ __forceinline__ void cadd(const BTrial& T, int k, uint64_t v) {
+  if (T.lane == 0) T.cnt[k] += v;
+}
 
 // in-place order-preserving compaction of the recency log [head, tail): keeps the
 // entries whose stamp is still the node's (pinned or not); returns the new tail
@@ -355,23 +360,93 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
   uint32_t mw = lane < nw ? S.markb[lane] : 0u;
   uint32_t uw = 0, incl = 0, total = 0;
   bool dirty = true;
-  uint64_t rbatch = 0, rbase = 0;
-  bool rvalid = false;
+  // loop state in plain registers (written back to x at the end)
+  uint32_t cntT = x.cntT, size = x.size, nres = 0, nfb = 0;
+  uint64_t e = x.e;
+  const uint64_t e0 = x.e;
+  // draws for counters rbase .. rbase+31, lane l holds counter rbase + l (ri = next unused)
+  uint32_t rlo = 0, rhi = 0, ri = 32;
+  uint64_t rbase = 0;
   const uint32_t lmle = lane == 31 ? kFull : (2u << lane) - 1u;
   uint32_t nv = 0;
-  for (uint32_t d = d0; d < n; ++d) {
+  auto refill = [&]() {
+    rbase = e;
+    const uint64_t r = philox_r64(T.K, rbase + lane, T.i, 1);
+    rlo = (uint32_t)r;
+    rhi = (uint32_t)(r >> 32);
+    ri = 0;
+  };
+  uint32_t d = d0;
+  while (d < n) {
+    // ---- fast segment: evictions from U with no mark reset, no refill, U != {} ----
+    if (size == B && !dirty && total > 0 && ri < 32 && cntT < B) {
+      const uint32_t lim = min(n, min(d + (B - cntT), d + (32u - ri)));
+      const uint32_t d1 = d;
+#pragma unroll 1
+      for (; d < lim && total > 0; ++d) {
+        const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+        ++ri;
+        // floor(r64 * |U| / 2^64) (A6) with |U| < 2^32
+        const uint32_t idx = (uint32_t)(((uint64_t)dhi * total + __umulhi(dlo, total)) >> 32);
+        const uint32_t owner = __reduce_min_sync(kFull, incl > idx ? lane : 32u);
+        // speculative: lane l fetches the parent of slot owner*32+l, its child count and pin
+        uint32_t sp = (uint32_t)S.parent[owner * 32 + lane];
+        const bool sok = sp < B;
+        sp = sok ? sp : 0u;
+        const uint32_t snc = (uint32_t)S.nchild[sp];
+        const uint32_t spin = (uint32_t)S.pin[sp];
+        const uint32_t smw = __shfl_sync(kFull, mw, sp >> 5);
+        const uint32_t ou = __shfl_sync(kFull, uw, owner);
+        const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
+        const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
+        const uint32_t v = owner * 32 + bit;
+        const uint32_t pa = __shfl_sync(kFull, sp, bit);
+        const bool hasp = __shfl_sync(kFull, (uint32_t)sok, bit) != 0u;
+        const uint32_t nc = __shfl_sync(kFull, snc, bit) - 1u;
+        const uint32_t ppin = __shfl_sync(kFull, spin, bit);
+        const uint32_t pmw = __shfl_sync(kFull, smw, bit);
+        // U and LEAFU lose v (its slot is reloaded with t: pinned, marked); U gains pa iff
+        // pa became an unpinned unmarked leaf
+        if (lane == owner) {
+          uw &= ~(1u << bit);
+          lw &= ~(1u << bit);
+          mw |= 1u << bit;
+        }
+        if (lane >= owner) --incl;
+        --total;
+        if (hasp) {
+          S.nchild[pa] = (Idx)nc;   // uniform store (every lane read its value above)
+          if (nc == 0 && ppin == 0) {
+            const uint32_t pw = pa >> 5, pb = 1u << (pa & 31);
+            if (lane == pw) lw |= pb;
+            if (!(pmw & pb)) {   // pa != v (v is its child): the victim's MARK bit is irrelevant
+              if (lane == pw) uw |= pb;
+              if (lane >= pw) ++incl;
+              ++total;
+            }
+          }
+        }
+        if (lane == 0) S.gam[d] = (uint64_t)v | (1ull << 32);
+      }
+      const uint32_t k = d - d1;
+      cntT += k;   // t marked at each step, no reset inside the segment
+      e += k;
+      nv += k;
+      continue;
+    }
+    // ---- general step: one block ----
     // Alg. 1 l.6-9: t is not cached, so not in T; the (B+1)-th distinct mark resets T
-    if (x.cntT + 1 == B + 1) {
+    if (cntT == B) {
       mw = 0u;
-      x.cntT = 1;
-      x.c[4]++;
+      cntT = 1;
+      ++nres;
       dirty = true;
     } else {
-      x.cntT++;
+      ++cntT;
     }
     uint32_t slot, ev = 0;
-    if (x.size < B) {
-      slot = x.size++;
+    if (size < B) {
+      slot = size++;
     } else {
       if (dirty) {
         uw = lw & ~mw;
@@ -379,32 +454,26 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
         dirty = false;
       }
       uint32_t v;
-      bool via_u = true;
       if (total == 0) {   // U = {} (A5)
-        x.c[5]++;
-        via_u = false;
+        ++nfb;
         dirty = true;
         bool draw = true;
-        uint32_t cw = lw, ci = 0, ct;
         if (fallback == KVR_RLT_EARLY_RESET) {
           mw = 0u;       // T <- {t}; t is loaded marked below
-          x.cntT = 1;
-          x.c[4]++;
+          cntT = 1;
+          ++nres;
         } else if (fallback == KVR_RLT_LRU_MARKED) {   // least (stamp, -depth) unpinned leaf
           draw = false;
         }
-        if (draw) {
-          ct = words_count(cw, lane, ci);
+        if (draw) {   // uniform over the unpinned leaves (marks cleared or ignored)
+          uint32_t ci = 0;
+          const uint32_t ct = words_count(lw, lane, ci);
           if (ct == 0) return false;   // every leaf is in flight
-          if (!rvalid || x.e - rbase >= 32) {
-            rvalid = true;
-            rbase = x.e;
-            rbatch = philox_r64(T.K, rbase + lane, T.i, 1);
-          }
-          const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
-          x.e++;
-          x.c[3]++;
-          v = words_select(cw, ci, (uint32_t)pick_index(r, ct), lane);
+          if (ri == 32) refill();
+          const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+          ++ri;
+          ++e;
+          v = words_select(lw, ci, (uint32_t)(((uint64_t)dhi * ct + __umulhi(dlo, ct)) >> 32), lane);
         } else {
           uint64_t best = ~0ull;
           uint32_t bits = lw;
@@ -419,7 +488,7 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
           if (best == ~0ull) return false;
           v = (uint32_t)(best & 0xffffu);
         }
-        if ((__shfl_sync(kFull, mw, v >> 5) >> (v & 31)) & 1u) x.cntT--;   // a marked victim leaves T
+        if ((__shfl_sync(kFull, mw, v >> 5) >> (v & 31)) & 1u) --cntT;   // a marked victim leaves T
         const uint32_t pa = S.parent[v];
         if (pa != BView<Idx>::NIL) {
           const uint32_t nc = S.nchild[pa] - 1u;
@@ -429,44 +498,24 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
         }
       } else {
         // Alg. 1 l.14-16: uniform over U in slot order (A6), counter e_i
-        if (!rvalid || x.e - rbase >= 32) {
-          rvalid = true;
-          rbase = x.e;
-          rbatch = philox_r64(T.K, rbase + lane, T.i, 1);
-        }
-        const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
-        x.e++;
-        x.c[3]++;
-        const uint32_t idx = (uint32_t)pick_index(r, total);
-        const uint32_t owner = __reduce_min_sync(kFull, incl > idx ? lane : 32u);
-        // speculative: lane l fetches the parent of slot owner*32+l, its child count and pin
-        const uint32_t ss = owner * 32 + lane;
-        uint32_t sp = ss < B ? (uint32_t)S.parent[ss] : BView<Idx>::NIL;
-        const bool sok = sp < B;
-        sp = sok ? sp : 0u;
-        const uint32_t snc = (uint32_t)S.nchild[sp];
-        const uint32_t spin = (uint32_t)S.pin[sp];
-        const uint32_t smw = __shfl_sync(kFull, mw, sp >> 5);
-        const uint32_t ou = __shfl_sync(kFull, uw, owner);
-        const uint32_t rem = idx - (__shfl_sync(kFull, incl, owner) - (uint32_t)__popc(ou));
-        const uint32_t bit = __reduce_min_sync(kFull, (uint32_t)__popc(ou & lmle) > rem ? lane : 32u);
-        v = owner * 32 + bit;
-        const uint32_t pa = __shfl_sync(kFull, sp, bit);
-        const bool hasp = __shfl_sync(kFull, (uint32_t)sok, bit) != 0u;
-        const uint32_t nc = __shfl_sync(kFull, snc, bit) - 1u;
-        const uint32_t ppin = __shfl_sync(kFull, spin, bit);
-        const uint32_t pmw = __shfl_sync(kFull, smw, bit);
-        // U loses v (the slot is reloaded with t: pinned, marked), gains pa iff pa became an
-        // unpinned unmarked leaf
-        if (lane == owner) uw &= ~(1u << bit);
-        if (lane >= owner) --incl;
+        if (ri == 32) refill();
+        const uint32_t dlo = __shfl_sync(kFull, rlo, ri), dhi = __shfl_sync(kFull, rhi, ri);
+        ++ri;
+        ++e;
+        const uint32_t idx = (uint32_t)(((uint64_t)dhi * total + __umulhi(dlo, total)) >> 32);
+        v = words_select(uw, incl, idx, lane);
+        const uint32_t pa = S.parent[v];
+        if (lane == (v >> 5)) uw &= ~(1u << (v & 31));
+        if (lane >= (v >> 5)) --incl;
         --total;
-        if (hasp) {
-          S.nchild[pa] = (Idx)nc;   // uniform store (every lane read its value above)
-          const uint32_t pw = pa >> 5, pb = 1u << (pa & 31);
-          if (nc == 0 && ppin == 0) {
+        if (pa != BView<Idx>::NIL) {
+          const uint32_t nc = S.nchild[pa] - 1u;
+          __syncwarp();
+          S.nchild[pa] = (Idx)nc;
+          if (nc == 0 && S.pin[pa] == 0) {
+            const uint32_t pw = pa >> 5, pb = 1u << (pa & 31);
             if (lane == pw) lw |= pb;
-            if (!(pmw & pb)) {   // pa != v (v is its child): the victim's MARK bit is irrelevant
+            if (!((__shfl_sync(kFull, mw, pw) >> (pa & 31)) & 1u)) {   // joins U
               if (lane == pw) uw |= pb;
               if (lane >= pw) ++incl;
               ++total;
@@ -474,27 +523,34 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
           }
         }
       }
-      (void)via_u;
-      // v leaves LEAFU and its MARK bit is replaced by t's
+      // v leaves LEAFU; its MARK bit is replaced by t's (below)
       if (lane == (v >> 5)) lw &= ~(1u << (v & 31));
       slot = v;
       ev = 1;
-      x.c[2]++;
       ++nv;
     }
     if (lane == (slot >> 5)) mw |= 1u << (slot & 31);   // t in T (Alg. 1 l.7)
     if (lane == 0) S.gam[d] = (uint64_t)slot | ((uint64_t)ev << 32);
-    x.c[1]++;
+    ++d;
   }
   if (lane < nw) {
     S.leafu[lane] = lw;
     S.markb[lane] = mw;
   }
+  cadd(T, 1, n - d0);          // loads
+  cadd(T, 2, nv);              // evictions
+  cadd(T, 3, e - e0);          // draws
+  cadd(T, 4, nres);
+  cadd(T, 5, nfb);
+  x.cntT = cntT;
+  x.size = size;
+  x.e = e;
   __syncwarp();
   // deferred, lane-parallel: victims' erases / digest terms / log entries (the k-th victim
   // of the update is the k-th evicting block), then the loads
   uint64_t V = 0;
-  uint32_t k0 = 0, cleared = 0, prev_last = prev0;
+  uint32_t k0 = 0, cleared = 0, prev_last = prev0, vfull = 0;
+  const uint64_t vc0 = T.ctrl->vcur[T.i];
   for (uint32_t b0 = d0; b0 < n; b0 += 32) {
     const uint32_t q = b0 + lane;
     const bool act = q < n;
@@ -509,8 +565,8 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
       cleared += t_erase(S, hv, slot);
       V ^= fmix64(hv ^ ((uint64_t)(k + 1) * kPosMul));
       if (T.vlog) {
-        if (x.vcur + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + x.vcur + k] = hv;
-        else x.c[11] = 1;
+        if (vc0 + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + vc0 + k] = hv;
+        else vfull = 1;
       }
     }
     k0 += __popc(evb);
@@ -532,10 +588,10 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
   }
   if (prev0 != kNone && lane == 0) S.nchild[prev0] = (Idx)(S.nchild[prev0] + 1);   // prev0 is pinned
   x.used -= __reduce_add_sync(kFull, cleared);
-  x.c[11] = __reduce_or_sync(kFull, x.c[11]);
+  if (__any_sync(kFull, vfull != 0u) && lane == 0) T.cnt[11] = 1;
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
-  x.vcur += nv;
+  if (lane == 0) T.ctrl->vcur[T.i] = vc0 + nv;
   __syncwarp();
   *nvict += nv;
   *Vout ^= V;
@@ -692,6 +748,8 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     // LEAFU / MARK bitmaps serve RLT only).
     const uint32_t M = n - d, nfree = min(M, B - x.size);
     d_ins0 = d;
+    const uint64_t vc0 = T.ctrl->vcur[T.i];
+    uint32_t vfull = 0;
     for (uint32_t cb = 0; cb < M; cb += 32) {
       const uint32_t q = cb + lane;
       const bool act = q < M;
@@ -708,8 +766,8 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
         const uint64_t k = nv + (q - max(cb, nfree));   // index of this victim in the update
         V ^= fmix64(hv ^ ((k + 1) * kPosMul));
         if (T.vlog) {
-          if (x.vcur + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + x.vcur + k] = hv;
-          else x.c[11] = 1;
+          if (vc0 + k < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + vc0 + k] = hv;
+          else vfull = 1;
         }
       }
       __syncwarp();
@@ -730,10 +788,11 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       nv += ne;
       __syncwarp();
     }
-    x.c[11] = __reduce_or_sync(kFull, x.c[11]);
-    x.c[1] += M;
-    x.c[2] += nv;
-    x.vcur += nv;
+    if (__any_sync(kFull, vfull != 0u) && lane == 0) T.cnt[11] = 1;
+    cadd(T, 1, M);
+    cadd(T, 2, nv);
+    if (lane == 0) T.ctrl->vcur[T.i] = vc0 + nv;
+    __syncwarp();
     x.size += nfree;
 #pragma unroll
     for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
@@ -755,7 +814,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
           for (uint32_t w = lane; w < T.nwords; w += 32) S.markb[w] = 0;
           __syncwarp();
           x.cntT = 1;
-          x.c[4]++;
+          cadd(T, 4, 1);
           nU_known = -1;
         } else {
           x.cntT++;
@@ -808,14 +867,14 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
           nU = cand_count(S, T, true);
         }
         if (nU == 0) {   // A5: U empty
-          x.c[5]++;
+          cadd(T, 5, 1);
           mark_ok = false;
           nU_known = -1;
           if (pol.rlt_fallback == KVR_RLT_EARLY_RESET) {
             for (uint32_t w = lane; w < T.nwords; w += 32) S.markb[w] = 0;
             __syncwarp();
             x.cntT = 1;    // T <- {t}; t is loaded marked below
-            x.c[4]++;
+            cadd(T, 4, 1);
           } else if (pol.rlt_fallback == KVR_RLT_LRU_MARKED) {
             use_lru = true;
           }
@@ -830,7 +889,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
           }
           const uint64_t r = __shfl_sync(kFull, rbatch, (int)(x.e - rbase));
           x.e++;
-          x.c[3]++;
+          cadd(T, 3, 1);
           const uint32_t idx = (uint32_t)pick_index(r, nU);
           if (mark_ok && regu) {
             // owner word: first lane whose inclusive count exceeds idx; the bit inside
@@ -898,16 +957,17 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       }
       x.used -= __shfl_sync(kFull, clr, 0);
       __syncwarp();
-      x.c[2]++;
+      cadd(T, 2, 1);
       V ^= fmix64(hv ^ ((uint64_t)(nv + 1) * kPosMul));
-      if (T.vlog) {
-        if (x.vcur < T.vshare) {
-          if (lane == 0) T.vlog[(uint64_t)T.i * T.vshare + x.vcur] = hv;
-        } else {
-          x.c[11] = 1;
+      if (lane == 0) {
+        const uint64_t vc = T.ctrl->vcur[T.i];
+        if (T.vlog) {
+          if (vc < T.vshare) T.vlog[(uint64_t)T.i * T.vshare + vc] = hv;
+          else T.cnt[11] = 1;
         }
+        T.ctrl->vcur[T.i] = vc + 1;
       }
-      x.vcur++;
+      __syncwarp();
       nv++;
       slot = v;
     } else {
@@ -927,7 +987,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
       if (prev != kNone) S.nchild[prev] = (Idx)(S.nchild[prev] + 1);   // prev is pinned: never in LEAFU
     }
     __syncwarp();
-    x.c[1]++;
+    cadd(T, 1, 1);
     prev = slot;
   }
   if (d < n) {   // RLT misses with register-resident LEAFU / MARK words (B <= 1024)
@@ -996,20 +1056,24 @@ __device__ __forceinline__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, 
   }
   __syncwarp();
   x.nfl++;
-  if (comp > x.F) x.F = comp;
-  x.P = x.P + cost;                                                           // Eq. 2
-  x.c[6] += m;        // hit blocks   (x bt at the end)
-  x.c[7] += n_in;     // input blocks (x bt at the end)
-  x.slat = x.slat + lat;
-  x.sttft = x.sttft + ttft;
-  if (lat > x.mlat) x.mlat = lat;
-  x.c[8]++;
+  if (lane == 0) {
+    BCtrl* c = T.ctrl;
+    const uint32_t i = T.i;
+    if (comp > c->F[i]) c->F[i] = comp;
+    c->P[i] = c->P[i] + cost;                                                 // Eq. 2
+    c->slat[i] = c->slat[i] + lat;
+    c->sttft[i] = c->sttft[i] + ttft;
+    if (lat > c->mlat[i]) c->mlat[i] = lat;
+    T.cnt[6] += m;      // hit blocks   (x bt at the end)
+    T.cnt[7] += n_in;   // input blocks (x bt at the end)
+    T.cnt[8] += 1;
+  }
   uint64_t Tj = fmix64(T.K ^ (uint64_t)j);
   Tj = fmix64(Tj ^ (uint64_t)T.i);
   Tj = fmix64(Tj ^ (uint64_t)m);
   Tj = fmix64(Tj ^ (uint64_t)nv);
   Tj = fmix64(Tj ^ V);
-  x.dsum += Tj;
+  if (lane == 0) T.cnt[10] += Tj;
   if (lane == 0) {
     if (T.rec) {
       kvr_query_record& R = T.rec[j];
@@ -1019,7 +1083,7 @@ __device__ __forceinline__ bool b_dequeue(const BTrial& T, const BView<Idx>& S, 
       R._pad = 0;
       R.ttft_ms = ttft;
       R.latency_ms = lat;
-      R.victim_offset = (uint64_t)T.i * T.vshare + (x.vcur - nv);
+      R.victim_offset = (uint64_t)T.i * T.vshare + (T.ctrl->vcur[T.i] - nv);
     }
     if (T.p->bins) atomicAdd(&T.ctrl->hist[hist_bin_b(lat, T.p->bins)], 1u);
   }
@@ -1121,19 +1185,6 @@ __device__ __forceinline__ bool b_complete(const BTrial& T, const BView<Idx>& S,
   return true;
 }
 
-// flush the u32 sum counters (0..8; 9 = max, 11 = flag) once one reaches 2^31
-__device__ __forceinline__ void b_flush(BW& x, unsigned long long* acc, uint32_t lane) {
-  uint32_t any = 0;
-#pragma unroll
-  for (int c = 0; c < 9; ++c) any |= x.c[c];
-  if (any & 0x80000000u) {
-    if (lane == 0)
-      for (int c = 0; c < 9; ++c) acc[c] += x.c[c];
-#pragma unroll
-    for (int c = 0; c < 9; ++c) x.c[c] = 0;
-  }
-}
-
 template <typename Idx>
 __device__ __forceinline__ uint32_t b_next(const BView<Idx>& S, const BW& x, double* c) {
   uint32_t b = kNone;
@@ -1231,14 +1282,20 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
     BW x;
     x.size = 0; x.cntT = 0; x.nfl = 0; x.wh = 0; x.wn = 0; x.used = 0;
     x.lhead = 0; x.ltail = 0;
-    x.e = 0; x.k = 0; x.vcur = 0;
-    x.Pt = 0.0; x.P = 0.0; x.F = 0.0; x.slat = 0.0; x.sttft = 0.0; x.mlat = 0.0;
+    x.e = 0; x.k = 0;
+    x.Pt = 0.0;
     x.th0 = pol.theta0[0]; x.th1 = pol.theta0[1]; x.th2 = pol.theta0[2]; x.th3 = pol.theta0[3];
-    for (int c = 0; c < 12; ++c) x.c[c] = 0;
-    x.dsum = 0;
     x.dead = false;
-    if (lane == 0)
+    if (lane == 0) {
       for (int c = 0; c < 12; ++c) ctrl->cnt[w][c] = 0;
+      ctrl->P[w] = 0.0;
+      ctrl->F[w] = 0.0;
+      ctrl->slat[w] = 0.0;
+      ctrl->sttft[w] = 0.0;
+      ctrl->mlat[w] = 0.0;
+      ctrl->vcur[w] = 0;
+    }
+    T.cnt = ctrl->cnt[w];
     if (!pol_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_POLICY;
     if (!tr_ok && tid == 0) ctrl->status = KVR_TRIAL_BAD_TRACE;
     const uint32_t Nrun = (pol_ok && tr_ok) ? N : 0;
@@ -1255,7 +1312,6 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       const double t = hq.arrival_ms;
       const uint32_t n_in = hq.n_in;
       const uint32_t q = T.bt * n_in;
-      b_flush(x, ctrl->cnt[w], lane);
       // 1. catch-up: ticks, completions and the dequeues they start, in time order (A31)
       if (!x.dead) {
         for (;;) {
@@ -1273,8 +1329,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
               x.dead = true;
               break;
             }
-            b_flush(x, ctrl->cnt[w], lane);
-            continue;
+                  continue;
           }
           break;
         }
@@ -1298,7 +1353,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
         m = b0 + 32;
       }
       if (m > n_in) m = n_in;
-      x.c[0] += (m + 1 < n_in) ? m + 1 : n_in;
+      cadd(T, 0, (m + 1 < n_in) ? m + 1 : n_in);
       const uint32_t pend = x.nfl + x.wn;
       double sc = 0.0;
       if (T.lbgr) {
@@ -1418,7 +1473,7 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
             x.wn++;
           }
           const uint32_t pe = x.nfl + x.wn;
-          if (pe > x.c[9]) x.c[9] = pe;
+          if (lane == 0 && pe > ctrl->cnt[w][9]) ctrl->cnt[w][9] = pe;
         }
         BP_ACC(4, tp);   // assignment (incl. a dequeue into a free slot)
       }
@@ -1438,21 +1493,11 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
           if (lane == 0) atomicCAS(&ctrl->status, 0u, (uint32_t)KVR_TRIAL_ADMISSION);
           break;
         }
-        b_flush(x, ctrl->cnt[w], lane);
       }
     }
     if (lane == 0) {
-      ctrl->P[w] = x.P;
-      ctrl->F[w] = x.F;
-      ctrl->slat[w] = x.slat;
-      ctrl->sttft[w] = x.sttft;
-      ctrl->mlat[w] = x.mlat;
-      for (int c = 0; c < 9; ++c) ctrl->cnt[w][c] += x.c[c];
       ctrl->cnt[w][6] *= T.bt;     // hit / input blocks -> tokens
       ctrl->cnt[w][7] *= T.bt;
-      ctrl->cnt[w][9] = x.c[9];
-      ctrl->cnt[w][10] = x.dsum;
-      ctrl->cnt[w][11] = x.c[11];
     }
     __syncthreads();
     if (tid == 0) {

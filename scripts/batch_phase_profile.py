@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2601_18999_b200 import build  # noqa: E402
 
-os.environ["KVR_LIB"] = build.build(profile=True)
+os.environ["KVR_LIB"] = os.environ.get("KVR_PROF_LIB") or build.build(profile=True)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
