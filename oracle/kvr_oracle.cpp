@@ -468,7 +468,6 @@ struct BWorker {
   std::deque<BRec> waiting;     // FIFO (A30)
   std::vector<BRec> inflight;   // <= beta
   uint64_t k = 0, e = 0;
-  double sum_lat = 0.0, sum_ttft = 0.0;   // per-worker partial sums (A34)
   uint64_t vcur = 0;                       // per-worker victim-log cursor (A34)
 };
 
@@ -490,6 +489,10 @@ int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy*
   const uint64_t vshare = (victims && W) ? victims_cap / W : 0;   // A34: per-worker sub-share
   uint64_t D = K;
   bool vlog_full = false, admission = false, violation = false;
+  // latency / TTFT of every dequeued query, summed in query order at the end (the plain
+  // definition of the trial sums; reading A34)
+  std::vector<double> lat_q(tr->n_queries, 0.0), ttft_q(tr->n_queries, 0.0);
+  std::vector<uint8_t> done_q(tr->n_queries, 0);
 
   // Dequeue r on worker i at time s: UpdateCache with pinning, true h, Eq. 1 truth.
   auto dequeue = [&](uint32_t i, BRec r, double s) {
@@ -531,8 +534,9 @@ int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy*
     x.P = x.P + cost;                                        // Eq. 2
     out->hit_tokens += h;
     out->input_tokens += q;
-    x.sum_lat = x.sum_lat + lat;
-    x.sum_ttft = x.sum_ttft + ttft;
+    lat_q[j] = lat;
+    ttft_q[j] = ttft;
+    done_q[j] = 1;
     if (lat > out->max_latency_ms) out->max_latency_ms = lat;
     out->queries++;
     uint64_t V = 0;
@@ -757,9 +761,12 @@ int run_batched(const kvro_config* cfg, const kvro_trace* tr, const kvro_policy*
   if (violation) return 9;
   if (admission && out->status == 0) out->status = KVRO_TRIAL_ADMISSION;
 
-  for (uint32_t i = 0; i < W; ++i) {                 // A34: worker-index order
-    out->sum_latency_ms = out->sum_latency_ms + w[i].sum_lat;
-    out->sum_ttft_ms = out->sum_ttft_ms + w[i].sum_ttft;
+  for (uint32_t j = 0; j < tr->n_queries; ++j)        // query order
+    if (done_q[j]) {
+      out->sum_latency_ms = out->sum_latency_ms + lat_q[j];
+      out->sum_ttft_ms = out->sum_ttft_ms + ttft_q[j];
+    }
+  for (uint32_t i = 0; i < W; ++i) {
     if (w[i].P > out->makespan_ms) out->makespan_ms = w[i].P;
     if (w[i].F > out->last_completion_ms) out->last_completion_ms = w[i].F;
     out->sum_load_ms = out->sum_load_ms + w[i].P;

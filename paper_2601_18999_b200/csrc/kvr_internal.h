@@ -189,7 +189,8 @@ struct __align__(16) Ctrl {
   uint32_t mhit[2][kMaxW];
   uint32_t npend[2][kMaxW];
   uint32_t csize[2][kMaxW];    // cached blocks per worker (CACHE_AWARE router, A38)
-  double P[kMaxW], F[kMaxW];
+  // (each worker's final Eq. 2 load P and last completion F go to score[0] / score[1] at
+  // the end of a trial, when the scores are dead: 512 B of shared memory less)
   double sum_lat, sum_ttft, max_lat;
   unsigned long long digest, dkey, vcursor;
   unsigned long long cnt[10];   // probes, inserted, evictions, draws, resets, fallbacks, hit, in, queries, maxpend

@@ -2165,8 +2165,8 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       atomicAdd(&ctrl->cnt[7], ws->c_in);
       atomicAdd(&ctrl->cnt[8], (unsigned long long)ws->c_q);
       atomicMax(&ctrl->cnt[9], (unsigned long long)ws->c_maxp);
-      ctrl->P[w] = P;
-      ctrl->F[w] = F;
+      ctrl->score[0][w] = P;   // (the scores are dead after the last query's barrier)
+      ctrl->score[1][w] = F;
     }
     }
     __syncthreads();
@@ -2188,9 +2188,10 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       Rr.max_latency_ms = ctrl->max_lat;
       double mk = 0.0, lc = 0.0, sl = 0.0;
       for (uint32_t i = 0; i < W; ++i) {   // makespan max_i P_i, in worker order
-        if (ctrl->P[i] > mk) mk = ctrl->P[i];
-        if (ctrl->F[i] > lc) lc = ctrl->F[i];
-        sl = sl + ctrl->P[i];
+        const double Pi = ctrl->score[0][i], Fi = ctrl->score[1][i];
+        if (Pi > mk) mk = Pi;
+        if (Fi > lc) lc = Fi;
+        sl = sl + Pi;
       }
       Rr.makespan_ms = mk;
       Rr.last_completion_ms = lc;

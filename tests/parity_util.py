@@ -48,13 +48,23 @@ def run_gpu(kvr, traces, W, B, pols, keys, truth, ring, record, victims_cap, for
     return out, dts, sim
 
 
-def assert_result_equal(g, o, ctx=""):
+# the batching engine sums latency / TTFT per worker and adds the partial sums in
+# worker order (kvr_batch.cu); the oracle sums them in query order (the plain
+# definition).  The north star bounds those aggregates at 1e-12 relative.
+BATCH_SUM_FIELDS = ("sum_latency_ms", "sum_ttft_ms")
+REL_TOL = 1e-12
+
+
+def assert_result_equal(g, o, ctx="", rel_fields=()):
     for f in INT_FIELDS:
         assert int(g[f]) == int(o[f]), f"{ctx} field {f}: gpu {int(g[f])} oracle {int(o[f])}"
     for f in FP_FIELDS:
         gv, ov = float(g[f]), float(o[f])
         rel = abs(gv - ov) / max(abs(ov), 1e-300)
-        assert gv == ov, f"{ctx} field {f}: gpu {gv!r} oracle {ov!r} rel {rel:.3e}"
+        if f in rel_fields:
+            assert gv == ov or rel <= REL_TOL, f"{ctx} field {f}: gpu {gv!r} oracle {ov!r} rel {rel:.3e}"
+        else:
+            assert gv == ov, f"{ctx} field {f}: gpu {gv!r} oracle {ov!r} rel {rel:.3e}"
 
 
 def assert_records_equal(grec, orec, n, ctx=""):
@@ -126,7 +136,7 @@ def compare_batched(oracle, kvr, tr, W, B, beta, pols, keys, truth=(0.0, 1.0, 20
         if o.result["status"] not in (0, 2) or int(g["status"]) not in (0, 2):
             assert int(g["status"]) == o.result["status"], ctx
             continue
-        assert_result_equal(g, o.result, ctx)
+        assert_result_equal(g, o.result, ctx, rel_fields=BATCH_SUM_FIELDS)
         if record:
             assert_records_equal(out.records[t], o.records, n, ctx)
             gv = out.victims[t * victims_cap:(t + 1) * victims_cap]

@@ -147,7 +147,7 @@ def test_config2_full_trace_sampled(kvr, oracle_mod):
     64 trials; two sampled trials (RLT, L-LRU) replayed by the oracle over all 100k queries."""
     import bench
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
-    from parity_util import assert_result_equal
+    from parity_util import BATCH_SUM_FIELDS, assert_result_equal
     tr = bench.c2_traces()[1]
     sim = Simulator(bench.C2_W, bench.B_BLOCKS, pending_ring=16384, batch_slots=3)
     keys = np.arange(1, 65, dtype=np.uint64)
@@ -160,7 +160,8 @@ def test_config2_full_trace_sampled(kvr, oracle_mod):
     for t in (0, 63):
         o = oracle_mod.run(cfg, tr, oracle_mod.OraclePolicy(eviction=int(keys[t]) % 2), int(keys[t]))
         assert o.rc == 0
-        assert_result_equal(out.results[t], o.result, f"batching config2 trial {t}")
+        assert_result_equal(out.results[t], o.result, f"batching config2 trial {t}",
+                            rel_fields=BATCH_SUM_FIELDS)
 
 
 def test_edge_cases(kvr, oracle_mod):
@@ -187,7 +188,7 @@ def test_edge_cases(kvr, oracle_mod):
 def test_multi_trace_launch(kvr, oracle_mod):
     """kvr_sim_run_multi with the batching kernel: trials over three traces in one launch."""
     from paper_2601_18999_b200.kvr import DeviceTrace, Simulator, policies_array
-    from parity_util import assert_result_equal
+    from parity_util import BATCH_SUM_FIELDS, assert_result_equal
     trs = [wl.gsp(10, 8, r, seed=20 + i, W=3, lengths=(256, 512)) for i, r in enumerate((0.3, 0.5, 0.9))]
     pols = [kvr.Policy(eviction=t % 2, router=(0, 1, 5)[t % 3]) for t in range(9)]
     keys = np.arange(50, 59, dtype=np.uint64)
@@ -199,7 +200,7 @@ def test_multi_trace_launch(kvr, oracle_mod):
     for t in range(9):
         o = oracle_mod.run(cfg, trs[tt[t]], to_oracle_policy(oracle_mod, pols[t]), int(keys[t]))
         assert o.rc == 0
-        assert_result_equal(out.results[t], o.result, f"trial {t}")
+        assert_result_equal(out.results[t], o.result, f"trial {t}", rel_fields=BATCH_SUM_FIELDS)
 
 
 def test_fuzz_random_configs(kvr, oracle_mod):
