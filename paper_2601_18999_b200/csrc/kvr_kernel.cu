@@ -212,6 +212,59 @@ __device__ __forceinline__ void tbl_rebuild(const WorkerView<Idx>& S, uint32_t T
   __syncwarp();
 }
 
+// One 32-block window of a longest-cached-prefix match: lane l looks up block base + l
+// (blocks >= nq count as misses).  Membership = on the path Hp[0..npp) at the same depth,
+// or in the table and, with ovl, not among the pending update's victims (bitmap vbits,
+// lane l: word l).  The lanes step their probe chains together and the warp stops as soon
+// as the prefix is decided -- the first lane that is not a hit has finished with a miss --
+// instead of waiting for the longest chain of the window (most workers miss the first
+// block).  Returns the hit ballot, exact up to its first zero bit.
+template <typename Idx>
+__device__ __forceinline__ uint32_t probe_window(const WorkerView<Idx>& S, uint32_t mask, const uint64_t* Hq,
+                                                 uint32_t base, uint32_t nq, const uint64_t* Hp,
+                                                 uint32_t npp, bool ovl, uint32_t vbits, uint32_t lane) {
+  const uint32_t d = base + lane;
+  bool done = true, hit = false;
+  uint64_t hh = 0;
+  uint32_t pos = 0;
+  if (d < nq) {
+    hh = Hq[d];
+    if (d < npp && Hp[d] == hh) {
+      hit = true;
+    } else {
+      done = false;
+      pos = (uint32_t)hh & mask;
+    }
+  }
+#pragma unroll 1
+  for (;;) {
+    bool fin = false;
+    uint32_t sidx = 0;
+    if (!done) {
+      const Idx e = S.table[pos];
+      if (e == Nil<Idx>::empty) {
+        done = true;
+      } else if (e != Nil<Idx>::tomb && S.key[e] == hh) {
+        done = true;
+        fin = true;
+        hit = true;
+        sidx = (uint32_t)e;
+      } else {
+        pos = (pos + 1) & mask;
+      }
+    }
+    if (ovl) {   // found in the old table but evicted by the pending update?
+      const uint32_t vw = __shfl_sync(kFull, vbits, fin ? (sidx >> 5) : 0u);
+      if (fin && ((vw >> (sidx & 31)) & 1u)) hit = false;
+    }
+    const uint32_t dn = __ballot_sync(kFull, done);
+    const uint32_t hb = __ballot_sync(kFull, done && hit);
+    if (hb == kFull || dn == kFull) return hb;
+    const uint32_t k = __ffs(~hb) - 1;   // first lane not (yet) known to hit
+    if ((dn >> k) & 1u) return hb;       // ... and it finished with a miss
+  }
+}
+
 __device__ __forceinline__ uint32_t hist_bin(double lat, uint32_t bins) {
   if (!(lat >= 1.0)) return 0;
   int e;
@@ -1593,25 +1646,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
             uint32_t mx = 0;
     #pragma unroll 1
             for (uint32_t base = 0; base < nq_in; base += 32) {
-              const uint32_t d = base + lane;
-              bool hit = false, check = false;
-              uint32_t sidx = 0;
-              if (d < nq_in) {
-                const uint64_t hh = Hq[d];
-                if (d < npp && Hp[d] == hh) {
-                  hit = true;
-                } else {
-                  const Idx s = tbl_find<Idx>(V, tmask, hh);
-                  hit = s != NIL;
-                  check = ovl && hit;
-                  sidx = (uint32_t)s;
-                }
-              }
-              if (ovl) {   // found in the old table but evicted by the pending update?
-                const uint32_t vw = __shfl_sync(kFull, vbits, check ? (sidx >> 5) : 0u);
-                if (check && ((vw >> (sidx & 31)) & 1u)) hit = false;
-              }
-              const uint32_t bal = __ballot_sync(kFull, hit);
+              const uint32_t bal = probe_window<Idx>(V, tmask, Hq, base, nq_in, Hp, npp, ovl, vbits, lane);
               if (bal == kFull) {
                 mx = base + 32;
                 continue;
@@ -1885,10 +1920,7 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       if (m == n_in) {
 #pragma unroll 1
         for (uint32_t base = n_in; base < n; base += 32) {
-          const uint32_t d = base + lane;
-          bool hit = false;
-          if (d < n) hit = tbl_find<Idx>(S, tmask, H[d]) != NIL;
-          const uint32_t bal = __ballot_sync(kFull, hit);
+          const uint32_t bal = probe_window<Idx>(S, tmask, H, base, n, nullptr, 0u, false, 0u, lane);
           if (bal == kFull) {
             kf = base + 32;
             continue;
