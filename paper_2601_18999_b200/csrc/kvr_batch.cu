@@ -137,6 +137,40 @@ __device__ __forceinline__ uint32_t t_find(const BView<Idx>& S, uint64_t t) {
     i = (i + 1) & S.tmask;
   }
 }
+// One 32-block window of a prefix match (lane l: block base + l; blocks >= nq miss): the
+// lanes step their probe chains together and the warp stops once the prefix is decided
+// -- the first lane that is not a hit has finished with a miss -- instead of waiting for
+// the window's longest chain.  Returns the hit ballot, exact up to its first zero bit;
+// slot = the lane's slot when it is a known hit, else kNone.
+template <typename Idx>
+__device__ __forceinline__ uint32_t b_probe_window(const BView<Idx>& S, const uint64_t* H, uint32_t base,
+                                                   uint32_t nq, uint32_t lane, uint32_t& slot) {
+  const uint32_t d = base + lane;
+  bool done = d >= nq, hit = false;
+  const uint64_t t = done ? 0ull : H[d];
+  uint32_t i = (uint32_t)t & S.tmask;
+  slot = kNone;
+  for (;;) {
+    if (!done) {
+      const uint32_t s = S.table[i];
+      if (s == BView<Idx>::NIL) {
+        done = true;
+      } else if (s != BView<Idx>::TOMB && S.key[s] == t) {
+        done = true;
+        hit = true;
+        slot = s;
+      } else {
+        i = (i + 1) & S.tmask;
+      }
+    }
+    const uint32_t dn = __ballot_sync(kFull, done);
+    const uint32_t hb = __ballot_sync(kFull, done && hit);
+    if (hb == kFull || dn == kFull) return hb;
+    const uint32_t k = __ffs(~hb) - 1;   // first lane not (yet) known to hit
+    if ((dn >> k) & 1u) return hb;       // ... and it finished with a miss
+  }
+}
+
 // warp-cooperative insert of (t, slot) for the active lanes, no atomics: each round every
 // pending lane reads its probe position; among the lanes that found the same free entry
 // (EMPTY or tombstone) the lowest one takes it, the others move on.  Returns the number of
@@ -699,8 +733,8 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
   BP_T0(tu);
   while (d < n) {
     const uint32_t q = d + lane;
-    const uint32_t sl = q < n ? t_find(S, S.gam[q]) : kNone;
-    const uint32_t hb = __ballot_sync(kFull, sl != kNone);
+    uint32_t sl;
+    const uint32_t hb = b_probe_window(S, S.gam, d, n, lane, sl);
     const uint32_t hc = (~hb) ? (uint32_t)(__ffs(~hb) - 1) : 32u;   // leading hits of this step
     const bool hit = lane < hc;
     if (T.rlt) {
@@ -1343,9 +1377,8 @@ __global__ void __launch_bounds__(kMaxThreads, BMinBlocks<kMaxThreads>::value)
       const uint64_t* Hj = T.tr.hash + hq.block_off;
       uint32_t m = 0;
       for (uint32_t b0 = 0; b0 < n_in; b0 += 32) {
-        const uint32_t d = b0 + lane;
-        const bool hit = d < n_in && t_find(S, Hj[d]) != kNone;
-        const uint32_t bal = __ballot_sync(kFull, hit);
+        uint32_t sl;
+        const uint32_t bal = b_probe_window(S, Hj, b0, n_in, lane, sl);
         if (bal != kFull) {
           m = b0 + __ffs(~bal) - 1;
           break;
