@@ -1,7 +1,7 @@
 """Small replays of both kernels for compute-sanitizer (memcheck / racecheck /
 synccheck): the beta = 1 replay kernel (both tiers, lean and extended
 instantiations, every eviction/fallback and router) and the continuous-batching
-kernel (both tiers).  usage: compute-sanitizer --tool X python scripts/sanitize_case.py
+kernel (both tiers), and the split tier at W = 20.  usage: compute-sanitizer --tool X python scripts/sanitize_case.py
 """
 import os
 import sys
@@ -29,3 +29,9 @@ for ft in (1, 2):
     simb = Simulator(4, B, batch_slots=3, force_tier=ft, record_trials=len(pols), latency_hist_bins=16)
     out = simb.run(dt, keys, policies_array(pols), victims_cap=len(pols) * 4 * tr.total_blocks)
     print("batch tier", ft, out.results["status"], out.results["evictions"])
+# the split tier (W > 16: identities / tables in global memory, two workers per warp)
+tr20 = wl.random_tree(60, 5, max_len=40, alphabet=2, max_out=2, W=20, util=2.0)
+dt20 = DeviceTrace(tr20)
+sim20 = Simulator(20, 3 * int(tr20.max_blocks), force_tier=3, record_trials=len(pols), latency_hist_bins=16)
+out = sim20.run(dt20, keys, policies_array(pols), victims_cap=len(pols) * tr20.total_blocks)
+print("replay split tier W=20", out.results["status"], out.results["evictions"])
