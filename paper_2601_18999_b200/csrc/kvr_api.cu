@@ -593,8 +593,8 @@ kvr_status kvr_sim_run(kvr_sim* sim, const kvr_trace* trace, uint32_t n_trials,
 /* profiling builds only (not declared in kvr.h): per-phase cycle sums */
 kvr_status kvr_debug_phase_cycles(uint64_t* out32, int reset) {
   // reset 3 / 4: the batching kernel's counters (read / read and clear)
-  cudaError_t e = reset >= 3 ? kvr::batch_phase_cycles((unsigned long long*)out32, reset - 3)
-                             : kvr::phase_cycles((unsigned long long*)out32, reset);
+  cudaError_t e = (reset == 3 || reset == 4) ? kvr::batch_phase_cycles((unsigned long long*)out32, reset - 3)
+                                             : kvr::phase_cycles((unsigned long long*)out32, reset);
   if (e != cudaSuccess) return cuda_fail(e, "phase profile");
   return KVR_OK;
 }

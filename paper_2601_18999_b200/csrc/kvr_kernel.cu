@@ -36,6 +36,13 @@
 
 namespace kvr {
 
+#ifdef KVR_WHO_LAST
+// experiment build: which warp arrives last at the per-query barrier, by role
+// (0: updated the previous query's chosen worker, 1: ran a deferred apply after the
+// previous barrier, 2: scoring only); [4..6] the last arrival's lead over the second last
+__device__ unsigned long long g_who[8];
+__shared__ uint32_t s_arrive[32], s_role[32];
+#endif
 #ifdef KVR_PHASE_PROFILE
 // Phase profiler (profiling build only): cycles per phase summed over warps.
 __device__ unsigned long long g_phase_cycles[32];
@@ -159,7 +166,8 @@ __device__ __forceinline__ uint32_t tbl_erase(const WorkerView<Idx>& S, uint32_t
   return clear ? 1u : 0u;
 }
 
-// claim position pos if it is EMPTY or TOMB (CAS); returns 1 if it was EMPTY
+// claim position pos if it is EMPTY or TOMB (CAS); returns 1 if it was EMPTY.  (Starting
+// the CAS from a guessed all-EMPTY word instead of a load measured 3 % slower at W = 32.)
 __device__ __forceinline__ uint32_t tbl_claim_at(uint16_t* table, uint32_t pos, uint16_t slot,
                                                  bool* ok) {
   uint32_t* w32 = reinterpret_cast<uint32_t*>(table) + (pos >> 1);
@@ -1174,6 +1182,9 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   KVR_ACC(24, t_ap);   // rebuilds
 #pragma unroll
   for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  // (two workers per warp: another warp may be waiting to score this worker; every lane's
+  // table / slot writes are made visible before lane 0 clears `active`)
+  __threadfence_block();
   __syncwarp();   // every lane's reads of ws->x.used / ws->active precede lane 0's writes
   if (lane == 0) {
     // decision digest: D += T_j, order-independent across queries
@@ -1460,6 +1471,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
     // (identical in every warp)
     constexpr uint32_t kL = kV > 1 ? 3u : 1u;   // workers a warp may score in one query
     uint32_t pb = 0xffffffffu, pcw = 0xffffffffu;
+#ifdef KVR_WHO_LAST
+    uint32_t my_role = 2;
+#endif
 
     const double pol_inv_dt = 1.0 / pol.delta_t_ms;
 #pragma unroll 1
@@ -1688,6 +1702,19 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           f1_o = h1;
           f2_o = h2;
         };
+        if constexpr (kV > 1) {
+          // two workers per warp: a worker whose last update was applied after the previous
+          // barrier by another warp (it was updated while moved) may still be in that
+          // apply -- wait for it to finish before reading its cache.  (pb, scored by the
+          // warp that updated it, legitimately has its apply pending: overlay below.)
+          if (w != pb) {
+            if (lane == 0)
+              while (*reinterpret_cast<volatile uint32_t*>(&ws->active)) {
+              }
+            __syncwarp();
+            __threadfence_block();
+          }
+        }
         // with a pending deferred apply, membership = path of that query or the old
         // table minus that update's victims
         const bool overlay = defer && ws->active;
@@ -1722,7 +1749,25 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         KVR_SAVE_WORKER();
       }
       KVR_RESET(tp);
+#ifdef KVR_WHO_LAST
+      if (lane == 0) {
+        s_arrive[wid] = (uint32_t)clock();
+        s_role[wid] = my_role;
+      }
+      my_role = 2;
+#endif
       __syncthreads();
+#ifdef KVR_WHO_LAST
+      if (tid == 0 && j > 2) {
+        uint32_t best_w = 0, t1 = 0, t2 = 0;
+        for (uint32_t w2 = 0; w2 < nwarps; ++w2) {
+          const uint32_t t = s_arrive[w2] - s_arrive[0] + 0x40000000u;   // wrap-safe offsets
+          if (t > t1) { t2 = t1; t1 = t; best_w = w2; } else if (t > t2) { t2 = t; }
+        }
+        atomicAdd(&g_who[s_role[best_w]], 1ull);
+        atomicAdd(&g_who[4 + s_role[best_w]], (unsigned long long)(t1 - t2));
+      }
+#endif
       KVR_ACC(4, tp);
       if (ctrl->abortf[par]) break;   // set by i* of query j-1 (written to the other parity)
       if (issued < Nrun) {
@@ -1805,6 +1850,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
           apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
           if constexpr (kV > 1) wsave(p, w)->vb[lane] = 0u;
           else st0.vbits = 0;
+#ifdef KVR_WHO_LAST
+          my_role = 1;
+#endif
         }
       }
       uint32_t vib = 0xffffffffu;   // position of the chosen worker in this warp's list
@@ -1841,6 +1889,9 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
       KVR_ACC(6, tp);
 
       if (vib == 0xffffffffu) continue;
+#ifdef KVR_WHO_LAST
+      my_role = 0;
+#endif
 
       // ================= warp i* : UpdateCache decisions + accounting =================
       uint32_t m = m_v[0];
@@ -2286,6 +2337,16 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
 }
 
 cudaError_t phase_cycles(unsigned long long* out16, int reset) {
+#ifdef KVR_WHO_LAST
+  if (reset >= 5) {   // who-arrives-last counters (reset 6: and clear)
+    cudaError_t e = cudaMemcpyFromSymbol(out16, g_who, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess && reset == 6) {
+      unsigned long long z[8] = {0};
+      e = cudaMemcpyToSymbol(g_who, z, sizeof(z));
+    }
+    return e;
+  }
+#endif
 #ifdef KVR_PHASE_PROFILE
   if (reset == 2)   // per-trial cycles (4096 entries)
     return cudaMemcpyFromSymbol(out16, g_trial_cycles, 4096 * sizeof(unsigned long long));
