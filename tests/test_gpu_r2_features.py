@@ -189,3 +189,31 @@ def test_split_tier_two_workers_per_warp(kvr, oracle_mod, W):
     ext = [kvr.Policy(eviction=1, router=6), kvr.Policy(eviction=0, tracker_lag=3),
            kvr.Policy(eviction=1, router=5), kvr.Policy(eviction=1, rlt_fallback=2)]
     compare(oracle_mod, kvr, tr, W, 512, ext, [70, 71, 72, 73], ring=tr.n_queries)
+
+
+def test_split_tier_full_wave_every_trial(kvr, oracle_mod):
+    """The two-workers-per-warp tier under a full resident wave and more: 200 trials (> 148
+    CTAs) of W = 32 at B = 512 on one prefix-sharing trace, RLT and L-LRU mixed, every
+    trial's result bytes equal to the oracle's.  Guards the cross-warp apply / score
+    ordering (a worker updated by a non-home warp is scored by its home warp only after
+    that apply finished): the race it replaced showed up only under concurrent trials."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2601_18999_b200.kvr import DeviceTrace, Policy, Simulator, policies_array
+    from parity_util import assert_result_equal, to_oracle_policy
+    W, B, n = 32, 512, 200
+    tr = wl.gsp(40, 40, 0.7, seed=0x5E1, W=W, util=0.8, lengths=(256, 512, 1024))
+    pols = [Policy(eviction=t % 2) for t in range(n)]
+    keys = np.arange(1, n + 1, dtype=np.uint64)
+    sim = Simulator(W, B, pending_ring=4096)
+    assert sim.plan(tr.max_blocks)[0] == 3   # the split tier
+    out = sim.run(DeviceTrace(tr), keys, policies_array(pols))
+    cfg = oracle_mod.OracleConfig(W=W, capacity_blocks=B, pending_ring=4096)
+
+    def one(t):
+        return oracle_mod.run(cfg, tr, to_oracle_policy(oracle_mod, pols[t]), int(keys[t]))
+
+    with ThreadPoolExecutor(max_workers=16) as ex:
+        orc = list(ex.map(one, range(n)))
+    for t, o in enumerate(orc):
+        assert o.rc == 0
+        assert_result_equal(out.results[t], o.result, f"W=32 split trial {t}")
