@@ -623,8 +623,7 @@ __device__ __forceinline__ bool b_rlt_misses(const BTrial& T, const BView<Idx>& 
   if (prev0 != kNone && lane == 0) S.nchild[prev0] = (Idx)(S.nchild[prev0] + 1);   // prev0 is pinned
   x.used -= __reduce_add_sync(kFull, cleared);
   if (__any_sync(kFull, vfull != 0u) && lane == 0) T.cnt[11] = 1;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  V = warp_xor64(V);
   if (lane == 0) T.ctrl->vcur[T.i] = vc0 + nv;
   __syncwarp();
   *nvict += nv;
@@ -828,8 +827,7 @@ __device__ __forceinline__ uint32_t b_update(const BTrial& T, const BView<Idx>& 
     if (lane == 0) T.ctrl->vcur[T.i] = vc0 + nv;
     __syncwarp();
     x.size += nfree;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+    V = warp_xor64(V);
     d = n;   // the serial loop below has nothing left
   }
   BP_ACC(11, tu);   // Leaf-LRU miss run (incl. take / erase)

@@ -97,6 +97,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       : "memory");
 }
 
+// XOR of a u64 over the warp: two uniform-datapath reductions (REDUX.XOR) instead of a
+// ten-shuffle butterfly
+__device__ __forceinline__ uint64_t warp_xor64(uint64_t v) {
+  const uint32_t lo = __reduce_xor_sync(kFull, (uint32_t)v), hi = __reduce_xor_sync(kFull, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

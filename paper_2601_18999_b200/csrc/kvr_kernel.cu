@@ -40,8 +40,18 @@ namespace kvr {
 // experiment build: which warp arrives last at the per-query barrier, by role
 // (0: updated the previous query's chosen worker, 1: ran a deferred apply after the
 // previous barrier, 2: scoring only); [4..6] the last arrival's lead over the second last
-__device__ unsigned long long g_who[8];
+__device__ unsigned long long g_who[16];   // [8..12] apply phases: erase, arrays, inserts, rebuild, tail
+#define KVR_WT(v) long long v = clock64()
+#define KVR_WA(i, v)                                                              \
+  do {                                                                            \
+    const long long _n = clock64();                                               \
+    if (lane == 0) atomicAdd(&g_who[i], (unsigned long long)(_n - (v)));          \
+    v = _n;                                                                       \
+  } while (0)
 __shared__ uint32_t s_arrive[32], s_role[32];
+#else
+#define KVR_WT(v) (void)0
+#define KVR_WA(i, v) (void)0
 #endif
 #ifdef KVR_PHASE_PROFILE
 // Phase profiler (profiling build only): cycles per phase summed over warps.
@@ -1115,6 +1125,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   uint64_t V = 0;
   uint32_t used_add = 0, used_sub = 0, prev_last = ws->p0;
   KVR_T0(t_ap);
+  KVR_WT(tw);
 #pragma unroll 1
   for (uint32_t cb = 0; cb < M; cb += 32) {
     const uint32_t cnt = min(32u, M - cb);
@@ -1151,6 +1162,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
       }
     }
     KVR_ACC(29, t_ap);   // erase (victims) incl. slot/identity loads
+    KVR_WA(8, tw);
     const uint32_t up = __shfl_up_sync(kFull, my_slot, 1);
     const uint32_t par_slot = lane == 0 ? prev_last : up;
     __syncwarp();
@@ -1167,12 +1179,14 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     }
     __syncwarp();
     KVR_ACC(30, t_ap);   // slot arrays, stamps, log entries
+    KVR_WA(9, tw);
     const uint32_t claimed = act ? tbl_insert<Idx>(S, tmask, t, (Idx)my_slot) : 0u;
     used_add += __popc(__ballot_sync(kFull, claimed != 0));
     used_sub += __popc(__ballot_sync(kFull, cleared != 0));
     prev_last = __shfl_sync(kFull, my_slot, cnt - 1);
     __syncwarp();
     KVR_ACC(31, t_ap);   // table inserts
+    KVR_WA(10, tw);
   }
   uint32_t used = ws->x.used + used_add - used_sub;   // live + tombstone table entries
   if (used > p.lay.rebuild_at) {
@@ -1180,8 +1194,8 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
     used = ws->x.size;
   }
   KVR_ACC(24, t_ap);   // rebuilds
-#pragma unroll
-  for (int o = 16; o; o >>= 1) V ^= __shfl_xor_sync(kFull, V, o);
+  KVR_WA(11, tw);
+  V = warp_xor64(V);
   // (two workers per warp: another warp may be waiting to score this worker; every lane's
   // table / slot writes are made visible before lane 0 clears `active`)
   __threadfence_block();
@@ -1212,6 +1226,7 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   }
   __syncwarp();
   KVR_ACC(23, t_ap);   // digest term, record
+  KVR_WA(12, tw);
 }
 
 // Scalar state of one worker in the query loop (see the kernel): FIFO head / count,
@@ -1847,11 +1862,18 @@ __global__ void __launch_bounds__(kMaxThreads, MinBlocks<kMaxThreads>::value)
         const uint32_t w = wl[vi];
         WarpSm* ws = warp_sm(p, w);
         if (ws->active) {
+#ifdef KVR_WHO_LAST
+          const long long ta0 = clock64();
+#endif
           apply_update<Idx, kMem, kMaxThreads, kExt>(p, lane, w, tree, use_list, lbgr_or_static, rec, vlog);
           if constexpr (kV > 1) wsave(p, w)->vb[lane] = 0u;
           else st0.vbits = 0;
 #ifdef KVR_WHO_LAST
           my_role = 1;
+          if (lane == 0) {
+            atomicAdd(&g_who[3], (unsigned long long)(clock64() - ta0));
+            atomicAdd(&g_who[7], 1ull);
+          }
 #endif
         }
       }
@@ -2339,9 +2361,9 @@ cudaError_t launch_replay(uint32_t tier, const ReplayParams& p, uint32_t grid, s
 cudaError_t phase_cycles(unsigned long long* out16, int reset) {
 #ifdef KVR_WHO_LAST
   if (reset >= 5) {   // who-arrives-last counters (reset 6: and clear)
-    cudaError_t e = cudaMemcpyFromSymbol(out16, g_who, 8 * sizeof(unsigned long long));
+    cudaError_t e = cudaMemcpyFromSymbol(out16, g_who, 16 * sizeof(unsigned long long));
     if (e == cudaSuccess && reset == 6) {
-      unsigned long long z[8] = {0};
+      unsigned long long z[16] = {0};
       e = cudaMemcpyToSymbol(g_who, z, sizeof(z));
     }
     return e;

@@ -17,7 +17,7 @@ from paper_2601_18999_b200 import kvr  # noqa: E402
 Ws = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else list(bench.C5_WS)
 L_ = kvr.lib()
 L_.kvr_debug_phase_cycles.argtypes = [C.c_void_p, C.c_int]
-buf = np.zeros(8, dtype=np.uint64)
+buf = np.zeros(16, dtype=np.uint64)
 for L in bench.c5_plan(0, 8):
     if L.W not in Ws:
         continue
@@ -30,4 +30,7 @@ for L in bench.c5_plan(0, 8):
     n = buf[:3].sum()
     names = ["updated prev chosen", "deferred apply", "scoring only"]
     print(f"W={L.W}: " + ", ".join(f"{names[i]} {100 * buf[i] / n:.1f} % (lead {buf[4 + i] / max(1, buf[i]):.0f} cyc)"
-                                  for i in range(3)))
+                                  for i in range(3)) +
+          f"; deferred apply {buf[3] / max(1, buf[7]):.0f} cycles on average ({int(buf[7])} applies): " +
+          ", ".join(f"{nm} {buf[8 + i] / max(1, buf[7]):.0f}" for i, nm in
+                    enumerate(["erase", "arrays/log", "inserts", "rebuild", "digest/record"])))
