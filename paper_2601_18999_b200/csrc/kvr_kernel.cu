@@ -1197,8 +1197,9 @@ __device__ __noinline__ void apply_update(const ReplayParams& p, uint32_t lane, 
   KVR_WA(11, tw);
   V = warp_xor64(V);
   // (two workers per warp: another warp may be waiting to score this worker; every lane's
-  // table / slot writes are made visible before lane 0 clears `active`)
-  __threadfence_block();
+  // table / slot writes are made visible before lane 0 clears `active`.  With one worker
+  // per warp only the worker's own warp ever reads them.)
+  if constexpr (kMem >= 2) __threadfence_block();
   __syncwarp();   // every lane's reads of ws->x.used / ws->active precede lane 0's writes
   if (lane == 0) {
     // decision digest: D += T_j, order-independent across queries
